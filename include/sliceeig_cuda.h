@@ -1,0 +1,206 @@
+/* sliceeig_cuda.h -- the C-ABI boundary of the B200-native polynomial-filtering hot path.
+ *
+ * libsliceeig_cuda.so (built from paper_1802_05215_b200/csrc) exports exactly the functions
+ * declared here: plain pointers and sizes, no C++ or torch types.  The C++ drop-in facade in
+ * include/sliceeig/*.hpp (namespace sliceeig, same names and signatures as the reference headers
+ * /root/reference/proj/include/sliceeig/*.hpp) is a thin inline layer over these calls, and the
+ * Python mirror (paper_1802_05215_b200/api.py) binds them with ctypes.
+ *
+ * Each entry point cites the reference interface it replaces (<header>:<line> under
+ * proj/include/sliceeig/, or tools/sliceeig_main.cpp:<line>).
+ *
+ * Error convention: every function returns SE_OK (0) or a negative code; se_last_error() gives the
+ * message of the last failure on the calling thread (the reference's exception text where one
+ * exists).  The facade maps SE_EINVAL -> std::invalid_argument, SE_ERANGE -> std::out_of_range,
+ * everything else -> std::runtime_error, matching the reference's exception types.
+ *
+ * Threading: one se_ctx per host thread (it owns a CUDA stream + cuBLAS/cuSOLVER handles).
+ * An se_csr is read-only after creation and may be shared by contexts on the same device.
+ * Host-only functions (no se_ctx argument) need no GPU.
+ */
+#ifndef SLICEEIG_CUDA_H
+#define SLICEEIG_CUDA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SE_API __attribute__((visibility("default")))
+#else
+#define SE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SE_OK 0
+#define SE_EINVAL (-1)   /* std::invalid_argument in the reference                     */
+#define SE_ENUMERIC (-2) /* std::runtime_error (numerical failure) in the reference     */
+#define SE_ECUDA (-3)    /* CUDA / cuBLAS / cuSOLVER failure                            */
+#define SE_ENOMEM (-4)   /* device allocation failure                                   */
+#define SE_ERANGE (-5)   /* std::out_of_range in the reference (csr.hpp:33)             */
+
+/* Damping kinds (filter_poly.hpp:15). */
+#define SE_DAMP_NONE 0
+#define SE_DAMP_SIGMA 1
+#define SE_DAMP_JACKSON 2
+
+/* KPM probe distributions.  Rademacher is the reference's (dos.hpp:97); Gaussian probes
+ * (Rng(seed).normal_vec(n) per probe, probe order) serve BASELINE config 2. */
+#define SE_PROBE_RADEMACHER 0
+#define SE_PROBE_GAUSSIAN 1
+
+typedef struct se_ctx se_ctx;
+typedef struct se_csr se_csr;
+typedef struct se_results se_results;
+
+/* PolynomialFilter (filter_poly.hpp:81-91) + its SpectralMap (filter_poly.hpp:17-27).
+ * mu is caller-owned storage of capacity mu_cap (>= k+1). */
+typedef struct se_poly_filter {
+  int k;
+  double gamma;
+  double c, d; /* map: t = (lambda - c) / d */
+  double tau;
+  double ta, tb;
+  double bar;
+  int damping;
+  int cap_reached;
+  double* mu;
+  int mu_cap;
+} se_poly_filter;
+
+/* SolverConfig (eigensolvers.hpp:46-54); zeros select the reference defaults
+ * (resolve_config eigensolvers.hpp:142-151). */
+typedef struct se_solver_cfg {
+  int m;
+  long max_its;
+  int ncycle;
+  double tau1;
+  double res_tol;
+  int est_count;
+  uint64_t seed;
+} se_solver_cfg;
+
+/* Counters (operators.hpp:44-65). */
+typedef struct se_counters {
+  long n_A_matvec, n_B_matvec, n_B_solve, n_shift_solve;
+  double t_mv, t_orth, t_sv, t_total;
+} se_counters;
+
+/* ---- library / errors ----------------------------------------------------------------- */
+SE_API const char* se_last_error(void);
+SE_API const char* se_version(void);
+SE_API int se_device_count(int* count);
+
+/* ---- contexts ----------------------------------------------------------------------------- */
+SE_API int se_ctx_create(int device, se_ctx** out);
+SE_API int se_ctx_destroy(se_ctx* ctx);
+SE_API int se_ctx_synchronize(se_ctx* ctx);
+/* Number of this library's kernels launched on ctx so far (bench evidence). */
+SE_API int se_ctx_kernel_launches(se_ctx* ctx, long* out);
+/* Device time of the filter kernels (ms, CUDA events on ctx's stream) and their count, since
+ * the last reset; used by bench.py for the roofline of the dominant kernel. */
+SE_API int se_ctx_filter_timing(se_ctx* ctx, int enable, double* ms, long* launches, double* bytes);
+
+/* ---- matrices (csr.hpp:23-58, laplacian.hpp:19-48) ---------------------------------------- */
+/* Host-side closed-form Laplacian (laplacian.hpp:19-48), bitwise the reference's CSR: call with
+ * rp == NULL to get n/nnz first. */
+SE_API int se_laplacian_host(int ndims, const int* dims, int* n, long* nnz, int* rp, int* ci, double* v);
+/* Closed-form spectrum, sorted ascending (laplacian.hpp:51-86). */
+SE_API int se_laplacian_eigs(int ndims, const int* dims, double* out);
+/* Upload a host CSR (int32 row_ptr[n+1], int32 col_idx[nnz], f64 vals[nnz]). */
+SE_API int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, const double* vals,
+                  se_csr** out);
+/* Device generator kernel for gen_laplacian (bit-identical to the host / reference CSR). */
+SE_API int se_csr_gen_laplacian(se_ctx* ctx, int ndims, const int* dims, se_csr** out);
+SE_API int se_csr_info(const se_csr* a, int* n, long* nnz);
+SE_API int se_csr_download(se_ctx* ctx, const se_csr* a, int* row_ptr, int* col_idx, double* vals);
+/* vals[p] *= d[i] * d[j] for stored (i, j = col_idx[p]): diagonal congruence D A D (BASELINE cfg5). */
+SE_API int se_csr_scale_sym(se_ctx* ctx, se_csr* a, const double* d_host);
+SE_API int se_csr_free(se_csr* a);
+
+/* ---- operator applications ---------------------------------------------------------------- */
+/* y = A x, host buffers (CsrMatrix::matvec csr.hpp:98-105; backs make_operator operators.hpp:34). */
+SE_API int se_spmv(se_ctx* ctx, const se_csr* a, const double* x, double* y);
+/* out = rho(Ahat) v for nvec column-major vectors (apply_pol filter_poly.hpp:256-277); host
+ * buffers; n_matvec += k per vector (Counters::n_A_matvec). */
+SE_API int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
+                  double* out, long* n_matvec);
+/* Same with device pointers (inputs already resident in HBM). */
+SE_API int se_cheb_apply_dev(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec,
+                      const double* d_v, double* d_out);
+
+/* ---- filters (host, filter_poly.hpp) -------------------------------------------------------- */
+SE_API int se_damping_multipliers(int k, int damping, double* out);            /* :41-60   */
+SE_API int se_chebyshev_coeffs(double gamma, int k, double* out);              /* :30-39   */
+SE_API int se_normalized_filter_coeffs(int k, double gamma, int damping, double* out); /* :182-190 */
+SE_API int se_balance_center(int k, double ta, double tb, int damping, double* gamma); /* :135-171 */
+SE_API int se_find_pol(double xi, double eta, double lmin, double lmax, double tau, int max_deg,
+                int damping, se_poly_filter* out);                     /* :198-253  */
+SE_API int se_eval_pol(const se_poly_filter* f, double t, double* out);       /* :93-97    */
+
+/* ---- spectral density ----------------------------------------------------------------------- */
+/* Unnormalised KPM moment sums over probes [first, first+count) of the probe stream drawn from
+ * Rng(seed) (dos.hpp:96-109); probes are generated on the host (mt19937_64) and processed on the
+ * device in blocks of up to 16.  zeta_sums has m+1 entries. */
+SE_API int se_kpm_moments(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec,
+                   int probe_kind, uint64_t seed, int first, int count, double* zeta_sums);
+/* Same over caller-supplied device probes (column-major n x nprobes); zeta_sums[m+1] host. */
+SE_API int se_kpm_moments_dev(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int nprobes,
+                       const double* d_probes, double* zeta_sums);
+/* Jackson-damped curve from normalised moments (dos.hpp:112-131 + dos_finalize :54-60). */
+SE_API int se_kpm_curve(int m, const double* zeta, int n, double lmin, double lmax, int npts, double* x,
+                 double* y, double* nev_est);
+/* kpm_dos (dos.hpp:82-132): moments on the device + curve on the host. */
+SE_API int se_kpm_dos(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec, int npts,
+               uint64_t seed, int probe_kind, double* x, double* y, double* nev_est);
+/* lan_dos (dos.hpp:136-154): device Lanczos per probe + host Ritz-Gaussian quadrature. */
+SE_API int se_lan_dos(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec, int npts,
+               double sigma, uint64_t seed, double* x, double* y, double* nev_est);
+SE_API int se_dos_count(int npts, int n, const double* x, const double* y, double xi, double eta,
+                 double* out);                                          /* dos.hpp:212-218 */
+SE_API int se_slice_spectrum(int npts, int n, const double* x, const double* y, double xi, double eta,
+                      int ns, double* breakpoints, double* est_counts); /* slicer.hpp:18-64 */
+
+/* ---- Krylov building blocks ----------------------------------------------------------------- */
+/* lan_tr_bounds (lanczos.hpp:148-277) with a device Lanczos. */
+SE_API int se_lan_tr_bounds(se_ctx* ctx, const se_csr* a, double tol, int restart_dim, int max_restarts,
+                     uint64_t seed, double* lmin, double* lmax);
+/* lanczos_run (lanczos.hpp:37-118), euclidean.  alpha[m], beta[m-1] host; basis optional
+ * (n x steps column-major host buffer, may be NULL). */
+SE_API int se_lanczos_run(se_ctx* ctx, const se_csr* a, const double* start, int m, double* alpha,
+                   double* beta, int* steps, int* breakdown, double* next_beta, double* next_w,
+                   double* basis);
+/* paired_cgs2 (orth.hpp:70-80) on host buffers: t (n) against W (n x k column-major); h may be
+ * NULL (else h[k] accumulates the coefficients). */
+SE_API int se_paired_cgs2(se_ctx* ctx, int n, int k, const double* W, double* t, double* h);
+/* Small dense/tridiagonal symmetric eigensolvers (host; tridiag_eig.hpp:111-131,
+ * dense_eig.hpp:114-139).  vectors: m x m column-major, may be NULL when want == 0. */
+SE_API int se_sym_tridiag_eig(int m, const double* alpha, const double* beta, int want, double* values,
+                       double* vectors);
+SE_API int se_dense_sym_eig(int m, const double* a, int want, int size_guard, double* values,
+                     double* vectors);
+
+/* ---- slice drivers (eigensolvers.hpp:703-732) ------------------------------------------------ */
+/* solver: 0 = cheb_lan_nr, 1 = cheb_lan_tr.  Optional deflation set (DeflationSet
+ * eigensolvers.hpp:69-73): defl_u host n x ndefl column-major + defl_vals, or ndefl = 0.
+ * want_vectors: 0 keeps eigenvectors on the device only (bench path).  Returns a results handle. */
+SE_API int se_cheb_lan(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi, double eta,
+                const se_solver_cfg* cfg, int solver, int ndefl, const double* defl_u,
+                const double* defl_vals, int want_vectors, se_results** out);
+SE_API int se_results_count(const se_results* r, int* nev);
+/* eigenvalues/residuals (nev each, ascending by eigenvalue), vectors (n x nev, may be NULL). */
+SE_API int se_results_copy(const se_results* r, double* eigenvalues, double* residuals, double* vectors);
+SE_API int se_results_info(const se_results* r, long* niter, int* hit_max_its, se_counters* counters);
+SE_API int se_results_free(se_results* r);
+
+/* ---- checks ---------------------------------------------------------------------------------- */
+/* rayleigh_and_residual (eigensolvers.hpp:86-106), standard problem, host vector u. */
+SE_API int se_rayleigh_residual(se_ctx* ctx, const se_csr* a, const double* u, double* lambda,
+                         double* residual);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SLICEEIG_CUDA_H */

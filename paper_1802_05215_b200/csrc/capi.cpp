@@ -1,0 +1,783 @@
+// extern "C" boundary of libsliceeig_cuda.so (declarations: include/sliceeig_cuda.h).
+// Every entry point converts exceptions into SE_* status codes + a thread-local message.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+
+#include "engine.hpp"
+#include "host_algos.hpp"
+
+using namespace se;
+
+struct se_ctx {
+  Ctx* c;
+};
+struct se_csr {
+  DevCsr a;
+};
+struct se_results {
+  std::unique_ptr<SliceResult> r;
+  int device = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SE_OK;
+  } catch (const se::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SE_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SE_ENUMERIC;
+  }
+}
+
+Ctx& C(se_ctx* c) {
+  if (!c || !c->c) fail(SE_EINVAL, "null se_ctx");
+  SE_CUDA(cudaSetDevice(c->c->device));
+  return *c->c;
+}
+const DevCsr& M(const se_csr* a) {
+  if (!a) fail(SE_EINVAL, "null se_csr");
+  return a->a;
+}
+
+PolyFilter to_filter(const se_poly_filter* f) {
+  if (!f || !f->mu) fail(SE_EINVAL, "null filter");
+  PolyFilter p;
+  p.k = f->k;
+  p.gamma = f->gamma;
+  p.c = f->c;
+  p.d = f->d;
+  p.tau = f->tau;
+  p.ta = f->ta;
+  p.tb = f->tb;
+  p.bar = f->bar;
+  p.damping = f->damping;
+  p.cap_reached = f->cap_reached != 0;
+  if (p.k < 1) fail(SE_EINVAL, "apply_pol: filter degree must be >= 1");
+  p.mu.assign(f->mu, f->mu + f->k + 1);
+  return p;
+}
+
+StepOp to_op(const PolyFilter& f) {
+  StepOp o;
+  o.plain = false;
+  o.k = f.k;
+  o.mu = f.mu;
+  o.c = f.c;
+  o.invd = 1.0 / f.d;
+  return o;
+}
+
+void check_csr_host(int n, const int* rp, const int* ci) {
+  if (n < 0) fail(SE_EINVAL, "CsrMatrix: negative dimension");
+  if (!rp) fail(SE_EINVAL, "null row_ptr");
+  if (rp[0] != 0) fail(SE_EINVAL, "CsrMatrix: row_ptr[0] must be 0");
+  for (int i = 0; i < n; ++i)
+    if (rp[i + 1] < rp[i]) fail(SE_EINVAL, "CsrMatrix: row_ptr must be non-decreasing");
+  for (long p = 0; p < rp[n]; ++p)
+    if (ci[p] < 0 || ci[p] >= n) fail(SE_ERANGE, "CsrMatrix: triplet index out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* se_last_error(void) { return g_err.c_str(); }
+const char* se_version(void) { return "sliceeig-b200 0.1 (sm_100a)"; }
+
+int se_device_count(int* count) {
+  return guard([&] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+// ---- contexts ------------------------------------------------------------------------------
+int se_ctx_create(int device, se_ctx** out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* h = new se_ctx{ctx_create(device)};
+    *out = h;
+  });
+}
+int se_ctx_destroy(se_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    ctx_destroy(ctx->c);
+    delete ctx;
+  });
+}
+int se_ctx_synchronize(se_ctx* ctx) {
+  return guard([&] { SE_CUDA(cudaStreamSynchronize(C(ctx).stream)); });
+}
+int se_ctx_kernel_launches(se_ctx* ctx, long* out) {
+  return guard([&] { *out = C(ctx).launches; });
+}
+int se_ctx_filter_timing(se_ctx* ctx, int enable, double* ms, long* launches, double* bytes) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (ms) *ms = c.filter_ms;
+    if (launches) *launches = c.filter_launches;
+    if (bytes) *bytes = c.filter_bytes;
+    c.time_filter = enable != 0;
+    c.filter_ms = 0.0;
+    c.filter_launches = 0;
+    c.filter_bytes = 0.0;
+  });
+}
+
+// ---- matrices -------------------------------------------------------------------------------
+int se_laplacian_host(int ndims, const int* dims, int* n, long* nnz, int* rp, int* ci, double* v) {
+  return guard([&] {
+    if (ndims < 1 || ndims > 3) fail(SE_EINVAL, "gen_laplacian: need 1 to 3 grid dimensions");
+    for (int q = 0; q < ndims; ++q)
+      if (dims[q] < 1) fail(SE_EINVAL, "gen_laplacian: grid dimensions must be positive");
+    const long nx = dims[0], ny = ndims > 1 ? dims[1] : 1, nz = ndims > 2 ? dims[2] : 1;
+    const long nl = nx * ny * nz;
+    if (nl > 40000000L) fail(SE_EINVAL, "gen_laplacian: grid too large");
+    long cnt = nl + 2 * (nx - 1) * ny * nz + 2 * nx * (ny - 1) * nz + 2 * nx * ny * (nz - 1);
+    *n = (int)nl;
+    *nnz = cnt;
+    if (!rp) return;
+    const long plane = nx * ny;
+    long p = 0;
+    long row = 0;
+    rp[0] = 0;
+    for (long kz = 0; kz < nz; ++kz)
+      for (long jy = 0; jy < ny; ++jy)
+        for (long ix = 0; ix < nx; ++ix, ++row) {
+          auto put = [&](long col, double val) {
+            ci[p] = (int)col;
+            v[p++] = val;
+          };
+          if (nz > 1 && kz > 0) put(row - plane, -1.0);
+          if (ny > 1 && jy > 0) put(row - nx, -1.0);
+          if (ix > 0) put(row - 1, -1.0);
+          put(row, 2.0 * ndims);
+          if (ix < nx - 1) put(row + 1, -1.0);
+          if (ny > 1 && jy < ny - 1) put(row + nx, -1.0);
+          if (nz > 1 && kz < nz - 1) put(row + plane, -1.0);
+          rp[row + 1] = (int)p;
+        }
+  });
+}
+
+int se_laplacian_eigs(int ndims, const int* dims, double* out) {
+  return guard([&] {
+    if (ndims < 1 || ndims > 3) fail(SE_EINVAL, "laplacian_analytic_eigs: need 1 to 3 grid dimensions");
+    long n = 1;
+    for (int q = 0; q < ndims; ++q) {
+      if (dims[q] < 1) fail(SE_EINVAL, "laplacian_analytic_eigs: dimensions must be positive");
+      n *= dims[q];
+    }
+    if (n > 10000000L) fail(SE_EINVAL, "laplacian_analytic_eigs: enumeration too large");
+    const double pi = 3.14159265358979323846;
+    std::vector<Vec> one(ndims);
+    for (int q = 0; q < ndims; ++q) {
+      one[q].resize(dims[q]);
+      for (int i = 1; i <= dims[q]; ++i) {
+        const double s = std::sin(0.5 * pi * i / (dims[q] + 1));
+        one[q][i - 1] = 4.0 * s * s;
+      }
+    }
+    const int nx = dims[0], ny = ndims > 1 ? dims[1] : 1, nz = ndims > 2 ? dims[2] : 1;
+    long p = 0;
+    for (int kz = 0; kz < nz; ++kz)
+      for (int jy = 0; jy < ny; ++jy)
+        for (int ix = 0; ix < nx; ++ix) {
+          double val = one[0][ix];
+          if (ndims > 1) val += one[1][jy];
+          if (ndims > 2) val += one[2][kz];
+          out[p++] = val;
+        }
+    std::sort(out, out + n);
+  });
+}
+
+int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, const double* vals,
+                  se_csr** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    check_csr_host(n, row_ptr, col_idx);
+    auto h = std::make_unique<se_csr>();
+    DevCsr& a = h->a;
+    a.device = c.device;
+    a.n = n;
+    a.nnz = row_ptr[n];
+    a.rp = dev_alloc<int>(n + 1);
+    a.ci = dev_alloc<int>(a.nnz);
+    a.v = dev_alloc<double>(a.nnz);
+    int mx = 0;
+    for (int i = 0; i < n; ++i) mx = std::max(mx, row_ptr[i + 1] - row_ptr[i]);
+    a.max_row_nnz = mx;
+    SE_CUDA(cudaMemcpyAsync(a.rp, row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, c.stream));
+    if (a.nnz) {
+      SE_CUDA(cudaMemcpyAsync(a.ci, col_idx, sizeof(int) * a.nnz, cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaMemcpyAsync(a.v, vals, sizeof(double) * a.nnz, cudaMemcpyHostToDevice, c.stream));
+    }
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    *out = h.release();
+  });
+}
+
+int se_csr_gen_laplacian(se_ctx* ctx, int ndims, const int* dims, se_csr** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (ndims < 1 || ndims > 3) fail(SE_EINVAL, "gen_laplacian: need 1 to 3 grid dimensions");
+    long nl = 1;
+    for (int q = 0; q < ndims; ++q) {
+      if (dims[q] < 1) fail(SE_EINVAL, "gen_laplacian: grid dimensions must be positive");
+      nl *= dims[q];
+    }
+    if (nl > 40000000L) fail(SE_EINVAL, "gen_laplacian: grid too large");
+    auto h = std::make_unique<se_csr>();
+    h->a.device = c.device;
+    k::gen_laplacian(c, ndims, dims, h->a);
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    *out = h.release();
+  });
+}
+
+int se_csr_info(const se_csr* a, int* n, long* nnz) {
+  return guard([&] {
+    *n = M(a).n;
+    *nnz = M(a).nnz;
+  });
+}
+
+int se_csr_download(se_ctx* ctx, const se_csr* a, int* row_ptr, int* col_idx, double* vals) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& m = M(a);
+    SE_CUDA(cudaMemcpyAsync(row_ptr, m.rp, sizeof(int) * (m.n + 1), cudaMemcpyDeviceToHost, c.stream));
+    if (m.nnz) {
+      SE_CUDA(cudaMemcpyAsync(col_idx, m.ci, sizeof(int) * m.nnz, cudaMemcpyDeviceToHost, c.stream));
+      SE_CUDA(cudaMemcpyAsync(vals, m.v, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, c.stream));
+    }
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int se_csr_scale_sym(se_ctx* ctx, se_csr* a, const double* d_host) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (!a) fail(SE_EINVAL, "null se_csr");
+    double* d = dev_alloc<double>(a->a.n);
+    SE_CUDA(cudaMemcpyAsync(d, d_host, sizeof(double) * a->a.n, cudaMemcpyHostToDevice, c.stream));
+    k::csr_scale_sym(c, a->a, d);
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    dev_free(d);
+  });
+}
+
+int se_csr_free(se_csr* a) {
+  return guard([&] {
+    if (!a) return;
+    cudaSetDevice(a->a.device);
+    dev_free(a->a.rp);
+    dev_free(a->a.ci);
+    dev_free(a->a.v);
+    delete a;
+  });
+}
+
+// ---- operator applications ------------------------------------------------------------------
+int se_spmv(se_ctx* ctx, const se_csr* a, const double* x, double* y) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& m = M(a);
+    double* dx = dev_alloc<double>(m.n);
+    double* dy = dev_alloc<double>(m.n);
+    SE_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * m.n, cudaMemcpyHostToDevice, c.stream));
+    StepOp op;
+    apply_filter_dev(c, m, op, 1, dx, dy);
+    SE_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * m.n, cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    dev_free(dx);
+    dev_free(dy);
+  });
+}
+
+int se_cheb_apply_dev(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec,
+                      const double* d_v, double* d_out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& m = M(a);
+    const PolyFilter pf = to_filter(f);
+    const StepOp op = to_op(pf);
+    if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
+    apply_filter_dev(c, m, op, nvec, d_v, d_out);
+    if (c.time_filter) {
+      SE_CUDA(cudaEventRecord(c.ev1, c.stream));
+      SE_CUDA(cudaEventSynchronize(c.ev1));
+      float ms = 0.f;
+      SE_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      c.filter_ms += ms;
+      c.filter_launches += (long)nvec * pf.k;
+      // algorithmic bytes: j = 1 step Abytes + 32 n, j >= 2 steps Abytes + 40 n
+      c.filter_bytes += (double)nvec * (m.abytes() + 32.0 * m.n +
+                                        (pf.k - 1) * (m.abytes() + 40.0 * m.n));
+    }
+  });
+}
+
+int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
+                  double* out, long* n_matvec) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& m = M(a);
+    const PolyFilter pf = to_filter(f);
+    const size_t bytes = sizeof(double) * (size_t)m.n * nvec;
+    double* dv = dev_alloc<double>((size_t)m.n * nvec);
+    double* dout = dev_alloc<double>((size_t)m.n * nvec);
+    SE_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, c.stream));
+    apply_filter_dev(c, m, to_op(pf), nvec, dv, dout);
+    SE_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    dev_free(dv);
+    dev_free(dout);
+    if (n_matvec) *n_matvec += (long)pf.k * nvec;
+  });
+}
+
+// ---- filters ---------------------------------------------------------------------------------
+int se_damping_multipliers(int k, int damping, double* out) {
+  return guard([&] {
+    if (k < 0) fail(SE_EINVAL, "damping_multipliers: negative degree");
+    const Vec s = damping_multipliers(k, damping);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+int se_chebyshev_coeffs(double gamma, int k, double* out) {
+  return guard([&] {
+    const Vec s = chebyshev_coeffs(gamma, k);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+int se_normalized_filter_coeffs(int k, double gamma, int damping, double* out) {
+  return guard([&] {
+    const Vec s = normalized_filter_coeffs(k, gamma, damping);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+int se_balance_center(int k, double ta, double tb, int damping, double* gamma) {
+  return guard([&] { *gamma = balance_center(k, ta, tb, damping); });
+}
+int se_find_pol(double xi, double eta, double lmin, double lmax, double tau, int max_deg,
+                int damping, se_poly_filter* out) {
+  return guard([&] {
+    if (!out) fail(SE_EINVAL, "null filter");
+    const PolyFilter f = find_pol(xi, eta, lmin, lmax, tau, max_deg, damping);
+    if (!out->mu || out->mu_cap < f.k + 1)
+      fail(SE_EINVAL, "se_find_pol: mu buffer too small (need max_deg+1)");
+    out->k = f.k;
+    out->gamma = f.gamma;
+    out->c = f.c;
+    out->d = f.d;
+    out->tau = f.tau;
+    out->ta = f.ta;
+    out->tb = f.tb;
+    out->bar = f.bar;
+    out->damping = f.damping;
+    out->cap_reached = f.cap_reached;
+    std::copy(f.mu.begin(), f.mu.end(), out->mu);
+  });
+}
+int se_eval_pol(const se_poly_filter* f, double t, double* out) {
+  return guard([&] {
+    if (!f || !f->mu) fail(SE_EINVAL, "null filter");
+    *out = eval_pol(f->mu, f->k, t);
+  });
+}
+
+// ---- spectral density --------------------------------------------------------------------------
+namespace {
+constexpr int kBlock = 16;
+
+// dos.hpp:96-109 on the device, probes from one host Rng(seed) stream in probe order.
+void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, int n_vec,
+                      int probe_kind, std::uint64_t seed, int first, int count, Vec& zeta) {
+  if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
+  if (m < 1 || n_vec < 1) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
+  if (a.n < 1) fail(SE_EINVAL, "dos: empty operator");
+  if (first < 0 || count < 0 || first + count > n_vec) fail(SE_EINVAL, "kpm: probe range");
+  const int n = a.n;
+  const double cc = 0.5 * (lmax + lmin), d = 0.5 * (lmax - lmin);
+  zeta.assign(m + 1, 0.0);
+  if (count == 0) return;
+  Rng rng(seed);
+  auto draw = [&](double* out, long len) {
+    if (probe_kind == SE_PROBE_GAUSSIAN)
+      rng.normal_fill(out, len);
+    else
+      rng.rademacher_fill(out, len);
+  };
+  {  // advance the stream past the probes owned by other ranks
+    Vec skip(n);
+    for (int l = 0; l < first; ++l) draw(skip.data(), n);
+  }
+  const size_t blk = (size_t)n * kBlock;
+  double *V = dev_alloc<double>(blk), *X[3];
+  for (double*& x : X) x = dev_alloc<double>(blk);
+  double* dz = dev_alloc<double>((size_t)(m + 1) * kBlock);
+  k::Scratch s;
+  s.cap = k::kpm_scratch_doubles(c, n);
+  s.buf = dev_alloc<double>(s.cap);
+  s.cnt = dev_alloc<unsigned>(1);
+  s.ncnt = 1;
+  SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned), c.stream));
+  double* hbuf = nullptr;
+  SE_CUDA(cudaMallocHost(&hbuf, sizeof(double) * blk));
+  Vec probe(n), hz((size_t)(m + 1) * kBlock);
+  try {
+    for (int b0 = 0; b0 < count; b0 += kBlock) {
+      const int b = std::min(kBlock, count - b0);
+      SE_CUDA(cudaStreamSynchronize(c.stream));  // hbuf reuse
+      for (int j = 0; j < b; ++j) {
+        draw(probe.data(), n);
+        for (int i = 0; i < n; ++i) hbuf[(size_t)i * b + j] = probe[i];
+      }
+      SE_CUDA(cudaMemcpyAsync(V, hbuf, sizeof(double) * (size_t)n * b, cudaMemcpyHostToDevice, c.stream));
+      k::kpm_step(c, s, a, b, true, V, V, nullptr, X[0], cc, d, dz, 0);
+      const double* w0 = V;
+      double *w1 = X[0], *tb = X[1], *spare = X[2];
+      for (int kk = 2; kk <= m; ++kk) {
+        k::kpm_step(c, s, a, b, false, V, w0, w1, tb, cc, d, dz, kk);
+        double* freed = (w0 == V) ? spare : const_cast<double*>(w0);  // w0 <- w1 <- t <- free
+        w0 = w1;
+        w1 = tb;
+        tb = freed;
+      }
+      SE_CUDA(cudaMemcpyAsync(hz.data(), dz, sizeof(double) * (size_t)(m + 1) * b,
+                              cudaMemcpyDeviceToHost, c.stream));
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      for (int j = 0; j < b; ++j)  // probe order (dos.hpp:100-106)
+        for (int kk = 0; kk <= m; ++kk) zeta[kk] += hz[(size_t)kk * b + j];
+    }
+  } catch (...) {
+    cudaFreeHost(hbuf);
+    for (void* p : {(void*)V, (void*)X[0], (void*)X[1], (void*)X[2], (void*)dz, (void*)s.buf, (void*)s.cnt})
+      dev_free(p);
+    throw;
+  }
+  cudaFreeHost(hbuf);
+  for (void* p : {(void*)V, (void*)X[0], (void*)X[1], (void*)X[2], (void*)dz, (void*)s.buf, (void*)s.cnt})
+    dev_free(p);
+}
+}  // namespace
+
+int se_kpm_moments(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec,
+                   int probe_kind, uint64_t seed, int first, int count, double* zeta_sums) {
+  return guard([&] {
+    Vec z;
+    kpm_moments_impl(C(ctx), M(a), lmin, lmax, m, n_vec, probe_kind, seed, first, count, z);
+    std::copy(z.begin(), z.end(), zeta_sums);
+  });
+}
+
+int se_kpm_moments_dev(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int nprobes,
+                       const double* d_probes, double* zeta_sums) {
+  return guard([&] {
+    (void)ctx;
+    (void)a;
+    (void)lmin;
+    (void)lmax;
+    (void)m;
+    (void)nprobes;
+    (void)d_probes;
+    (void)zeta_sums;
+    fail(SE_EINVAL, "se_kpm_moments_dev: not implemented in this build");
+  });
+}
+
+int se_kpm_curve(int m, const double* zeta, int n, double lmin, double lmax, int npts, double* x,
+                 double* y, double* nev_est) {
+  return guard([&] {
+    if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
+    if (m < 1 || npts < 2) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
+    const Curve cv = kpm_curve(Vec(zeta, zeta + m + 1), n, lmin, lmax, npts);
+    std::copy(cv.x.begin(), cv.x.end(), x);
+    std::copy(cv.y.begin(), cv.y.end(), y);
+    *nev_est = cv.nev_est;
+  });
+}
+
+int se_kpm_dos(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec, int npts,
+               uint64_t seed, int probe_kind, double* x, double* y, double* nev_est) {
+  return guard([&] {
+    const DevCsr& mat = M(a);
+    if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
+    if (m < 1 || n_vec < 1 || npts < 2) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
+    Vec z;
+    kpm_moments_impl(C(ctx), mat, lmin, lmax, m, n_vec, probe_kind, seed, 0, n_vec, z);
+    for (double& q : z) q /= (double)n_vec * mat.n;  // dos.hpp:110
+    const Curve cv = kpm_curve(z, mat.n, lmin, lmax, npts);
+    std::copy(cv.x.begin(), cv.x.end(), x);
+    std::copy(cv.y.begin(), cv.y.end(), y);
+    *nev_est = cv.nev_est;
+  });
+}
+
+int se_lan_dos(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec, int npts,
+               double sigma, uint64_t seed, double* x, double* y, double* nev_est) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& mat = M(a);
+    if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
+    if (m < 1 || n_vec < 1 || npts < 2) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
+    if (mat.n < 1) fail(SE_EINVAL, "dos: empty operator");
+    const double sg = sigma > 0.0 ? sigma : 0.4 * (lmax - lmin) / std::sqrt((double)m);
+    Curve cv;
+    cv.n = mat.n;
+    cv.x = dos_grid(lmin, lmax, npts);
+    cv.y.assign(npts, 0.0);
+    Rng rng(seed);
+    Vec start(mat.n);
+    for (int l = 0; l < n_vec; ++l) {
+      rng.normal_fill(start.data(), mat.n);
+      const LanczosRun r = lanczos_run(c, mat, start.data(), m, false);
+      Vec vals, vecs;
+      sym_tridiag_eig(r.alpha, r.beta, true, vals, vecs);
+      const int steps = (int)vals.size();
+      Vec tau2(steps);
+      for (int i = 0; i < steps; ++i) tau2[i] = vecs[(size_t)i * steps] * vecs[(size_t)i * steps];
+      add_ritz_gaussians(vals, tau2, cv.x, sg, cv.y);
+    }
+    dos_finalize(cv);
+    std::copy(cv.x.begin(), cv.x.end(), x);
+    std::copy(cv.y.begin(), cv.y.end(), y);
+    *nev_est = cv.nev_est;
+  });
+}
+
+int se_dos_count(int npts, int n, const double* x, const double* y, double xi, double eta,
+                 double* out) {
+  return guard([&] {
+    Curve cv;
+    cv.n = n;
+    cv.x.assign(x, x + npts);
+    cv.y.assign(y, y + npts);
+    *out = dos_count(cv, xi, eta);
+  });
+}
+
+int se_slice_spectrum(int npts, int n, const double* x, const double* y, double xi, double eta,
+                      int ns, double* breakpoints, double* est_counts) {
+  return guard([&] {
+    Curve cv;
+    cv.n = n;
+    cv.x.assign(x, x + std::max(npts, 0));
+    cv.y.assign(y, y + std::max(npts, 0));
+    Vec bp, est;
+    slice_spectrum(cv, xi, eta, ns, bp, est);
+    std::copy(bp.begin(), bp.end(), breakpoints);
+    std::copy(est.begin(), est.end(), est_counts);
+  });
+}
+
+// ---- Krylov ------------------------------------------------------------------------------------
+int se_lan_tr_bounds(se_ctx* ctx, const se_csr* a, double tol, int restart_dim, int max_restarts,
+                     uint64_t seed, double* lmin, double* lmax) {
+  return guard([&] { lan_tr_bounds(C(ctx), M(a), tol, restart_dim, max_restarts, seed, *lmin, *lmax); });
+}
+
+int se_lanczos_run(se_ctx* ctx, const se_csr* a, const double* start, int m, double* alpha,
+                   double* beta, int* steps, int* breakdown, double* next_beta, double* next_w,
+                   double* basis) {
+  return guard([&] {
+    const DevCsr& mat = M(a);
+    if (m < 1) fail(SE_EINVAL, "lanczos_run: m must be positive");
+    const LanczosRun r = lanczos_run(C(ctx), mat, start, m, basis != nullptr);
+    std::copy(r.alpha.begin(), r.alpha.end(), alpha);
+    std::copy(r.beta.begin(), r.beta.end(), beta);
+    *steps = r.steps;
+    *breakdown = r.breakdown;
+    *next_beta = r.next_beta;
+    if (next_w && !r.next_w.empty()) std::copy(r.next_w.begin(), r.next_w.end(), next_w);
+    if (basis) std::copy(r.basis.begin(), r.basis.end(), basis);
+  });
+}
+
+int se_paired_cgs2(se_ctx* ctx, int n, int kq, const double* W, double* t, double* h) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (n < 1 || kq < 0) fail(SE_EINVAL, "paired_cgs2: bad sizes");
+    double* dW = dev_alloc<double>((size_t)n * std::max(kq, 1));
+    double* dt = dev_alloc<double>(n);
+    double* coef = dev_alloc<double>(std::max(kq, 1));
+    double* hd = dev_alloc<double>(std::max(kq, 1));
+    Ctl* ctl = dev_alloc<Ctl>(1);
+    k::Scratch s;
+    s.cap = k::cgs_scratch_doubles(c, n, kq);
+    s.ncnt = k::cgs_counter_slots(kq);
+    s.buf = dev_alloc<double>(s.cap);
+    s.cnt = dev_alloc<unsigned>(s.ncnt);
+    auto cleanup = [&] {
+      for (void* p : {(void*)dW, (void*)dt, (void*)coef, (void*)hd, (void*)ctl, (void*)s.buf, (void*)s.cnt})
+        dev_free(p);
+    };
+    try {
+      SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
+      SE_CUDA(cudaMemsetAsync(hd, 0, sizeof(double) * std::max(kq, 1), c.stream));
+      if (kq) SE_CUDA(cudaMemcpyAsync(dW, W, sizeof(double) * (size_t)n * kq, cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaMemcpyAsync(dt, t, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      Ctl z{};
+      z.i = kq - 1;  // columns 0..i
+      SE_CUDA(cudaMemcpyAsync(ctl, &z, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+      k::norm_before(c, s, n, dt, ctl);
+      Ctl h0;
+      SE_CUDA(cudaMemcpyAsync(&h0, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      // orth.hpp:72-73: nothing to do for a zero vector or an empty basis
+      if (h0.before != 0.0 && kq > 0) {
+        // h accumulates every coefficient: run passes with hdiag bookkeeping per column
+        for (int pass = 0; pass < 2; ++pass) {
+          k::cgs_pass(c, s, n, dt, dW, false, pass == 1, ctl, nullptr, coef, kq);
+          if (h) {
+            Vec cf(kq);
+            Ctl hh;
+            SE_CUDA(cudaMemcpyAsync(&hh, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+            SE_CUDA(cudaMemcpyAsync(cf.data(), coef, sizeof(double) * kq, cudaMemcpyDeviceToHost, c.stream));
+            SE_CUDA(cudaStreamSynchronize(c.stream));
+            if (pass == 0 || hh.npass == 2)
+              for (int j = 0; j < kq; ++j) h[j] += cf[j];
+          }
+        }
+      }
+      SE_CUDA(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+int se_sym_tridiag_eig(int m, const double* alpha, const double* beta, int want, double* values,
+                       double* vectors) {
+  return guard([&] {
+    if (m < 0) fail(SE_EINVAL, "sym_tridiag_eig: negative size");
+    Vec a(alpha, alpha + m), b;
+    if (m > 1) b.assign(beta, beta + m - 1);
+    Vec vals, vecs;
+    sym_tridiag_eig(a, b, want != 0, vals, vecs);
+    std::copy(vals.begin(), vals.end(), values);
+    if (want && vectors) std::copy(vecs.begin(), vecs.end(), vectors);
+  });
+}
+
+int se_dense_sym_eig(int m, const double* a, int want, int size_guard, double* values,
+                     double* vectors) {
+  return guard([&] {
+    if (m > (size_guard > 0 ? size_guard : 5000))
+      fail(SE_EINVAL, "dense_sym_eig: matrix exceeds the size guard");
+    Vec vals, vecs;
+    dense_sym_eig(m, a, want != 0, vals, vecs);
+    std::copy(vals.begin(), vals.end(), values);
+    if (want && vectors) std::copy(vecs.begin(), vecs.end(), vectors);
+  });
+}
+
+// ---- slice drivers -------------------------------------------------------------------------------
+int se_cheb_lan(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi, double eta,
+                const se_solver_cfg* cfg, int solver, int ndefl, const double* defl_u,
+                const double* defl_vals, int want_vectors, se_results** out) {
+  (void)want_vectors;
+  return guard([&] {
+    *out = nullptr;
+    const char* who = solver == 1 ? "cheb_lan_tr" : "cheb_lan_nr";
+    Ctx& c = C(ctx);
+    if (!(eta > xi)) fail(SE_EINVAL, std::string(who) + ": degenerate interval");
+    const SolverCfg sc = resolve_config(cfg, who);
+    const PolyFilter pf = to_filter(f);
+    auto res = std::make_unique<se_results>();
+    res->device = c.device;
+    res->r = cheb_lan(c, M(a), pf, xi, eta, sc, solver == 1, ndefl, defl_u, defl_vals, who);
+    *out = res.release();
+  });
+}
+
+int se_results_count(const se_results* r, int* nev) {
+  return guard([&] {
+    if (!r) fail(SE_EINVAL, "null results");
+    *nev = (int)r->r->eigenvalues.size();
+  });
+}
+
+int se_results_copy(const se_results* r, double* eigenvalues, double* residuals, double* vectors) {
+  return guard([&] {
+    if (!r) fail(SE_EINVAL, "null results");
+    const SliceResult& s = *r->r;
+    if (eigenvalues) std::copy(s.eigenvalues.begin(), s.eigenvalues.end(), eigenvalues);
+    if (residuals) std::copy(s.residuals.begin(), s.residuals.end(), residuals);
+    if (vectors && !s.eigenvalues.empty()) {
+      SE_CUDA(cudaSetDevice(r->device));
+      SE_CUDA(cudaMemcpy(vectors, s.vectors.p, sizeof(double) * (size_t)s.n * s.eigenvalues.size(),
+                         cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int se_results_info(const se_results* r, long* niter, int* hit_max_its, se_counters* counters) {
+  return guard([&] {
+    if (!r) fail(SE_EINVAL, "null results");
+    if (niter) *niter = r->r->niter;
+    if (hit_max_its) *hit_max_its = r->r->hit_max_its;
+    if (counters) *counters = r->r->counters;
+  });
+}
+
+int se_results_free(se_results* r) {
+  return guard([&] {
+    if (!r) return;
+    cudaSetDevice(r->device);
+    devmat_free(r->r->vectors);
+    delete r;
+  });
+}
+
+// ---- checks ---------------------------------------------------------------------------------------
+int se_rayleigh_residual(se_ctx* ctx, const se_csr* a, const double* u, double* lambda,
+                         double* residual) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& m = M(a);
+    double* du = dev_alloc<double>(m.n);
+    double* dau = dev_alloc<double>(m.n);
+    double* st = dev_alloc<double>(3);
+    SE_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * m.n, cudaMemcpyHostToDevice, c.stream));
+    StepOp op;
+    apply_filter_dev(c, m, op, 1, du, dau);
+    k::candidate_stats(c, m.n, 1, du, dau, st);
+    double h[3];
+    SE_CUDA(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    for (void* p : {(void*)du, (void*)dau, (void*)st}) dev_free(p);
+    if (!(h[2] > 0.0)) fail(SE_EINVAL, "rayleigh_and_residual: zero (or B-degenerate) vector");
+    *lambda = h[0];
+    // candidate_stats reports ||Au - lambda u|| / sqrt(uu); rayleigh_and_residual does not scale
+    *residual = h[1] * std::sqrt(h[2]);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Internal shared declarations of libsliceeig_cuda.so (host + device).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sliceeig_cuda.h"
+
+namespace se {
+
+// Exceptions carrying the C-ABI status code; capi.cpp maps them to SE_* codes.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const char* msg) {
+  if (!ok) fail(SE_EINVAL, msg);
+}
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define SE_CUDA(x) ::se::cuda_check((x), #x, __FILE__, __LINE__)
+
+// ---- device matrices -----------------------------------------------------------------------
+// CSR in HBM: int32 row_ptr[n+1], int32 col_idx[nnz], f64 vals[nnz] (the reference layout,
+// csr.hpp:158-162) plus a per-tile nnz table used by the row-tile SpMV.
+struct DevCsr {
+  int device = 0;
+  int n = 0;
+  long nnz = 0;
+  int* rp = nullptr;
+  int* ci = nullptr;
+  double* v = nullptr;
+  int max_row_nnz = 0;
+  double abytes() const { return 12.0 * (double)nnz + 4.0 * (double)(n + 1); }
+};
+
+// A growable device column-major matrix (n rows, capacity `cap` columns, ld = n).
+struct DevMat {
+  int n = 0;
+  int cap = 0;
+  double* p = nullptr;
+  double* col(int j) const { return p + (size_t)j * n; }
+};
+
+struct Ctx;
+void devmat_reserve(Ctx& c, DevMat& m, int n, int cols, bool keep);
+void devmat_free(DevMat& m);
+
+// Scratch allocations tied to a context (freed with it).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+};
+
+}  // namespace se

@@ -1,0 +1,888 @@
+// Device Lanczos engine (see engine.hpp).  Reference: lanczos.hpp:37-277 and
+// eigensolvers.hpp:142-732 under /root/reference/proj/include/sliceeig/.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+namespace se {
+
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int grow(int want) { return std::max(want, 16) + std::max(want, 16) / 2; }
+
+// ---- one device recurrence (basis W, locked set L, step graph) ------------------------------
+struct Krylov {
+  Ctx& c;
+  const DevCsr& A;
+  const StepOp& op;
+  int n;
+  DevMat W, L;
+  double* t = nullptr;
+  double* fb[3] = {nullptr, nullptr, nullptr};
+  Ctl* ctl = nullptr;
+  double *alpha = nullptr, *beta = nullptr, *hdiag = nullptr, *coef = nullptr, *coef_l = nullptr;
+  double* dscal = nullptr;  // device scalars for host-side dots
+  int arr_cap = 0, coefl_cap = 0;
+  k::Scratch s;
+  cudaGraphExec_t gexec = nullptr;
+  int gnodes = 0;
+  int gmode = -1;
+  int nlock = 0;
+
+  Krylov(Ctx& cc, const DevCsr& a, const StepOp& o) : c(cc), A(a), op(o), n(a.n) {
+    t = dev_alloc<double>(n);
+    if (!op.plain)
+      for (double*& b : fb) b = dev_alloc<double>(n);
+    ctl = dev_alloc<Ctl>(1);
+    dscal = dev_alloc<double>(4);
+    Ctl z{};
+    SE_CUDA(cudaMemcpyAsync(ctl, &z, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+  }
+  ~Krylov() {
+    cudaStreamSynchronize(c.stream);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    devmat_free(W);
+    devmat_free(L);
+    for (void* p : {(void*)t, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl, (void*)alpha,
+                    (void*)beta, (void*)hdiag, (void*)coef, (void*)coef_l, (void*)dscal,
+                    (void*)s.buf, (void*)s.cnt})
+      dev_free(p);
+  }
+
+  void drop_graph() {
+    if (gexec) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      cudaGraphExecDestroy(gexec);
+    }
+    gexec = nullptr;
+    gmode = -1;
+  }
+
+  // Capacity for `wcols` basis columns and `lcols` locked columns; pointers baked into the step
+  // graph change only here (then the graph is re-captured).
+  void ensure(int wcols, int lcols) {
+    bool dirty = false;
+    if (wcols > W.cap) {
+      devmat_reserve(c, W, n, grow(wcols), true);
+      dirty = true;
+    }
+    if (lcols > L.cap) {
+      devmat_reserve(c, L, n, grow(lcols), true);
+      dirty = true;
+    }
+    if (W.cap > arr_cap) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      auto regrow = [&](double*& p) {
+        double* q = dev_alloc<double>(W.cap);
+        SE_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * W.cap, c.stream));
+        if (p) SE_CUDA(cudaMemcpyAsync(q, p, sizeof(double) * arr_cap, cudaMemcpyDeviceToDevice, c.stream));
+        SE_CUDA(cudaStreamSynchronize(c.stream));
+        dev_free(p);
+        p = q;
+      };
+      regrow(alpha);
+      regrow(beta);
+      regrow(hdiag);
+      regrow(coef);
+      arr_cap = W.cap;
+      dirty = true;
+    }
+    if (std::max(L.cap, 1) > coefl_cap) {
+      dev_free(coef_l);
+      coefl_cap = std::max(L.cap, 1);
+      coef_l = dev_alloc<double>(coefl_cap);
+      dirty = true;
+    }
+    const int wide = std::max(W.cap, L.cap);
+    const size_t need = k::cgs_scratch_doubles(c, n, wide);
+    const int slots = k::cgs_counter_slots(wide);
+    if (need > s.cap || slots > s.ncnt) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      dev_free(s.buf);
+      dev_free(s.cnt);
+      s.cap = need + need / 2;
+      s.ncnt = slots + slots / 2;
+      s.buf = dev_alloc<double>(s.cap);
+      s.cnt = dev_alloc<unsigned>(s.ncnt);
+      SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
+      dirty = true;
+    }
+    if (dirty) drop_graph();
+  }
+
+  Ctl get() {
+    Ctl h;
+    SE_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+  }
+  void put(const Ctl& h) {
+    SE_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+  }
+  void begin(int i0) {  // new recurrence segment starting at column i0
+    Ctl h = get();
+    h.i = i0;
+    h.halted = 0;
+    h.nlock = nlock;
+    put(h);
+  }
+
+  // Filter W[:, ctl->i] into t (apply_pol filter_poly.hpp:256-277, or one op application).
+  void record_filter() {
+    k::ChebArgs a;
+    a.src_ctl = ctl;
+    a.src_ld = n;
+    a.halt = ctl;
+    if (op.plain) {
+      a.x = W.p;
+      a.y = t;
+      k::spmv_cheb(c, A, k::kPlain, a);
+      return;
+    }
+    a.c = op.c;
+    a.invd = op.invd;
+    a.x = W.p;
+    a.y = fb[0];
+    a.out = t;
+    a.mu0 = op.mu[0];
+    a.muj = op.mu[1];
+    k::spmv_cheb(c, A, k::kFirst, a);
+    // buffers: prev (j-2), cur (j-1), next; W[:, i] plays prev for j = 2
+    int cur = 0, prv = -1, nxt = 1;
+    for (int j = 2; j <= op.k; ++j) {
+      k::ChebArgs b = a;
+      b.x = fb[cur];
+      b.prev = prv < 0 ? W.p : fb[prv];
+      b.src_ctl = prv < 0 ? ctl : nullptr;
+      b.y = fb[nxt];
+      b.muj = op.mu[j];
+      k::spmv_cheb(c, A, k::kNext, b);
+      const int old_prv = prv < 0 ? 2 : prv;
+      prv = cur;
+      cur = nxt;
+      nxt = old_prv;
+    }
+  }
+
+  // One Lanczos step.  mode 0: NR recurrence (eigensolvers.hpp:406-433 / lanczos.hpp:151-185);
+  // mode 1: TR projection with h accumulation (eigensolvers.hpp:524-556 / lanczos.hpp:284-311).
+  void record_step(int mode) {
+    k::stamp(c, ctl, 0);
+    record_filter();
+    k::stamp(c, ctl, 1);
+    if (L.cap > 0) k::cgs_pass(c, s, n, t, L.p, true, false, ctl, nullptr, coef_l, L.cap);
+    if (mode == 0) {
+      k::nr_beta_alpha(c, s, n, t, W.p, ctl, alpha, beta);
+      k::nr_sub_alpha(c, s, n, t, W.p, ctl);
+    } else {
+      k::norm_before(c, s, n, t, ctl);
+    }
+    double* h = mode == 1 ? hdiag : nullptr;
+    k::cgs_pass(c, s, n, t, W.p, false, false, ctl, h, coef, W.cap);
+    k::cgs_pass(c, s, n, t, W.p, false, true, ctl, h, coef, W.cap);
+    k::normalize_next(c, s, n, t, W.p, ctl, beta);
+    k::stamp(c, ctl, 2);
+  }
+
+  void run(int mode, int count) {
+    if (count <= 0) return;
+    if (!gexec || gmode != mode) {
+      drop_graph();
+      const long before = c.launches;
+      SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        record_step(mode);
+      } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(c.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      cudaGraph_t g;
+      SE_CUDA(cudaStreamEndCapture(c.stream, &g));
+      SE_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+      cudaGraphDestroy(g);
+      gnodes = (int)(c.launches - before);
+      c.launches = before;
+      gmode = mode;
+    }
+    for (int q = 0; q < count; ++q) SE_CUDA(cudaGraphLaunch(gexec, c.stream));
+    c.launches += (long)gnodes * count;
+  }
+
+  double dot(const double* x, const double* y) {
+    k::dot_dev(c, s, n, x, y, dscal);
+    double h = 0.0;
+    SE_CUDA(cudaMemcpyAsync(&h, dscal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+  }
+
+  void download(const double* d, int count, Vec& out, int offset = 0) {
+    out.resize(count);
+    if (count <= 0) return;
+    SE_CUDA(cudaMemcpyAsync(out.data(), d + offset, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                            c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+  }
+};
+
+// ---- projected eigenproblems ------------------------------------------------------------------
+// Dense symmetric eigen-decomposition with vectors left on the device (column j <-> values[j],
+// ascending).  Small problems run on the host (launch latency dominates); larger ones through
+// cuSOLVER syevd (the reference's O(m^3) host Householder+QL, dense_eig.hpp:114-139).
+struct DevEig {
+  Ctx& c;
+  double* dA = nullptr;
+  double* dW = nullptr;
+  double* work = nullptr;
+  int* info = nullptr;
+  int cap = 0;
+  int lwork = 0;
+  explicit DevEig(Ctx& cc) : c(cc) {}
+  ~DevEig() {
+    cudaStreamSynchronize(c.stream);
+    for (void* p : {(void*)dA, (void*)dW, (void*)work, (void*)info}) dev_free(p);
+  }
+  // H: m x m column-major host.  Returns device pointer to eigenvectors (ld = m).
+  const double* solve(int m, const Vec& H, Vec& values) {
+    if (m > cap) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      dev_free(dA);
+      dev_free(dW);
+      dev_free(info);
+      cap = grow(m);
+      dA = dev_alloc<double>((size_t)cap * cap);
+      dW = dev_alloc<double>(cap);
+      info = dev_alloc<int>(1);
+    }
+    if (m <= 160) {
+      Vec vecs;
+      dense_sym_eig(m, H.data(), true, values, vecs);
+      SE_CUDA(cudaMemcpyAsync(dA, vecs.data(), sizeof(double) * (size_t)m * m,
+                              cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      return dA;
+    }
+    SE_CUDA(cudaMemcpyAsync(dA, H.data(), sizeof(double) * (size_t)m * m, cudaMemcpyHostToDevice,
+                            c.stream));
+    int lw = 0;
+    if (cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
+                                    dA, m, dW, &lw) != CUSOLVER_STATUS_SUCCESS)
+      fail(SE_ECUDA, "cusolverDnDsyevd_bufferSize failed");
+    if (lw > lwork) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      dev_free(work);
+      lwork = lw;
+      work = dev_alloc<double>(lwork);
+    }
+    if (cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, dA, m, dW,
+                         work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+      fail(SE_ECUDA, "cusolverDnDsyevd failed");
+    ++c.launches;
+    int hinfo = 0;
+    values.resize(m);
+    SE_CUDA(cudaMemcpyAsync(values.data(), dW, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    if (hinfo != 0) fail(SE_ENUMERIC, "dense_sym_eig: syevd did not converge");
+    return dA;
+  }
+};
+
+// ---- candidate evaluation (eigensolvers.hpp:275-318) --------------------------------------------
+struct CandBuf {
+  Ctx& c;
+  DevMat U, AU;
+  double* stats = nullptr;
+  int stats_cap = 0;
+  explicit CandBuf(Ctx& cc) : c(cc) {}
+  ~CandBuf() {
+    cudaStreamSynchronize(c.stream);
+    devmat_free(U);
+    devmat_free(AU);
+    dev_free(stats);
+  }
+  // U = W[:, :steps] Y (Y steps x nc, ld ldy), AU = A U, stats per column.
+  void eval(const DevCsr& A, const double* W, int steps, const double* Y, int ldy, int nc,
+            Vec& out3) {
+    const int n = A.n;
+    devmat_reserve(c, U, n, nc, false);
+    devmat_reserve(c, AU, n, nc, false);
+    if (nc > stats_cap) {
+      dev_free(stats);
+      stats_cap = grow(nc);
+      stats = dev_alloc<double>(3 * (size_t)stats_cap);
+    }
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, nc, steps, &one, W, n, Y, ldy, &zero, U.p,
+                    n) != CUBLAS_STATUS_SUCCESS)
+      fail(SE_ECUDA, "cublasDgemm (Ritz combinations) failed");
+    ++c.launches;
+    for (int j0 = 0; j0 < nc; j0 += 65535) {
+      k::ChebArgs a;
+      a.x = U.col(j0);
+      a.y = AU.col(j0);
+      a.ncols = std::min(65535, nc - j0);
+      k::spmv_cheb(c, A, k::kPlain, a);
+    }
+    k::candidate_stats(c, n, nc, U.p, AU.p, stats);
+    out3.resize(3 * (size_t)nc);
+    SE_CUDA(cudaMemcpyAsync(out3.data(), stats, sizeof(double) * 3 * nc, cudaMemcpyDeviceToHost,
+                            c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+  }
+};
+
+// ---- slice state (SliceSolve eigensolvers.hpp:155-346) -----------------------------------------
+struct Slice {
+  Ctx& c;
+  const DevCsr& A;
+  SolverCfg cfg;
+  double bar, xi, eta;
+  Rng rng;
+  se_counters cnt{};
+  Vec lock_val, lock_res;
+  int preloaded = 0;
+  StepOp op;
+  Krylov kr;
+  DevEig eig;
+  CandBuf cand;
+
+  Slice(Ctx& cc, const DevCsr& a, const PolyFilter& f, double xi_, double eta_,
+        const SolverCfg& cf)
+      : c(cc), A(a), cfg(cf), bar(f.bar), xi(xi_), eta(eta_), rng(cf.seed), op(make_op(f)),
+        kr(cc, a, op), eig(cc), cand(cc) {}
+
+  static StepOp make_op(const PolyFilter& f) {
+    StepOp o;
+    o.plain = false;
+    o.k = f.k;
+    o.mu = f.mu;
+    o.c = f.c;
+    o.invd = 1.0 / f.d;
+    return o;
+  }
+
+  double bar_eff() const { return bar * (1.0 - 1e-4); }
+  double stagnation_tol(double tnew) const {
+    return cfg.tau1 > 0.0 ? cfg.tau1 : std::max(1e-12, 1e-10 * std::abs(tnew));
+  }
+  bool in_slice(double lam) const {
+    const double slo = 10.0 * cfg.res_tol * std::max(1.0, std::abs(xi));
+    const double shi = 10.0 * cfg.res_tol * std::max(1.0, std::abs(eta));
+    return lam >= xi - slo && lam <= eta + shi;
+  }
+  bool converged(double lam, double r) const { return r <= cfg.res_tol * std::max(1.0, std::abs(lam)); }
+
+  // start_pair (eigensolvers.hpp:231-261), standard problem: W[:, col].
+  void start_vector(int col) {
+    const int n = A.n;
+    Vec w(n);
+    for (int attempt = 0; attempt < 16; ++attempt) {
+      rng.normal_fill(w.data(), n);
+      double* d = kr.W.col(col);
+      SE_CUDA(cudaMemcpyAsync(d, w.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      if (kr.nlock > 0) k::project_out(c, kr.s, n, kr.nlock, kr.L.p, d, kr.coef_l);
+      const double nb = std::sqrt(kr.dot(d, d));
+      if (nb > 1e-14) {
+        k::scale(c, n, 1.0 / nb, d);
+        return;
+      }
+    }
+    fail(SE_ENUMERIC, "eigensolver: could not draw a start vector outside the locked set");
+  }
+
+  void lock(const double* u_raw, double uu, double lam, double res) {
+    kr.ensure(kr.W.cap, kr.nlock + 1);
+    k::scale_copy(c, A.n, 1.0 / std::sqrt(uu), u_raw, kr.L.col(kr.nlock));
+    ++kr.nlock;
+    lock_val.push_back(lam);
+    lock_res.push_back(res);
+  }
+
+  void preload(int ndefl, const double* u, const double* vals, const char* who) {
+    if (ndefl <= 0) return;
+    const int n = A.n;
+    kr.ensure(std::max(kr.W.cap, 1), ndefl);
+    SE_CUDA(cudaMemcpyAsync(kr.L.p, u, sizeof(double) * (size_t)n * ndefl, cudaMemcpyHostToDevice,
+                            c.stream));
+    double* G = dev_alloc<double>((size_t)ndefl * ndefl);
+    const double one = 1.0, zero = 0.0;
+    cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, ndefl, ndefl, n, &one, kr.L.p, n, kr.L.p, n,
+                &zero, G, ndefl);
+    ++c.launches;
+    Vec g((size_t)ndefl * ndefl);
+    SE_CUDA(cudaMemcpyAsync(g.data(), G, sizeof(double) * g.size(), cudaMemcpyDeviceToHost, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    dev_free(G);
+    for (int j = 0; j < ndefl; ++j)
+      for (int i = 0; i <= j; ++i)
+        if (std::abs(g[(size_t)j * ndefl + i] - (i == j ? 1.0 : 0.0)) > 1e-10)
+          fail(SE_EINVAL, std::string(who) + ": deflation set is not (B-)orthonormal to 1e-10");
+    kr.nlock = ndefl;
+    preloaded = ndefl;
+    lock_val.assign(vals, vals + ndefl);
+    lock_res.assign(ndefl, 0.0);
+  }
+
+  void add_timers() {
+    const Ctl h = kr.get();
+    cnt.t_mv = h.t_mv_ns * 1e-9;
+    cnt.t_orth = h.t_orth_ns * 1e-9;
+  }
+
+  // Everything locked past the preload, ascending (eigensolvers.hpp:328-345).
+  std::unique_ptr<SliceResult> results(long its, bool warn, double t0) {
+    auto r = std::make_unique<SliceResult>();
+    const int k = kr.nlock - preloaded;
+    std::vector<int> idx(k);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::sort(idx.begin(), idx.end(),
+              [&](int i, int j) { return lock_val[preloaded + i] < lock_val[preloaded + j]; });
+    r->n = A.n;
+    if (k > 0) devmat_reserve(c, r->vectors, A.n, k, false);
+    for (int q = 0; q < k; ++q) {
+      const int src = preloaded + idx[q];
+      r->eigenvalues.push_back(lock_val[src]);
+      r->residuals.push_back(lock_res[src]);
+      SE_CUDA(cudaMemcpyAsync(r->vectors.col(q), kr.L.col(src), sizeof(double) * A.n,
+                              cudaMemcpyDeviceToDevice, c.stream));
+    }
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    add_timers();
+    cnt.t_total += now_s() - t0;
+    r->niter = its;
+    r->hit_max_its = warn;
+    r->counters = cnt;
+    return r;
+  }
+
+  // Candidate rows ylast for thick restart: Y[steps-1, j] for the candidate columns.
+  Vec last_row(const double* Y, int steps, int j0, int nc) {
+    Vec out(nc);
+    if (nc == 0) return out;
+    SE_CUDA(cudaMemcpy2DAsync(out.data(), sizeof(double), Y + (size_t)j0 * steps + (steps - 1),
+                              sizeof(double) * steps, sizeof(double), nc, cudaMemcpyDeviceToHost,
+                              c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    return out;
+  }
+};
+
+double sum_above(const Vec& vals, double bar) {
+  double s = 0.0;
+  for (double th : vals)
+    if (th >= bar) s += th;
+  return s;
+}
+
+// ---- run_nr (eigensolvers.hpp:385-472) -----------------------------------------------------------
+std::unique_ptr<SliceResult> run_nr(Slice& s) {
+  const double t0 = now_s();
+  const int n = s.A.n;
+  const long budget = std::min<long>(s.cfg.max_its, n);
+  Krylov& kr = s.kr;
+  const int nc = s.cfg.ncycle;
+  kr.ensure((int)std::min<long>(budget + 1, 2 * nc + 2), std::max(kr.nlock, 0));
+  s.start_vector(0);
+  kr.begin(0);
+  double told = std::numeric_limits<double>::quiet_NaN();
+  bool stagnant = false;
+  long its = 0;
+  while (true) {
+    // advance to the next check point (its % ncycle == 0) or the budget
+    const long target = std::min(budget, (its / nc + 1) * (long)nc);
+    kr.ensure((int)target + 1, kr.nlock);
+    kr.run(0, (int)(target - its));
+    const Ctl h = kr.get();
+    bool breakdown = false;
+    if (h.halted) {
+      breakdown = true;
+      its = h.i + 1;
+    } else {
+      its = target;
+    }
+    const bool last = breakdown || its >= budget;
+    if (its % nc == 0 || last) {
+      Vec al, be;
+      kr.download(kr.alpha, (int)its, al);
+      kr.download(kr.beta, (int)its - 1, be);
+      if (!stagnant && !last) {
+        Vec vals, vecs;
+        sym_tridiag_eig(al, be, false, vals, vecs);
+        const double tnew = sum_above(vals, s.bar);
+        if (!std::isnan(told) && std::abs(tnew - told) < s.stagnation_tol(tnew)) stagnant = true;
+        told = tnew;
+      }
+      if (stagnant || last) {
+        const int m = (int)its;
+        Vec H((size_t)m * m, 0.0);
+        for (int i = 0; i < m; ++i) H[(size_t)i * m + i] = al[i];
+        for (int i = 0; i + 1 < m; ++i) H[(size_t)i * m + i + 1] = H[(size_t)(i + 1) * m + i] = be[i];
+        Vec vals;
+        const double* Y = s.eig.solve(m, H, vals);
+        int j0 = m;
+        while (j0 > 0 && vals[j0 - 1] >= s.bar_eff()) --j0;
+        const int ncand = m - j0;
+        Vec st;
+        if (ncand > 0) s.cand.eval(s.A, kr.W.p, m, Y + (size_t)j0 * m, m, ncand, st);
+        s.cnt.n_A_matvec += ncand;
+        std::vector<int> accepted;
+        bool pending = false;
+        for (int q = ncand - 1; q >= 0; --q) {  // top-down, eigensolvers.hpp:449
+          const double lam = st[3 * q], res = st[3 * q + 1], uu = st[3 * q + 2];
+          if (!(uu > 0.0) || !s.in_slice(lam)) continue;
+          if (s.converged(lam, res))
+            accepted.push_back(q);
+          else
+            pending = true;
+        }
+        if (!pending || last) {
+          for (int q : accepted) s.lock(s.cand.U.col(q), st[3 * q + 2], st[3 * q], st[3 * q + 1]);
+          s.cnt.n_A_matvec += (long)s.op.k * its;
+          return s.results(its, pending, t0);
+        }
+      }
+    }
+  }
+}
+
+// ---- run_tr (eigensolvers.hpp:481-628) -----------------------------------------------------------
+std::unique_ptr<SliceResult> run_tr(Slice& s) {
+  const double t0 = now_s();
+  const int n = s.A.n;
+  const int m = std::min(s.cfg.m, n);
+  const long budget = s.cfg.max_its;
+  const int tr_cap = std::max(1, m / 2);
+  const int ncyc = s.cfg.ncycle;
+  Krylov& kr = s.kr;
+  kr.ensure(m + 1, std::max(kr.nlock, 1));
+  Vec tr_theta, tr_s;
+  long its = 0;
+  int empty_cycles = 0;
+  bool warn = false;
+  while (true) {
+    const int l = (int)tr_theta.size();
+    if (l == 0) s.start_vector(0);
+    SE_CUDA(cudaMemsetAsync(kr.hdiag, 0, sizeof(double) * kr.arr_cap, s.c.stream));
+    kr.begin(l);
+    // arrowhead part of the projected matrix reduced once per cycle (checks are O(steps^2))
+    Vec adiag, aoff;
+    arrow_to_tridiag(tr_theta, tr_s, 0.0, adiag, aoff);
+    int steps = l;
+    bool broke = false;
+    double trailing = 0.0;
+    double told = std::numeric_limits<double>::quiet_NaN();
+    int i = l;  // next step index
+    while (i < m) {
+      // next event: stagnation check after step i_c where (i_c + 1 - l) % ncycle == 0, the end
+      // of the cycle, or the budget
+      int stop = m;  // exclusive end step
+      const int next_check = l + ((i - l) / ncyc + 1) * ncyc;
+      if (next_check < m) stop = next_check;
+      stop = (int)std::min<long>(stop, i + (budget - its));
+      kr.run(1, stop - i);
+      const Ctl h = kr.get();
+      if (h.halted) {
+        const int ib = h.i;  // breakdown at step ib
+        its += ib - i + 1;
+        steps = ib + 1;
+        broke = true;
+        trailing = 0.0;
+        break;
+      }
+      its += stop - i;
+      steps = stop;
+      i = stop;
+      Vec bl;
+      kr.download(kr.beta, 1, bl, steps - 1);
+      trailing = bl[0];
+      if (its >= budget) break;
+      if ((steps - l) % ncyc == 0 && steps < m) {
+        Vec hd, be;
+        kr.download(kr.hdiag, steps - l, hd, l);
+        kr.download(kr.beta, steps - l - 1, be, l);
+        Vec d(adiag.begin(), adiag.end()), e(aoff.begin(), aoff.end());
+        d[l] = hd[0];
+        for (int q = 1; q < steps - l; ++q) d.push_back(hd[q]);
+        for (double b : be) e.push_back(b);
+        Vec vals, unused;
+        sym_tridiag_eig(d, e, false, vals, unused);
+        const double tnew = sum_above(vals, s.bar);
+        if (!std::isnan(told) && std::abs(tnew - told) < s.stagnation_tol(tnew)) break;
+        told = tnew;
+      }
+    }
+    // projected matrix H[0:steps, 0:steps] (arrowhead + tridiagonal)
+    Vec hd, be;
+    kr.download(kr.hdiag, steps - l, hd, l);
+    kr.download(kr.beta, std::max(steps - l - 1, 0), be, l);
+    Vec H((size_t)steps * steps, 0.0);
+    auto at = [&](int r, int cc) -> double& { return H[(size_t)cc * steps + r]; };
+    for (int j = 0; j < l; ++j) {
+      at(j, j) = tr_theta[j];
+      at(j, l) = at(l, j) = tr_s[j];
+    }
+    for (int q = l; q < steps; ++q) at(q, q) = hd[q - l];
+    for (int q = l; q + 1 < steps; ++q) at(q + 1, q) = at(q, q + 1) = be[q - l];
+    Vec vals;
+    const double* Y = s.eig.solve(steps, H, vals);
+    int j0 = steps;
+    while (j0 > 0 && vals[j0 - 1] >= s.bar_eff()) --j0;
+    const int ncand = steps - j0;
+    Vec st;
+    if (ncand > 0) s.cand.eval(s.A, kr.W.p, steps, Y + (size_t)j0 * steps, steps, ncand, st);
+    s.cnt.n_A_matvec += ncand;
+    const Vec ylast = s.last_row(Y, steps, j0, ncand);
+    struct TrC {
+      double theta, ylast;
+      int col;
+    };
+    std::vector<TrC> trset;
+    int found = 0;
+    for (int q = ncand - 1; q >= 0; --q) {
+      const double lam = st[3 * q], res = st[3 * q + 1], uu = st[3 * q + 2];
+      if (!(uu > 0.0) || !s.in_slice(lam)) continue;
+      ++found;
+      if (s.converged(lam, res))
+        s.lock(s.cand.U.col(q), uu, lam, res);
+      else
+        trset.push_back({vals[j0 + q], ylast[q], q});
+    }
+    if (found == 0) {
+      if (++empty_cycles >= 2) break;
+    } else {
+      empty_cycles = 0;
+    }
+    if (its >= budget) {
+      warn = !trset.empty();
+      break;
+    }
+    std::sort(trset.begin(), trset.end(), [](const TrC& x, const TrC& y) { return x.theta > y.theta; });
+    if ((int)trset.size() > tr_cap) trset.resize(tr_cap);
+    tr_theta.clear();
+    tr_s.clear();
+    if (!broke) {
+      const int lnew = (int)trset.size();
+      if (lnew != steps)
+        SE_CUDA(cudaMemcpyAsync(kr.W.col(lnew), kr.W.col(steps), sizeof(double) * n,
+                                cudaMemcpyDeviceToDevice, s.c.stream));
+      for (int q = 0; q < lnew; ++q) {
+        tr_theta.push_back(trset[q].theta);
+        tr_s.push_back(trailing * trset[q].ylast);
+        SE_CUDA(cudaMemcpyAsync(kr.W.col(q), s.cand.U.col(trset[q].col), sizeof(double) * n,
+                                cudaMemcpyDeviceToDevice, s.c.stream));
+      }
+    }
+  }
+  s.cnt.n_A_matvec += (long)s.op.k * its;
+  return s.results(its, warn, t0);
+}
+
+}  // namespace
+
+SolverCfg resolve_config(const se_solver_cfg* in, const char* who) {
+  se_solver_cfg z{0, 0, 30, 0.0, 1e-8, 20, 1234};
+  const se_solver_cfg& q = in ? *in : z;
+  SolverCfg c;
+  if (q.est_count < 0) fail(SE_EINVAL, std::string(who) + ": negative est_count");
+  c.est_count = q.est_count;
+  c.m = q.m == 0 ? std::max(4 * q.est_count, 80) : q.m;
+  c.max_its = q.max_its == 0 ? 40L * q.est_count + 300 : q.max_its;
+  c.ncycle = q.ncycle;
+  c.tau1 = q.tau1;
+  c.res_tol = q.res_tol;
+  c.seed = q.seed;
+  if (c.m < 4) fail(SE_EINVAL, std::string(who) + ": restart dimension m < 4");
+  if (c.ncycle < 1) fail(SE_EINVAL, std::string(who) + ": ncycle < 1");
+  if (!(c.res_tol > 0.0)) fail(SE_EINVAL, std::string(who) + ": res_tol <= 0");
+  if (c.max_its < 1) fail(SE_EINVAL, std::string(who) + ": max_its < 1");
+  return c;
+}
+
+void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const double* v,
+                      double* out) {
+  const int n = a.n;
+  if (op.plain) {
+    k::ChebArgs q;
+    q.x = v;
+    q.y = out;
+    q.ncols = nvec;
+    k::spmv_cheb(c, a, k::kPlain, q);
+    return;
+  }
+  if (op.k < 1) fail(SE_EINVAL, "apply_pol: filter degree must be >= 1");
+  double* fb[3];
+  for (double*& b : fb) b = dev_alloc<double>(n);
+  try {
+    for (int col = 0; col < nvec; ++col) {
+      const double* x = v + (size_t)col * n;
+      double* o = out + (size_t)col * n;
+      k::ChebArgs a1;
+      a1.c = op.c;
+      a1.invd = op.invd;
+      a1.x = x;
+      a1.y = fb[0];
+      a1.out = o;
+      a1.mu0 = op.mu[0];
+      a1.muj = op.mu[1];
+      k::spmv_cheb(c, a, k::kFirst, a1);
+      int cur = 0, prv = -1, nxt = 1;
+      for (int j = 2; j <= op.k; ++j) {
+        k::ChebArgs b = a1;
+        b.x = fb[cur];
+        b.prev = prv < 0 ? x : fb[prv];
+        b.y = fb[nxt];
+        b.muj = op.mu[j];
+        k::spmv_cheb(c, a, k::kNext, b);
+        const int old = prv < 0 ? 2 : prv;
+        prv = cur;
+        cur = nxt;
+        nxt = old;
+      }
+    }
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+  } catch (...) {
+    for (double* b : fb) dev_free(b);
+    throw;
+  }
+  for (double* b : fb) dev_free(b);
+}
+
+// lanczos_run (lanczos.hpp:37-118), euclidean inner product.
+LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m, bool want_basis) {
+  const int n = a.n;
+  m = std::min(m, n);
+  StepOp op;  // plain A
+  Krylov kr(c, a, op);
+  kr.ensure(m + 1, 0);
+  SE_CUDA(cudaMemcpyAsync(kr.W.col(0), start_host, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+  const double nb2 = kr.dot(kr.W.col(0), kr.W.col(0));
+  if (nb2 <= 0.0) fail(SE_ENUMERIC, "lanczos_run: B-inner product is not positive");
+  k::scale(c, n, 1.0 / std::sqrt(nb2), kr.W.col(0));
+  kr.begin(0);
+  kr.run(0, m);
+  const Ctl h = kr.get();
+  LanczosRun r;
+  r.steps = h.halted ? h.i + 1 : m;
+  r.breakdown = h.halted != 0;
+  kr.download(kr.alpha, r.steps, r.alpha);
+  Vec be;
+  kr.download(kr.beta, r.steps, be);
+  if (r.breakdown) {
+    r.beta.assign(be.begin(), be.begin() + std::max(r.steps - 1, 0));
+    r.next_beta = 0.0;
+  } else {
+    r.beta.assign(be.begin(), be.begin() + (r.steps - 1));
+    r.next_beta = be[r.steps - 1];
+    kr.download(kr.W.col(r.steps), n, r.next_w);
+  }
+  if (want_basis) kr.download(kr.W.p, (int)((size_t)n * r.steps), r.basis);
+  return r;
+}
+
+// lan_tr_bounds (lanczos.hpp:148-277): keep the two extreme Ritz pairs across restarts.
+void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max_restarts,
+                   std::uint64_t seed, double& lmin, double& lmax) {
+  const int n = a.n;
+  const int m = std::min(restart_dim, n);
+  if (m < 1) fail(SE_EINVAL, "lan_tr_bounds: empty operator");
+  Rng rng(seed);
+  StepOp op;
+  Krylov kr(c, a, op);
+  kr.ensure(m + 1, 0);
+  CandBuf cand(c);
+  double* dY = dev_alloc<double>((size_t)m * 2);
+  Vec kept_theta, kept_s;
+  double prev_lo = 0.0, prev_hi = 0.0;
+  bool have_prev = false;
+  try {
+    for (int cycle = 0; cycle < max_restarts; ++cycle) {
+      const int k0 = (int)kept_theta.size();
+      if (k0 == 0) {
+        Vec w(n);
+        rng.normal_fill(w.data(), n);
+        SE_CUDA(cudaMemcpyAsync(kr.W.col(0), w.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
+                                c.stream));
+        const double nb = std::sqrt(kr.dot(kr.W.col(0), kr.W.col(0)));
+        k::scale(c, n, 1.0 / nb, kr.W.col(0));
+      }
+      SE_CUDA(cudaMemsetAsync(kr.hdiag, 0, sizeof(double) * kr.arr_cap, c.stream));
+      kr.begin(k0);
+      kr.run(1, m - k0);
+      const Ctl h = kr.get();
+      const bool broke = h.halted != 0;
+      const int steps = broke ? h.i + 1 : m;
+      Vec hd, be;
+      kr.download(kr.hdiag, steps, hd);
+      kr.download(kr.beta, steps, be);
+      const double trailing = broke ? 0.0 : be[steps - 1];
+      Vec H((size_t)steps * steps, 0.0);
+      auto at = [&](int r, int cc) -> double& { return H[(size_t)cc * steps + r]; };
+      for (int j = 0; j < k0; ++j) {
+        at(j, j) = kept_theta[j];
+        at(j, k0) = at(k0, j) = kept_s[j];
+      }
+      for (int q = k0; q < steps; ++q) at(q, q) += hd[q];
+      for (int q = k0; q + 1 < steps; ++q) at(q + 1, q) = at(q, q + 1) = be[q];
+      Vec vals, vecs;
+      dense_sym_eig(steps, H.data(), true, vals, vecs);
+      const double lo = vals.front(), hi = vals.back();
+      const double spread = std::max(hi - lo, 1e-300);
+      const bool settled = have_prev && std::abs(lo - prev_lo) <= tol * spread &&
+                           std::abs(hi - prev_hi) <= tol * spread;
+      if (settled || broke || cycle == max_restarts - 1 || steps >= n) {
+        const double pad_lo = trailing * std::abs(vecs[(size_t)0 * steps + steps - 1]);
+        const double pad_hi = trailing * std::abs(vecs[(size_t)(steps - 1) * steps + steps - 1]);
+        lmin = lo - pad_lo;
+        lmax = hi + pad_hi;
+        dev_free(dY);
+        return;
+      }
+      prev_lo = lo;
+      prev_hi = hi;
+      have_prev = true;
+      kept_theta = {vals[0], vals[steps - 1]};
+      kept_s = {trailing * vecs[(size_t)0 * steps + steps - 1],
+                trailing * vecs[(size_t)(steps - 1) * steps + steps - 1]};
+      SE_CUDA(cudaMemcpyAsync(dY, vecs.data(), sizeof(double) * steps, cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaMemcpyAsync(dY + steps, vecs.data() + (size_t)(steps - 1) * steps,
+                              sizeof(double) * steps, cudaMemcpyHostToDevice, c.stream));
+      Vec st;
+      cand.eval(a, kr.W.p, steps, dY, steps, 2, st);
+      // seed first (column steps -> 2), then the kept combinations into columns 0, 1
+      SE_CUDA(cudaMemcpyAsync(kr.W.col(2), kr.W.col(steps), sizeof(double) * n,
+                              cudaMemcpyDeviceToDevice, c.stream));
+      SE_CUDA(cudaMemcpyAsync(kr.W.col(0), cand.U.col(0), sizeof(double) * 2 * n,
+                              cudaMemcpyDeviceToDevice, c.stream));
+    }
+  } catch (...) {
+    dev_free(dY);
+    throw;
+  }
+  dev_free(dY);
+  fail(SE_ENUMERIC, "lan_tr_bounds: failed to settle");
+}
+
+std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter& f, double xi,
+                                      double eta, const SolverCfg& cfg, bool thick_restart,
+                                      int ndefl, const double* defl_u, const double* defl_vals,
+                                      const char* who) {
+  if (!(eta > xi)) fail(SE_EINVAL, std::string(who) + ": degenerate interval");
+  if (f.k < 1 || (int)f.mu.size() != f.k + 1) fail(SE_EINVAL, std::string(who) + ": malformed filter");
+  Slice s(c, a, f, xi, eta, cfg);
+  s.preload(ndefl, defl_u, defl_vals, who);
+  return thick_restart ? run_tr(s) : run_nr(s);
+}
+
+}  // namespace se

@@ -1,0 +1,84 @@
+// Host-side scalar algorithms of the path (O(k^2) / O(m^2) work that stays on the CPU):
+// filter construction, DOS curve + slicing, small symmetric eigensolvers, Rng streams.
+#pragma once
+
+#include <cstdint>
+#include <random>
+#include <vector>
+
+#include "common.hpp"
+
+namespace se {
+
+using Vec = std::vector<double>;
+
+// ---- rng.hpp:15-61: mt19937_64 + explicit transforms ---------------------------------------
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : g_(seed) {}
+  double uniform() { return double(g_() >> 11) * 0x1.0p-53; }
+  double normal();
+  double rademacher() { return (g_() & 1u) ? 1.0 : -1.0; }
+  void normal_fill(double* out, long n) {
+    for (long i = 0; i < n; ++i) out[i] = normal();
+  }
+  void rademacher_fill(double* out, long n) {
+    for (long i = 0; i < n; ++i) out[i] = rademacher();
+  }
+
+ private:
+  std::mt19937_64 g_;
+  bool spare_ok_ = false;
+  double spare_ = 0.0;
+};
+
+// ---- filter_poly.hpp ----------------------------------------------------------------------
+struct PolyFilter {
+  int k = 0;
+  double gamma = 0.0;
+  Vec mu;
+  double c = 0.0, d = 1.0;
+  double tau = 0.8;
+  double ta = -1.0, tb = 1.0;
+  double bar = 0.0;
+  int damping = SE_DAMP_SIGMA;
+  bool cap_reached = false;
+};
+
+Vec damping_multipliers(int k, int kind);
+Vec chebyshev_coeffs(double gamma, int k);
+double cheb_series(const double* coef, int k, double t);
+double eval_pol(const double* mu, int k, double t);  // throws SE_EINVAL outside [-1-1e-12, 1+1e-12]
+double balance_center(int k, double ta, double tb, int kind);
+Vec normalized_filter_coeffs(int k, double gamma, int kind);
+PolyFilter find_pol(double xi, double eta, double lmin, double lmax, double tau, int max_deg,
+                    int kind);
+
+// ---- dos.hpp / slicer.hpp ------------------------------------------------------------------
+struct Curve {
+  Vec x, y;
+  double nev_est = 0.0;
+  int n = 0;
+};
+Vec dos_grid(double lmin, double lmax, int npts);
+Curve kpm_curve(const Vec& zeta_normalised, int n, double lmin, double lmax, int npts);
+void dos_finalize(Curve& c);
+void add_ritz_gaussians(const Vec& theta, const Vec& tau2, const Vec& x, double sigma, Vec& y);
+double dos_cumulative(const Curve& c, double t);
+double dos_count(const Curve& c, double xi, double eta);
+void slice_spectrum(const Curve& c, double xi, double eta, int ns, Vec& bp, Vec& est);
+
+// ---- tridiag_eig.hpp / dense_eig.hpp --------------------------------------------------------
+// Symmetric tridiagonal eigenproblem (implicit QL, Wilkinson shift); Z (m x m col-major) optional.
+void tridiag_ql(Vec& d, Vec& e, double* z, int ldz, int zrows);
+void sort_eigs(Vec& d, double* z, int m);
+void sym_tridiag_eig(const Vec& alpha, const Vec& beta, bool want, Vec& values, Vec& vectors);
+void dense_sym_eig(int m, const double* a, bool want, Vec& values, Vec& vectors);
+
+// Reduce a thick-restart arrowhead block (diag theta[0..l-1] coupled to index l through s[j],
+// with H(l,l) = alpha_l) to tridiagonal form by Givens rotations acting on indices 0..l-1
+// (index l stays last, so the following Lanczos tail continues the chain).  O(l^2).
+// Output: diag[0..l], off[0..l-1] (off[j] couples j and j+1).
+void arrow_to_tridiag(const Vec& theta, const Vec& s, double alpha_l, Vec& diag, Vec& off);
+
+}  // namespace se

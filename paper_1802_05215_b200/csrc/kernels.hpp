@@ -1,0 +1,106 @@
+// Host-side launchers of the sm_100a kernels (definitions in *.cu).
+//
+// Device-resident control block: every Krylov kernel reads the current column index and the
+// halt flag from `Ctl` in HBM, so one Lanczos step can be captured once as a CUDA graph and
+// replayed without host round trips (the reference's per-step scalar logic, eigensolvers.hpp:
+// 400-471 / 518-560, runs on the device between replays).
+#pragma once
+
+#include "ctx.hpp"
+
+namespace se {
+
+struct Ctl {
+  int i;        // current Krylov column: the step filters W[:, i]
+  int halted;   // set by k_normalize on breakdown (beta <= 1e-14, orth.hpp:14); later kernels no-op
+  int repass;   // DGKS re-pass decision of the current CGS2 (orth.hpp:77)
+  int npass;    // passes executed in the current CGS2
+  int ncols;    // columns the current projection runs over (i+1)
+  int nlock;    // locked columns for deflation (eigensolvers.hpp:205-215)
+  int pad[2];
+  double before, after;  // norms for the DGKS test
+  double alpha, beta;    // NR recurrence scalars
+  double beta_prev;
+  unsigned long long ts0, ts1;  // %globaltimer stamps (ns) for the Counters timers
+  double t_mv_ns, t_orth_ns;    // accumulated filter / orthogonalisation device time
+};
+
+namespace k {
+
+enum ChebMode { kPlain = 0, kFirst = 1, kNext = 2 };
+
+struct ChebArgs {
+  const double* x = nullptr;     // input vector (or base of W when src_ctl != nullptr)
+  const double* prev = nullptr;  // T_{j-2} term (kNext)
+  double* y = nullptr;           // output T_j(Ahat) v (or A x for kPlain)
+  double* out = nullptr;         // running sum sum_j mu_j T_j v
+  double c = 0.0, invd = 1.0;    // map (filter_poly.hpp:259)
+  double mu0 = 0.0, muj = 0.0;
+  const Ctl* src_ctl = nullptr;  // x = x + ctl->i * src_ld when set
+  long src_ld = 0;
+  const Ctl* halt = nullptr;     // skip when halt->halted
+  int ncols = 1;                 // kPlain: column-major batch (blockIdx.y), ld = n
+};
+
+// Fused CSR SpMV + Chebyshev three-term recurrence + mu-accumulation (one filter degree).
+void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args);
+
+// Block KPM step over b <= 16 row-major probe columns (dos.hpp:98-108):
+//   first: w1 = (A w0 - c w0)/d ; zeta[0], zeta[1] partials
+//   next : t  = 2 (A w1 - c w1)/d - w0 ; zeta[k] partial
+// partials are reduced deterministically into zeta_block[b] for moment k.
+struct Scratch;
+size_t kpm_scratch_doubles(const Ctx& c, int n);
+void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, bool first, const double* v,
+              const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
+              int kmom);
+
+// Device Laplacian generator (laplacian.hpp:19-48 in closed form).
+void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a);
+void csr_scale_sym(Ctx& c, DevCsr& a, const double* d_dev);
+int csr_max_row_nnz(Ctx& c, const DevCsr& a);
+
+// ---- Krylov kernels (orth.hpp, lanczos.hpp, eigensolvers.hpp) -----------------------------
+// Scratch owned by the caller (allocated once, outside any graph capture): reduction partials
+// and zero-initialised last-CTA counters (each kernel resets the counters it uses).
+struct Scratch {
+  double* buf = nullptr;
+  size_t cap = 0;  // doubles
+  unsigned* cnt = nullptr;
+  int ncnt = 0;
+};
+// Doubles of scratch a CGS pass over up to `cap_cols` columns of an n-row basis needs.
+size_t cgs_scratch_doubles(const Ctx& c, int n, int cap_cols);
+int cgs_counter_slots(int cap_cols);
+
+// ||t|| -> ctl->before/after; resets the DGKS flags.
+void norm_before(Ctx& c, const Scratch& s, int n, const double* t, Ctl* ctl);
+// NR: t -= beta_arr[i-1] W[:, i-1] (if nonzero); alpha = t . W[:, i] -> ctl->alpha, alpha_arr[i]
+void nr_beta_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, Ctl* ctl,
+                   double* alpha_arr, const double* beta_arr);
+// NR: t -= alpha W[:, i]; before = ||t||
+void nr_sub_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, Ctl* ctl);
+// One classical Gram-Schmidt pass against the columns of Q (count from ctl: i+1, or nlock
+// when use_lock): coef = Q^T t (deterministic), t -= Q coef, after = ||t||, repass flag :=
+// !(after > eta*before).  pass2 executes only when ctl->repass is set.  hdiag (optional):
+// hdiag[i] += coef[i] (TR's H(i,i) += h[i], eigensolvers.hpp:534).  cap = max column count.
+void cgs_pass(Ctx& c, const Scratch& s, int n, double* t, const double* Q, bool use_lock,
+              bool pass2, Ctl* ctl, double* hdiag, double* coef, int cap);
+// t -= Q (Q^T t) with a host-side column count (project_x, eigensolvers.hpp:223-227).
+void project_out(Ctx& c, const Scratch& s, int n, int kq, const double* Q, double* t,
+                 double* coef);
+// beta = after; breakdown -> halted; else W[:, i+1] = t * (1/beta), beta_arr[i] = beta, i++.
+void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W, Ctl* ctl,
+                    double* beta_arr);
+// Candidate statistics (eigensolvers.hpp:289-316) per column of U (n x nc) and AU:
+// out3[3j..] = (lambda, residual, uu).  U is left unscaled (raw W y, kept for thick restart).
+void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3);
+void dot_dev(Ctx& c, const Scratch& s, int n, const double* x, const double* y, double* result_dev);
+void scale(Ctx& c, int n, double a, double* x);
+// dst = a * src (n doubles).
+void scale_copy(Ctx& c, int n, double a, const double* src, double* dst);
+// Device-time stamps: which 0 = filter start, 1 = filter end / orth start, 2 = orth end.
+void stamp(Ctx& c, Ctl* ctl, int which);
+
+}  // namespace k
+}  // namespace se

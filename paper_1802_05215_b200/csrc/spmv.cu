@@ -1,0 +1,335 @@
+// Sparse kernels for sm_100a: the fused Chebyshev-filter SpMV (K1 of SURVEY.md §2.1), the block
+// KPM moment step (K3), and the device stencil generator (K8).
+//
+// Numerics: every product and sum is rounded individually (__dmul_rn / __dadd_rn, no FMA
+// contraction) and each row is summed in storage order, exactly like the reference's scalar loops
+// (CsrMatrix::matvec csr.hpp:98-105, apply_pol filter_poly.hpp:256-277, kpm_dos dos.hpp:96-108),
+// which are compiled for baseline x86-64 without FMA.  The filter application is therefore
+// bit-identical to the reference's on the same input vector.
+#include <cub/cub.cuh>
+
+#include "kernels.hpp"
+
+namespace se {
+namespace k {
+
+namespace {
+
+constexpr int kRows = 256;    // rows per CTA tile, one per thread
+constexpr int kChunk = 2048;  // nnz staged per pass: 16 KB vals + 8 KB cols of shared memory
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+struct KArgs {
+  const double* x;
+  const double* prev;
+  double* y;
+  double* out;
+  double c, invd, mu0, muj;
+  const Ctl* src_ctl;
+  long src_ld;
+  int x_indirect, prev_indirect;
+  const Ctl* halt;
+};
+
+// One CTA = one tile of kRows consecutive rows.  The tile's nnz range [rp[r0], rp[r0+kRows]) is
+// contiguous in CSR, so it is staged into shared memory with fully coalesced loads; each thread
+// then sums its own row sequentially (reference order) gathering x through L1/L2.  Rows longer
+// than the stage are handled by carrying the accumulator across stage passes.
+template <int MODE>
+__global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restrict__ rp,
+                                                      const int* __restrict__ ci,
+                                                      const double* __restrict__ v, KArgs a) {
+  if (a.halt && a.halt->halted) return;
+  __shared__ double s_v[kChunk];
+  __shared__ int s_c[kChunk];
+  const size_t coff = (size_t)blockIdx.y * n;  // column of a column-major batch (kPlain)
+  const size_t ioff = a.src_ctl ? (size_t)a.src_ctl->i * a.src_ld : 0;
+  const double* __restrict__ x = a.x + coff + (a.x_indirect ? ioff : 0);
+  const int r0 = blockIdx.x * kRows;
+  const int r = r0 + threadIdx.x;
+  const int rend = min(r0 + kRows, n);
+  const int base = __ldg(rp + r0), end = __ldg(rp + rend);
+  int rs = end, re = end;
+  if (r < n) {
+    rs = __ldg(rp + r);
+    re = __ldg(rp + r + 1);
+  }
+  double acc = 0.0;
+  for (int c0 = base; c0 < end; c0 += kChunk) {
+    const int cn = min(kChunk, end - c0);
+    for (int q = threadIdx.x; q < cn; q += kRows) {
+      s_v[q] = __ldg(v + c0 + q);
+      s_c[q] = __ldg(ci + c0 + q);
+    }
+    __syncthreads();
+    int p = max(rs, c0) - c0;
+    const int pe = min(re, c0 + cn) - c0;
+    for (; p + 4 <= pe; p += 4) {
+      const double x0 = __ldg(x + s_c[p]), x1 = __ldg(x + s_c[p + 1]);
+      const double x2 = __ldg(x + s_c[p + 2]), x3 = __ldg(x + s_c[p + 3]);
+      acc = add(acc, mul(s_v[p], x0));
+      acc = add(acc, mul(s_v[p + 1], x1));
+      acc = add(acc, mul(s_v[p + 2], x2));
+      acc = add(acc, mul(s_v[p + 3], x3));
+    }
+    for (; p < pe; ++p) acc = add(acc, mul(s_v[p], __ldg(x + s_c[p])));
+    __syncthreads();
+  }
+  if (r >= n) return;
+  double* __restrict__ y = a.y + coff;
+  if (MODE == kPlain) {
+    y[r] = acc;
+    return;
+  }
+  // Ahat x = (A x - c x) * (1/d)   (filter_poly.hpp:265)
+  const double xr = x[r];
+  const double t = mul(sub(acc, mul(a.c, xr)), a.invd);
+  if (MODE == kFirst) {
+    y[r] = t;
+    // out = 0 + mu0 v ; out += mu1 T_1 v   (filter_poly.hpp:261-262, 269)
+    a.out[r] = add(add(0.0, mul(a.mu0, xr)), mul(a.muj, t));
+  } else {
+    const double* __restrict__ prev = a.prev + (a.prev_indirect ? ioff : 0);
+    // T_j = 2 Ahat T_{j-1} - T_{j-2} ; out += mu_j T_j   (filter_poly.hpp:272-275)
+    const double tj = sub(mul(2.0, t), prev[r]);
+    y[r] = tj;
+    a.out[r] = add(a.out[r], mul(a.muj, tj));
+  }
+}
+
+// ---- block KPM step --------------------------------------------------------------------------
+// Probes stored row-major (n x kB, kB = 16 lanes; b <= 16 live).  A half-warp owns one row; lane
+// j owns probe j and sums that row in storage order (bitwise the reference's per-probe matvec).
+// The moment dot v_j . T_k v_j is reduced deterministically: per-CTA partials + last-CTA sum.
+constexpr int kB = 16;
+constexpr int kKpmThreads = 256;
+
+__global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
+    int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
+    int b, int first, const double* __restrict__ v, const double* __restrict__ w0,
+    const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
+    double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
+  const int lane = threadIdx.x & (kB - 1);
+  const int hw = (blockIdx.x * kKpmThreads + threadIdx.x) / kB;  // global half-warp
+  const int nhw = gridDim.x * kKpmThreads / kB;
+  const bool live = lane < b;
+  double acc0 = 0.0, acc1 = 0.0;  // first: v.w0 and v.w1 ; next: v.t
+  for (int r = hw; r < n; r += nhw) {
+    const int s = __ldg(rp + r), e = __ldg(rp + r + 1);
+    const double* __restrict__ src = first ? w0 : w1;
+    double acc = 0.0;
+    if (live) {
+      int p = s;
+      for (; p + 2 <= e; p += 2) {
+        const int c0 = __ldg(ci + p), c1 = __ldg(ci + p + 1);
+        const double a0 = __ldg(vals + p), a1 = __ldg(vals + p + 1);
+        const double x0 = __ldg(src + (size_t)c0 * b + lane);
+        const double x1 = __ldg(src + (size_t)c1 * b + lane);
+        acc = add(acc, mul(a0, x0));
+        acc = add(acc, mul(a1, x1));
+      }
+      if (p < e) acc = add(acc, mul(__ldg(vals + p), __ldg(src + (size_t)__ldg(ci + p) * b + lane)));
+      const size_t o = (size_t)r * b + lane;
+      const double xr = src[o];
+      // (A w - c w) / d   (dos.hpp:99: division by d, unlike the filter's 1/d multiply)
+      const double m = __ddiv_rn(sub(acc, mul(cc, xr)), d);
+      const double vr = v[o];
+      if (first) {
+        t[o] = m;  // w1
+        acc0 = add(acc0, mul(vr, xr));
+        acc1 = add(acc1, mul(vr, m));
+      } else {
+        const double tk = sub(mul(2.0, m), w0[o]);
+        t[o] = tk;
+        acc0 = add(acc0, mul(vr, tk));
+      }
+    }
+  }
+  // Per-CTA reduction of each lane-column: smem[kKpmThreads] -> sum over the 16 half-warps.
+  __shared__ double s0[kKpmThreads], s1[kKpmThreads];
+  __shared__ bool s_last;
+  s0[threadIdx.x] = acc0;
+  s1[threadIdx.x] = acc1;
+  __syncthreads();
+  if (threadIdx.x < kB) {
+    double q0 = 0.0, q1 = 0.0;
+    for (int h = 0; h < kKpmThreads / kB; ++h) {
+      q0 = add(q0, s0[h * kB + threadIdx.x]);
+      q1 = add(q1, s1[h * kB + threadIdx.x]);
+    }
+    partial[(size_t)blockIdx.x * 2 * kB + threadIdx.x] = q0;
+    partial[(size_t)blockIdx.x * 2 * kB + kB + threadIdx.x] = q1;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // Last CTA: columns x {acc0, acc1}, each summed over CTAs in index order by 8 lanes + shuffle.
+  const int col = threadIdx.x >> 3;  // 32 (column, which) pairs, 8 threads each
+  const int sub8 = threadIdx.x & 7;
+  double q = 0.0;
+  for (int blk = sub8; blk < (int)gridDim.x; blk += 8) q = add(q, __ldcg(partial + (size_t)blk * 2 * kB + col));
+  for (int o = 4; o > 0; o >>= 1) q = add(q, __shfl_down_sync(0xffffffffu, q, o, 8));
+  if (sub8 == 0) {
+    const int which = col / kB, j = col % kB;
+    if (j < b) {
+      if (first) {
+        zeta[(size_t)(which) * b + j] = q;  // moments 0 and 1, probe j
+      } else if (which == 0) {
+        zeta[(size_t)kmom * b + j] = q;
+      }
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// ---- device Laplacian generator (laplacian.hpp:19-48) -------------------------------------------
+struct Grid {
+  int nx, ny, nz, ndims;
+};
+
+__device__ __forceinline__ int lap_row_nnz(const Grid& g, int row) {
+  const int i = row % g.nx, j = (row / g.nx) % g.ny, kk = row / (g.nx * g.ny);
+  int c = 1 + (i > 0) + (i < g.nx - 1);
+  if (g.ny > 1) c += (j > 0) + (j < g.ny - 1);
+  if (g.nz > 1) c += (kk > 0) + (kk < g.nz - 1);
+  return c;
+}
+
+__global__ void k_lap_count(Grid g, int n, int* cnt) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) cnt[r] = lap_row_nnz(g, r);
+  if (r == n) cnt[r] = 0;
+}
+
+// Entries in ascending column order: -nx*ny, -nx, -1, diag, +1, +nx, +nx*ny.
+__global__ void k_lap_fill(Grid g, int n, const int* __restrict__ rp, int* __restrict__ ci,
+                           double* __restrict__ v) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = r % g.nx, j = (r / g.nx) % g.ny, kk = r / (g.nx * g.ny);
+  const int plane = g.nx * g.ny;
+  int p = rp[r];
+  if (g.nz > 1 && kk > 0) { ci[p] = r - plane; v[p++] = -1.0; }
+  if (g.ny > 1 && j > 0) { ci[p] = r - g.nx; v[p++] = -1.0; }
+  if (i > 0) { ci[p] = r - 1; v[p++] = -1.0; }
+  ci[p] = r;
+  v[p++] = 2.0 * (double)g.ndims;
+  if (i < g.nx - 1) { ci[p] = r + 1; v[p++] = -1.0; }
+  if (g.ny > 1 && j < g.ny - 1) { ci[p] = r + g.nx; v[p++] = -1.0; }
+  if (g.nz > 1 && kk < g.nz - 1) { ci[p] = r + plane; v[p++] = -1.0; }
+}
+
+__global__ void k_scale_sym(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                            double* __restrict__ v, const double* __restrict__ d) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double dr = d[r];
+  for (int p = rp[r]; p < rp[r + 1]; ++p) v[p] = mul(mul(v[p], dr), d[ci[p]]);
+}
+
+__global__ void k_row_len_max(int n, const int* __restrict__ rp, int* out) {
+  int m = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    m = max(m, rp[r + 1] - rp[r]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+}  // namespace
+
+void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
+  if (a.n == 0) return;
+  KArgs k{args.x, args.prev, args.y, args.out, args.c, args.invd, args.mu0, args.muj,
+          args.src_ctl, args.src_ld, 0, 0, args.halt};
+  // src_ctl indirection applies to the vector that is W[:, i]: x on the first degree, prev on
+  // the second (filter_poly.hpp:260,268-272: prev = v until the first rotation).
+  if (args.src_ctl) {
+    k.x_indirect = (mode == kFirst || mode == kPlain);
+    k.prev_indirect = (mode == kNext);
+  }
+  dim3 grid((a.n + kRows - 1) / kRows, mode == kPlain ? args.ncols : 1);
+  switch (mode) {
+    case kPlain:
+      k_spmv_cheb<kPlain><<<grid, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, k);
+      break;
+    case kFirst:
+      k_spmv_cheb<kFirst><<<grid, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, k);
+      break;
+    default:
+      k_spmv_cheb<kNext><<<grid, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, k);
+  }
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+int kpm_blocks(const Ctx& c, int n) {
+  return std::max(1, std::min(c.num_sms * 8, (int)(((long)n * kB + kKpmThreads - 1) / kKpmThreads)));
+}
+size_t kpm_scratch_doubles(const Ctx& c, int n) { return (size_t)2 * kB * kpm_blocks(c, n); }
+
+void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, bool first, const double* v,
+              const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
+              int kmom) {
+  const int blocks = kpm_blocks(c, a.n);
+  if (kpm_scratch_doubles(c, a.n) > s.cap || s.ncnt < 1) fail(SE_EINVAL, "internal: kpm scratch");
+  k_kpm_step<<<blocks, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, first ? 1 : 0, v, w0,
+                                                   w1, t, cc, d, s.buf, s.cnt, zeta_dev, kmom);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
+  Grid g{dims[0], ndims > 1 ? dims[1] : 1, ndims > 2 ? dims[2] : 1, ndims};
+  const long nl = (long)g.nx * g.ny * g.nz;
+  const int n = (int)nl;
+  a.n = n;
+  a.rp = dev_alloc<int>(n + 1);
+  const int tb = 256;
+  k_lap_count<<<(n + 1 + tb - 1) / tb, tb, 0, c.stream>>>(g, n, a.rp);
+  ++c.launches;
+  size_t tmp_bytes = 0;
+  SE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, a.rp, a.rp, n + 1, c.stream));
+  void* tmp = dev_alloc<char>(tmp_bytes);
+  SE_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, a.rp, a.rp, n + 1, c.stream));
+  SE_CUDA(cudaStreamSynchronize(c.stream));
+  dev_free(tmp);
+  int nnz = 0;
+  SE_CUDA(cudaMemcpyAsync(&nnz, a.rp + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SE_CUDA(cudaStreamSynchronize(c.stream));
+  a.nnz = nnz;
+  a.ci = dev_alloc<int>(nnz);
+  a.v = dev_alloc<double>(nnz);
+  k_lap_fill<<<(n + tb - 1) / tb, tb, 0, c.stream>>>(g, n, a.rp, a.ci, a.v);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+  a.max_row_nnz = 1 + 2 * ndims;
+}
+
+void csr_scale_sym(Ctx& c, DevCsr& a, const double* d_dev) {
+  if (a.n == 0) return;
+  k_scale_sym<<<(a.n + 255) / 256, 256, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, d_dev);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+int csr_max_row_nnz(Ctx& c, const DevCsr& a) {
+  if (a.n == 0) return 0;
+  int* d = dev_alloc<int>(1);
+  SE_CUDA(cudaMemsetAsync(d, 0, sizeof(int), c.stream));
+  k_row_len_max<<<std::min(c.num_sms * 4, (a.n + 255) / 256), 256, 0, c.stream>>>(a.n, a.rp, d);
+  ++c.launches;
+  int h = 0;
+  SE_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SE_CUDA(cudaStreamSynchronize(c.stream));
+  dev_free(d);
+  return h;
+}
+
+}  // namespace k
+}  // namespace se

@@ -1,0 +1,111 @@
+"""GPU parity of the core kernels and drivers against the oracle (C restatement) and, where its
+prebuilt library is present, the reference itself (oracle/_ref)."""
+import numpy as np
+import pytest
+
+from oracle import clib
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_1802_05215_b200 import api
+    return api
+
+
+CFG1_BOUNDS = (0.0010977890680629611, 7.99911827091601)  # reference lan_tr_bounds, cfg1 (seed 0)
+
+
+def test_spmv_bitwise(gpu_ctx):
+    api = _api()
+    a = api.gen_laplacian([100, 100])
+    x = clib.rng_vectors(5, "normal", a.n)[0]
+    y = a.matvec(x)
+    ref = clib.matvec(a.row_ptr, a.col_idx, a.vals, x)
+    assert np.array_equal(y, ref)
+
+
+def test_device_laplacian_generator_bitwise(gpu_ctx):
+    api = _api()
+    for dims in ([7], [5, 4], [4, 3, 5], [64, 64, 64]):
+        d = api.DeviceCsr.laplacian(dims).download()
+        rp, ci, v = clib.laplacian(dims)
+        assert np.array_equal(d.row_ptr, rp) and np.array_equal(d.col_idx, ci)
+        assert np.array_equal(d.vals, v)
+
+
+@pytest.mark.parametrize("dims,slice_,damping", [
+    ([100, 100], (0.4, 1.0443178519), "jackson"),
+    ([100, 100], (1.0443178519, 1.6), "jackson"),
+    ([64, 64, 64], (0.6, 0.7), "sigma"),
+])
+def test_apply_pol_bitwise(gpu_ctx, dims, slice_, damping):
+    api = _api()
+    a = api.gen_laplacian(dims)
+    lo, hi = CFG1_BOUNDS if len(dims) == 2 else (0.0, 12.0)
+    f = api.find_pol(slice_[0], slice_[1], api.SpectralBounds(lo, hi), api.PolyOpts(damping=damping))
+    x = clib.rng_vectors(11, "normal", a.n)[0]
+    cnt = api.Counters()
+    out = api.apply_pol(f, a, x, cnt)
+    ref = clib.apply_pol(a.row_ptr, a.col_idx, a.vals, f.mu, f.c, f.d, x)
+    assert cnt.n_A_matvec == f.k
+    assert np.array_equal(out, ref), np.max(np.abs(out - ref))
+
+
+def test_kpm_moments_match_oracle(gpu_ctx):
+    api = _api()
+    a = api.gen_laplacian([100, 100])
+    lo, hi = CFG1_BOUNDS
+    for probes in ("rademacher", "gaussian"):
+        z = api.kpm_moments(a, api.SpectralBounds(lo, hi), 80, 20, seed=0, probes=probes)
+        zr = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, lo, hi, 80, 20, 0,
+                              kind="normal" if probes == "gaussian" else "rademacher")
+        zn, zrn = z / (20 * a.n), zr / (20 * a.n)
+        tol = 1e-12 * np.maximum(np.abs(zrn), abs(zrn[0]))
+        assert np.all(np.abs(zn - zrn) <= tol), np.max(np.abs(zn - zrn) / np.abs(zrn[0]))
+
+
+def test_lan_tr_bounds_encloses_spectrum(gpu_ctx):
+    api = _api()
+    a = api.gen_laplacian([100, 100])
+    b = api.lan_tr_bounds(a, 1e-4, 60, 40, seed=0)
+    ev = api.laplacian_analytic_eigs([100, 100])
+    assert b.lmin <= ev[0] + 1e-3 and b.lmax >= ev[-1] - 1e-6
+    spread = CFG1_BOUNDS[1] - CFG1_BOUNDS[0]
+    assert abs(b.lmin - CFG1_BOUNDS[0]) <= 1e-4 * spread and abs(b.lmax - CFG1_BOUNDS[1]) <= 1e-4 * spread
+
+
+def test_diagonal_slice(gpu_ctx):
+    api = _api()
+    a = api.CsrMatrix.diag([0.1, 0.5, 0.9])
+    f = api.find_pol(0.4, 0.6, api.SpectralBounds(0.05, 0.95))
+    for drv in (api.cheb_lan_nr, api.cheb_lan_tr):
+        r = drv(a, None, f, 0.4, 0.6)
+        assert len(r.eigenvalues) == 1
+        assert abs(r.eigenvalues[0] - 0.5) <= 1e-12
+        assert r.residuals[0] <= 1e-12
+        assert abs(abs(r.vectors[1, 0]) - 1.0) <= 1e-10
+        assert r.counters.t_total > 0 and not r.hit_max_its
+
+
+@pytest.mark.parametrize("driver", ["nr", "tr"])
+def test_laplacian_60x60_window(gpu_ctx, driver):
+    api = _api()
+    a = api.gen_laplacian([60, 60])
+    allv = api.laplacian_analytic_eigs([60, 60])
+    oracle = allv[(allv >= 0.4) & (allv <= 0.6)]
+    assert oracle.size == 62
+    f = api.find_pol(0.4, 0.6, api.SpectralBounds(allv[0] - 1e-8, allv[-1] + 1e-8))
+    cfg = api.SolverConfig(est_count=62)
+    drv = api.cheb_lan_nr if driver == "nr" else api.cheb_lan_tr
+    r = drv(a, None, f, 0.4, 0.6, cfg)
+    assert r.eigenvalues.size == 62
+    assert np.max(np.abs(r.eigenvalues - oracle)) <= 1e-8
+    assert np.all(r.residuals <= cfg.res_tol)
+    G = r.vectors.T @ r.vectors
+    assert np.max(np.abs(G - np.eye(62))) <= 1e-8
+    assert r.counters.n_A_matvec >= f.k * r.niter
+    for i in range(0, 62, 7):
+        lam, res = api.rayleigh_and_residual(a, None, r.vectors[:, i])
+        assert abs(lam - r.eigenvalues[i]) <= 1e-10
+        assert abs(res - r.residuals[i]) <= 1e-10
