@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- eigenpairs/s of the full sliced solve (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1], "cfg2"): 3-D 7-point Laplacian 64^3 (n = 262,144, fp64 CSR),
+KPM DOS with 100 moments and 40 seeded Gaussian probes, [0.6, 1.2] sliced into 8 by the DOS,
+every slice solved with ChebLanTr (thick-restart filtered Lanczos, sigma damping), tol 1e-8.
+One step = one full pipeline pass: bounds -> KPM -> slicing -> 8 filtered-Lanczos slice solves.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  (N > 1: launched by torch.distributed.run, one rank per GPU; slice i runs on rank i % N and the
+   KPM probes are split across ranks with one all-gather of the per-probe moments.)
+
+`value`  : eigenpairs/s with the matrix already resident in HBM (device generator) at t0.
+`e2e`    : the same pipeline through the public API from a pinned HOST CSR: H2D of the matrix and
+           D2H of all eigenpairs (values + vectors) inside the timed region.
+`roofline`: the fused Chebyshev-filter SpMV kernel (the path's HBM-bound hot kernel), bytes =
+           Abytes + 40 n per degree, timed with CUDA events on its stream.
+`cpu_baseline` / `--impl reference`: the unmodified reference (oracle/_ref, compiled from
+           /root/reference headers) timed on this host's cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG2 = dict(dims=[64, 64, 64], xi=0.6, eta=1.2, ns=8, solver="tr", damping="sigma", dos_m=100,
+            dos_nvec=40, probes="gaussian", tol=1e-8, seed=1234)
+# CPU-boundable proxy of the same recipe (used only for the reference arm / cpu_baseline)
+PROXY = dict(CFG2, dims=[20, 20, 20])
+METRIC = "eigenpairs/sec for full sliced solve"
+UNIT = "eigenpairs/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as td
+        td.barrier()
+
+
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as td
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    td.all_reduce(t, op=td.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as td
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    td.all_reduce(t)
+    return float(t.item())
+
+
+def _plan(cfg, **kw):
+    from paper_1802_05215_b200.pipeline import Plan
+    keys = ("xi", "eta", "ns", "solver", "damping", "dos_m", "dos_nvec", "probes", "tol", "seed")
+    return Plan(**{k: cfg[k] for k in keys}, **kw)
+
+
+def filter_roofline(local_gpu: int, dims, launches_min: int = 400):
+    """Time the fused filter kernel alone (CUDA events on its stream) on the workload's matrix and
+    on a 160^3 matrix (A = 359 MB > L2) -- the latter is the HBM-resident figure."""
+    import ctypes as C
+    import torch
+    from paper_1802_05215_b200 import _lib, api
+    peak, peak_kind = _peaks()
+    out = {}
+    for tag, dd in (("workload", dims), ("hbm_resident_160^3", [160, 160, 160])):
+        ctx = api.Context(local_gpu)
+        A = api.DeviceCsr.laplacian(dd, ctx)
+        f = api.find_pol(1.1691525, 1.2, api.SpectralBounds(0.0, 12.0))  # cfg2-like narrow slice
+        reps = max(1, launches_min // f.k)
+        v = torch.randn(A.n, dtype=torch.float64, device=f"cuda:{local_gpu}")
+        o = torch.empty_like(v)
+        s, keep = f._c()
+        _lib.call("se_cheb_apply_dev", ctx.handle, A.handle, C.byref(s), 1, C.c_void_p(v.data_ptr()),
+                  C.c_void_p(o.data_ptr()))  # warm-up
+        _lib.call("se_ctx_filter_timing", ctx.handle, 1, None, None, None)
+        for _ in range(reps):
+            _lib.call("se_cheb_apply_dev", ctx.handle, A.handle, C.byref(s), 1,
+                      C.c_void_p(v.data_ptr()), C.c_void_p(o.data_ptr()))
+        ms, nl, by = C.c_double(), C.c_long(), C.c_double()
+        _lib.call("se_ctx_filter_timing", ctx.handle, 0, C.byref(ms), C.byref(nl), C.byref(by))
+        per_launch_s = ms.value * 1e-3 / nl.value
+        achieved = by.value / (ms.value * 1e-3) / 1e9
+        out[tag] = {"n": A.n, "nnz": A.nnz, "launches": nl.value, "us_per_launch": per_launch_s * 1e6,
+                    "achieved_GBs": achieved, "bytes_per_launch": by.value / nl.value}
+        A.free()
+        ctx.close()
+    w = out["hbm_resident_160^3"]
+    roof = {"bound": "hbm", "kernel": "k_spmv_cheb<kNext> (fused Chebyshev filter SpMV)",
+            "achieved": round(w["achieved_GBs"], 1), "peak": peak, "unit": "GB/s",
+            "frac": round(w["achieved_GBs"] / peak, 4), "peak_kind": peak_kind,
+            "traffic": None, "matrix": "160^3 7-pt Laplacian (A 359 MB > L2)",
+            "bytes_per_launch": w["bytes_per_launch"],
+            "workload_matrix": {"achieved": round(out["workload"]["achieved_GBs"], 1),
+                                "note": "64^3: A (22.8 MB) + vectors are L2-resident",
+                                "us_per_launch": round(out["workload"]["us_per_launch"], 3)}}
+    return roof
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the unmodified reference pipeline (oracle/_ref) on this host's cores."""
+    if rank != 0:
+        return
+    from oracle import reflib
+    cfg = PROXY
+    cores = os.cpu_count() or 1
+    rp, ci, v = reflib.laplacian(cfg["dims"])
+    res = None
+    for _ in range(args.warmup):
+        reflib.solve(rp, ci, v, cfg["xi"], cfg["eta"], cfg["ns"], cfg["solver"], cfg["damping"],
+                     cfg["dos_m"], cfg["dos_nvec"], 300, "normal", cfg["tol"], cfg["seed"],
+                     jobs=min(cores, cfg["ns"]))
+    t0 = time.perf_counter()
+    found = 0
+    for _ in range(args.steps):
+        res = reflib.solve(rp, ci, v, cfg["xi"], cfg["eta"], cfg["ns"], cfg["solver"],
+                           cfg["damping"], cfg["dos_m"], cfg["dos_nvec"], 300, "normal", cfg["tol"],
+                           cfg["seed"], jobs=min(cores, cfg["ns"]))
+        found += sum(len(s["eigenvalues"]) for s in res["slices"])
+    el = time.perf_counter() - t0
+    val = found / el
+    sample = (f"reference `sliceeig solve` semantics (bounds, KPM 100x40 Gaussian, 8 slices, "
+              f"ChebLanTr tol 1e-8, {min(cores, cfg['ns'])} slice threads) on the CPU-boundable "
+              f"{cfg['dims'][0]}^3 proxy of cfg2 ({found // args.steps} eigenpairs/step); the full "
+              f"64^3 cfg2 takes ~2 h on 8 CPU threads (SURVEY.md §6.2)")
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg2 recipe on {cfg['dims'][0]}^3 proxy (CPU-bounded sample)",
+                       "matrix": "3-D 7-pt Laplacian", "interval": [cfg["xi"], cfg["eta"]],
+                       "slices": cfg["ns"], "solver": "ChebLanTr", "tol": cfg["tol"]},
+            "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": min(cores, cfg["ns"]),
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample():
+    from oracle import reflib
+    if not reflib.available():
+        return None
+    cfg = PROXY
+    cores = os.cpu_count() or 1
+    rp, ci, v = reflib.laplacian(cfg["dims"])
+    t0 = time.perf_counter()
+    res = reflib.solve(rp, ci, v, cfg["xi"], cfg["eta"], cfg["ns"], cfg["solver"], cfg["damping"],
+                       cfg["dos_m"], cfg["dos_nvec"], 300, "normal", cfg["tol"], cfg["seed"],
+                       jobs=min(cores, cfg["ns"]))
+    el = time.perf_counter() - t0
+    found = sum(len(s["eigenvalues"]) for s in res["slices"])
+    return {"value": round(found / el, 4), "unit": UNIT, "cores": min(cores, cfg["ns"]),
+            "kind": "reference",
+            "sample": f"full reference pipeline of the cfg2 recipe on the {cfg['dims'][0]}^3 proxy "
+                      f"({found} eigenpairs in {el:.1f} s, {min(cores, cfg['ns'])} slice threads)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--proxy", action="store_true", help="run the GPU arm on the CPU proxy size")
+    args = ap.parse_args()
+    rank, world, local = _dist_init() if args.impl == "ours" or int(os.environ.get("WORLD_SIZE", "1")) > 1 else (0, 1, 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    from paper_1802_05215_b200 import api
+    from paper_1802_05215_b200.pipeline import Dist, GpuBackend, run
+    torch.cuda.set_device(local)
+    cfg = PROXY if args.proxy else CFG2
+    dist = Dist.from_torch() if world > 1 else Dist()
+    backend = GpuBackend(device=local, dims=cfg["dims"])
+    plan = _plan(cfg)
+    for _ in range(args.warmup):
+        res = run(plan, backend, dist)
+    # ---- timed region: matrix resident in HBM ------------------------------------------------
+    clocks = ClockSampler(local)
+    l0 = backend.launches()
+    _barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    found = 0
+    for _ in range(args.steps):
+        res = run(plan, backend, dist)
+        found += sum(s.eigenvalues.size for s in res.slices if s.rank == rank)
+    torch.cuda.synchronize()
+    e1.record()
+    torch.cuda.synchronize()
+    _barrier(world)
+    clk = clocks.stop()
+    ms = _max_over_ranks(e0.elapsed_time(e1), world)
+    found_all = _sum_over_ranks(found, world)
+    launches = int(_sum_over_ranks(backend.launches() - l0, world))
+    value = found_all / (ms * 1e-3)
+    per_slice = [{"slice": s.index, "lo": round(s.lo, 8), "hi": round(s.hi, 8), "est": round(s.est, 1),
+                  "found": int(s.eigenvalues.size), "degree": s.degree, "niter": s.niter,
+                  "seconds": round(s.seconds, 3), "rank": s.rank, "error": s.error}
+                 for s in res.slices]
+    # ---- end to end through the public API from host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = api.gen_laplacian(cfg["dims"])
+        pinned = {}
+        for nm in ("row_ptr", "col_idx", "vals"):
+            arr = getattr(host, nm)
+            t = torch.from_numpy(arr).pin_memory()
+            pinned[nm] = t.numpy()
+        hcsr = api.CsrMatrix(host.n, pinned["row_ptr"], pinned["col_idx"], pinned["vals"])
+        plan_v = _plan(cfg, want_vectors=True)
+        h2d = hcsr.row_ptr.nbytes + hcsr.col_idx.nbytes + hcsr.vals.nbytes
+        _barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        got = 0
+        for _ in range(args.steps):
+            be = GpuBackend(device=local, matrix=hcsr)  # H2D of the CSR
+            r2 = run(plan_v, be, dist)
+            mine = [s for s in r2.slices if s.rank == rank]
+            got += sum(s.eigenvalues.size for s in mine)
+            d2h += sum(s.eigenvalues.nbytes + s.residuals.nbytes +
+                       (s.vectors.nbytes if s.vectors is not None else 0) for s in mine)
+            be.A.free()
+        torch.cuda.synchronize()
+        el = _max_over_ranks(time.perf_counter() - t0, world)
+        got_all = _sum_over_ranks(got, world)
+        e2e = {"value": round(got_all / el, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(_sum_over_ranks(d2h, world) / args.steps)}
+    roof = filter_roofline(local, cfg["dims"]) if rank == 0 else None
+    cpu = cpu_baseline_sample() if (rank == 0 and world == 1 and not args.no_cpu) else None
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (generated Laplacian, seeded Gaussian/normal probes)",
+                "config": {"workload": f"cfg2: {cfg['dims'][0]}^3 7-pt Laplacian, KPM 100x40 Gaussian, "
+                                       f"[0.6,1.2] in 8 slices, ChebLanTr tol 1e-8",
+                           "n": backend.n, "slices": cfg["ns"], "parallelism": f"slices{world}",
+                           "l2": "working set (Krylov bases ~1-6 GB per slice) >> 126 MB L2; no flush"},
+                "eigenpairs_per_step": int(found_all / args.steps),
+                "per_slice": per_slice, "t_bounds": round(res.t_bounds, 3),
+                "t_dos": round(res.t_dos, 3), "t_solve": round(res.t_solve, 3),
+                "e2e": e2e, "gpu_launches": launches, "roofline": roof, "clocks": clk,
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as td
+        td.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

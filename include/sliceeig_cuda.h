@@ -145,9 +145,12 @@ SE_API int se_eval_pol(const se_poly_filter* f, double t, double* out);       /*
  * device in blocks of up to 16.  zeta_sums has m+1 entries. */
 SE_API int se_kpm_moments(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec,
                    int probe_kind, uint64_t seed, int first, int count, double* zeta_sums);
-/* Same over caller-supplied device probes (column-major n x nprobes); zeta_sums[m+1] host. */
-SE_API int se_kpm_moments_dev(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int nprobes,
-                       const double* d_probes, double* zeta_sums);
+/* Per-probe moments v_l^T T_k(Ahat) v_l for probes [first, first+count): per_probe is
+ * count x (m+1) row-major (probe-major).  Summing rows in probe order reproduces the reference's
+ * accumulation order (dos.hpp:100-106) independently of how probes were split across GPUs. */
+SE_API int se_kpm_moments_probes(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m,
+                                 int n_vec, int probe_kind, uint64_t seed, int first, int count,
+                                 double* per_probe);
 /* Jackson-damped curve from normalised moments (dos.hpp:112-131 + dos_finalize :54-60). */
 SE_API int se_kpm_curve(int m, const double* zeta, int n, double lmin, double lmax, int npts, double* x,
                  double* y, double* nev_est);

@@ -76,7 +76,8 @@ SIGNATURES = {
     "se_eval_pol": [C.POINTER(SePolyFilter), C.c_double, _PD],
     "se_kpm_moments": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_uint64,
                        C.c_int, C.c_int, _PD],
-    "se_kpm_moments_dev": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, _VP, _PD],
+    "se_kpm_moments_probes": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                              C.c_uint64, C.c_int, C.c_int, _PD],
     "se_kpm_curve": [C.c_int, _PD, C.c_int, C.c_double, C.c_double, C.c_int, _PD, _PD, _PD],
     "se_kpm_dos": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
                    _PD, _PD, _PD],

@@ -417,6 +417,18 @@ def kpm_moments(op, bounds: SpectralBounds, m: int, n_vec: int, seed: int = 1234
     return z
 
 
+def kpm_moments_probes(op, bounds: SpectralBounds, m: int, n_vec: int, seed: int = 1234,
+                       probes: str = "rademacher", first: int = 0, count: Optional[int] = None
+                       ) -> np.ndarray:
+    """Per-probe moments (count, m+1) for probes [first, first+count) of the Rng(seed) stream."""
+    d = _dev(op)
+    count = n_vec - first if count is None else count
+    out = np.empty((max(count, 1), m + 1), np.float64)
+    call("se_kpm_moments_probes", d.ctx.handle, d.handle, bounds.lmin, bounds.lmax, m, n_vec,
+         _lib.PROBES[probes], seed, first, count, _pd(out))
+    return out[:count]
+
+
 def kpm_curve(zeta_normalised, n: int, bounds: SpectralBounds, npts: int = 300) -> DosCurve:
     z = _f64(zeta_normalised)
     x = np.empty(npts, np.float64)

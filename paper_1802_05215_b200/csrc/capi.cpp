@@ -415,7 +415,8 @@ constexpr int kBlock = 16;
 
 // dos.hpp:96-109 on the device, probes from one host Rng(seed) stream in probe order.
 void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, int n_vec,
-                      int probe_kind, std::uint64_t seed, int first, int count, Vec& zeta) {
+                      int probe_kind, std::uint64_t seed, int first, int count, Vec& zeta,
+                      Vec* per_probe = nullptr) {
   if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
   if (m < 1 || n_vec < 1) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
   if (a.n < 1) fail(SE_EINVAL, "dos: empty operator");
@@ -423,6 +424,7 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
   const int n = a.n;
   const double cc = 0.5 * (lmax + lmin), d = 0.5 * (lmax - lmin);
   zeta.assign(m + 1, 0.0);
+  if (per_probe) per_probe->assign((size_t)count * (m + 1), 0.0);
   if (count == 0) return;
   Rng rng(seed);
   auto draw = [&](double* out, long len) {
@@ -471,7 +473,10 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
                               cudaMemcpyDeviceToHost, c.stream));
       SE_CUDA(cudaStreamSynchronize(c.stream));
       for (int j = 0; j < b; ++j)  // probe order (dos.hpp:100-106)
-        for (int kk = 0; kk <= m; ++kk) zeta[kk] += hz[(size_t)kk * b + j];
+        for (int kk = 0; kk <= m; ++kk) {
+          zeta[kk] += hz[(size_t)kk * b + j];
+          if (per_probe) (*per_probe)[(size_t)(b0 + j) * (m + 1) + kk] = hz[(size_t)kk * b + j];
+        }
     }
   } catch (...) {
     cudaFreeHost(hbuf);
@@ -494,18 +499,13 @@ int se_kpm_moments(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m
   });
 }
 
-int se_kpm_moments_dev(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int nprobes,
-                       const double* d_probes, double* zeta_sums) {
+int se_kpm_moments_probes(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m,
+                          int n_vec, int probe_kind, uint64_t seed, int first, int count,
+                          double* per_probe) {
   return guard([&] {
-    (void)ctx;
-    (void)a;
-    (void)lmin;
-    (void)lmax;
-    (void)m;
-    (void)nprobes;
-    (void)d_probes;
-    (void)zeta_sums;
-    fail(SE_EINVAL, "se_kpm_moments_dev: not implemented in this build");
+    Vec z, pp;
+    kpm_moments_impl(C(ctx), M(a), lmin, lmax, m, n_vec, probe_kind, seed, first, count, z, &pp);
+    std::copy(pp.begin(), pp.end(), per_probe);
   });
 }
 

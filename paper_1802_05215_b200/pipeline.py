@@ -1,0 +1,293 @@
+"""Sliced-solve pipeline (the semantics of `sliceeig solve`, tools/sliceeig_main.cpp:464-619), one
+process per GPU.
+
+    bounds (lan_tr_bounds tol 1e-4, 60, 40, seed; :128-136)
+ -> KPM density: probes split across ranks, per-probe moments all-gathered and summed in probe
+    order (so the curve is identical for any GPU count), curve + slicing on the host (:138-157)
+ -> slice_clipped (:270-278): outer breakpoints reset to the user's interval
+ -> per slice: est_count = max(1, ceil(est)) (:396-399), find_pol, cheb_lan_nr/tr (:394-418),
+    trim_to_slice with delta = 1e-10 (lmax - lmin) (:422-442, :497)
+
+Slices are independent: slice i runs on rank i % world, and the slices of one rank run
+concurrently, one host thread + CUDA stream each (the reference's std::thread pool,
+:494-523).  The only data-path collective is the KPM all-gather of per-probe moments.
+
+The compute backend is pluggable only so the multi-rank plumbing can be exercised on CPU with
+the test oracle (tests/test_pipeline_dist.py); the product backend is `GpuBackend`.
+"""
+from __future__ import annotations
+
+import math
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import api
+
+
+@dataclass
+class Plan:
+    xi: float
+    eta: float
+    ns: int = 1
+    solver: str = "nr"            # nr | tr
+    damping: str = "sigma"        # sigma | jackson | none
+    dos_m: int = 60
+    dos_nvec: int = 40
+    dos_npts: int = 300
+    probes: str = "rademacher"    # rademacher | gaussian
+    tol: float = 1e-8
+    seed: int = 1234
+    bounds: Optional[tuple] = None  # fixed (lmin, lmax) skips the bounds stage
+    solver_m: int = 0              # SolverConfig.m override (0: reference default)
+    jobs: int = 0                  # concurrent slices per rank (0: all of the rank's slices)
+    want_vectors: bool = False
+
+
+@dataclass
+class SliceOutcome:
+    index: int
+    lo: float
+    hi: float
+    est: float
+    degree: int = 0
+    eigenvalues: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    residuals: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    vectors: Optional[np.ndarray] = None
+    niter: int = 0
+    n_A_matvec: int = 0
+    hit_max_its: bool = False
+    seconds: float = 0.0
+    error: Optional[str] = None
+    rank: int = 0
+
+
+@dataclass
+class PipelineResult:
+    lmin: float
+    lmax: float
+    breakpoints: np.ndarray
+    est_counts: np.ndarray
+    slices: List[SliceOutcome]
+    t_bounds: float
+    t_dos: float
+    t_solve: float
+    t_total: float
+    kernel_launches: int = 0
+
+    @property
+    def eigenvalues(self) -> np.ndarray:
+        vals = [s.eigenvalues for s in sorted(self.slices, key=lambda s: s.index)]
+        return np.concatenate(vals) if vals else np.zeros(0)
+
+    @property
+    def n_found(self) -> int:
+        return int(sum(s.eigenvalues.size for s in self.slices))
+
+
+class Dist:
+    """Rank/world + the two collectives the pipeline needs (torch.distributed when initialised)."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device=None):
+        self.rank, self.world, self.device = rank, world, device
+
+    @classmethod
+    def from_torch(cls):
+        import torch.distributed as td
+        if td.is_available() and td.is_initialized():
+            import torch
+            dev = torch.device("cuda", torch.cuda.current_device()) if td.get_backend() == "nccl" else None
+            return cls(td.get_rank(), td.get_world_size(), dev)
+        return cls()
+
+    def allgather_rows(self, local: np.ndarray, counts: Sequence[int]) -> np.ndarray:
+        """All-gather row blocks (rank r contributes counts[r] rows) in rank order."""
+        if self.world == 1:
+            return local
+        import torch
+        import torch.distributed as td
+        width = local.shape[1]
+        mx = max(counts)
+        buf = np.zeros((mx, width), np.float64)
+        buf[: local.shape[0]] = local
+        t = torch.from_numpy(buf)
+        if self.device is not None:
+            t = t.to(self.device)
+        outs = [torch.empty_like(t) for _ in range(self.world)]
+        td.all_gather(outs, t)
+        return np.concatenate([o.cpu().numpy()[: counts[r]] for r, o in enumerate(outs)])
+
+    def broadcast_f64(self, vals: np.ndarray) -> np.ndarray:
+        if self.world == 1:
+            return vals
+        import torch
+        import torch.distributed as td
+        t = torch.from_numpy(np.ascontiguousarray(vals, np.float64).copy())
+        if self.device is not None:
+            t = t.to(self.device)
+        td.broadcast(t, 0)
+        return t.cpu().numpy()
+
+    def gather_objects(self, obj):
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as td
+        out = [None] * self.world
+        td.all_gather_object(out, obj)
+        return out
+
+
+def probe_split(n_vec: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous probe range [first, first+count) of `rank` (probe order is preserved)."""
+    base, rem = divmod(n_vec, world)
+    first = rank * base + min(rank, rem)
+    return first, base + (1 if rank < rem else 0)
+
+
+def slice_owner(index: int, world: int) -> int:
+    return index % world
+
+
+def trim_to_slice(vals, res, index: int, ns: int, lo: float, hi: float, delta: float):
+    """sliceeig_main.cpp:422-442: an eigenvalue within delta of an interior breakpoint belongs to
+    the slice below it.  Returns the kept positions."""
+    keep = []
+    for i, v in enumerate(vals):
+        if index > 0 and v <= lo + delta:
+            continue
+        if index + 1 < ns and v > hi + delta:
+            continue
+        keep.append(i)
+    return np.asarray(keep, dtype=np.int64)
+
+
+def slice_clipped(curve: api.DosCurve, xi: float, eta: float, ns: int, slicer=None):
+    """sliceeig_main.cpp:187-193 + 270-278."""
+    lo, hi = max(xi, curve.xdos[0]), min(eta, curve.xdos[-1])
+    if not lo < hi:
+        raise ValueError("requested interval does not meet the sampled spectrum")
+    s = (slicer or api.slice_spectrum)(curve, lo, hi, ns)
+    bp = np.array(s.breakpoints, np.float64)
+    bp[0], bp[-1] = xi, eta
+    return bp, np.asarray(s.est_counts, np.float64)
+
+
+class GpuBackend:
+    """The product path: every stage runs through libsliceeig_cuda.so on this rank's GPU."""
+
+    def __init__(self, device: int = 0, matrix=None, dims=None, ctx=None):
+        self.device = device
+        self.ctx = ctx or api.default_context(device)
+        if dims is not None:
+            self.A = api.DeviceCsr.laplacian(dims, self.ctx)
+        elif isinstance(matrix, api.DeviceCsr):
+            self.A = matrix
+        else:
+            self.A = api.DeviceCsr.upload(matrix, self.ctx)
+        self.n = self.A.n
+        self._thread_ctx = {}
+
+    def _ctx(self):
+        import threading
+        tid = threading.get_ident()
+        if tid not in self._thread_ctx:
+            self._thread_ctx[tid] = api.Context(self.device)
+        return self._thread_ctx[tid]
+
+    def launches(self) -> int:
+        return self.ctx.kernel_launches() + sum(c.kernel_launches() for c in self._thread_ctx.values())
+
+    def bounds(self, seed: int):
+        b = api.lan_tr_bounds(self.A, 1e-4, 60, 40, seed)
+        return b.lmin, b.lmax
+
+    def moments(self, lmin, lmax, m, n_vec, seed, probes, first, count):
+        if count == 0:
+            return np.zeros((0, m + 1))
+        return api.kpm_moments_probes(self.A, api.SpectralBounds(lmin, lmax), m, n_vec, seed,
+                                      probes, first, count)
+
+    def curve(self, zeta, lmin, lmax, npts):
+        return api.kpm_curve(zeta, self.n, api.SpectralBounds(lmin, lmax), npts)
+
+    def solve_slice(self, plan: Plan, lmin, lmax, lo, hi, est):
+        ctx = self._ctx()
+        A = api.DeviceCsr(self.A.handle, ctx)  # se_csr is shareable across contexts on a device
+        try:
+            f = api.find_pol(lo, hi, api.SpectralBounds(lmin, lmax), api.PolyOpts(damping=plan.damping))
+            cfg = api.SolverConfig(m=plan.solver_m, res_tol=plan.tol, seed=plan.seed,
+                                   est_count=max(1, int(math.ceil(est))))
+            drv = api.cheb_lan_tr if plan.solver == "tr" else api.cheb_lan_nr
+            r = drv(A, None, f, lo, hi, cfg, want_vectors=plan.want_vectors)
+        finally:
+            A.handle = None  # borrowed handle: do not free
+        return f.k, r
+
+
+def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
+    """Full sliced solve; every rank returns the gathered result (slices in index order)."""
+    dist = dist or Dist()
+    t0 = time.perf_counter()
+    # bounds: deterministic on every rank; rank 0's copy is broadcast so all ranks agree bitwise
+    if plan.bounds is not None:
+        lmin, lmax = plan.bounds
+    else:
+        lmin, lmax = backend.bounds(plan.seed)
+        lmin, lmax = (float(v) for v in dist.broadcast_f64(np.array([lmin, lmax])))
+    t1 = time.perf_counter()
+    # KPM: this rank's contiguous probe range, then an all-gather of per-probe moments
+    counts = [probe_split(plan.dos_nvec, dist.world, r)[1] for r in range(dist.world)]
+    first, count = probe_split(plan.dos_nvec, dist.world, dist.rank)
+    mine = backend.moments(lmin, lmax, plan.dos_m, plan.dos_nvec, plan.seed, plan.probes, first,
+                           count)
+    allp = dist.allgather_rows(np.asarray(mine, np.float64).reshape(count, plan.dos_m + 1), counts)
+    zeta = np.zeros(plan.dos_m + 1)
+    for row in allp:  # probe order (dos.hpp:100-106)
+        zeta += row
+    zeta /= float(plan.dos_nvec) * backend.n  # dos.hpp:110
+    curve = backend.curve(zeta, lmin, lmax, plan.dos_npts)
+    if plan.ns <= 1:
+        lo, hi = max(plan.xi, curve.xdos[0]), min(plan.eta, curve.xdos[-1])
+        est0 = api.dos_count(curve, lo, hi) if lo < hi else 0.0
+        bp, est = np.array([plan.xi, plan.eta]), np.array([est0])
+    else:
+        bp, est = slice_clipped(curve, plan.xi, plan.eta, plan.ns)
+    t2 = time.perf_counter()
+    ns = len(est)
+    delta = 1e-10 * (lmax - lmin)
+    mine_idx = [i for i in range(ns) if slice_owner(i, dist.world) == dist.rank]
+
+    def work(i):
+        out = SliceOutcome(i, float(bp[i]), float(bp[i + 1]), float(est[i]), rank=dist.rank)
+        ts = time.perf_counter()
+        try:
+            k, r = backend.solve_slice(plan, lmin, lmax, out.lo, out.hi, out.est)
+            keep = trim_to_slice(r.eigenvalues, r.residuals, i, ns, out.lo, out.hi, delta)
+            out.degree = k
+            out.eigenvalues = np.asarray(r.eigenvalues)[keep]
+            out.residuals = np.asarray(r.residuals)[keep]
+            if plan.want_vectors and r.vectors is not None:
+                out.vectors = np.asarray(r.vectors)[:, keep]
+            out.niter = r.niter
+            out.n_A_matvec = r.counters.n_A_matvec
+            out.hit_max_its = r.hit_max_its
+        except Exception as e:  # per-slice failure is recorded (sliceeig_main.cpp:506-514)
+            out.error = f"{type(e).__name__}: {e}"
+        out.seconds = time.perf_counter() - ts
+        return out
+
+    jobs = plan.jobs if plan.jobs > 0 else max(1, len(mine_idx))
+    if jobs == 1 or len(mine_idx) <= 1:
+        local = [work(i) for i in mine_idx]
+    else:
+        with ThreadPoolExecutor(max_workers=jobs) as ex:
+            local = list(ex.map(work, mine_idx))
+    t3 = time.perf_counter()
+    gathered = dist.gather_objects(local)
+    slices = sorted([s for part in gathered for s in part], key=lambda s: s.index)
+    t4 = time.perf_counter()
+    return PipelineResult(lmin, lmax, bp, est, slices, t1 - t0, t2 - t1, t3 - t2, t4 - t0,
+                          backend.launches() if hasattr(backend, "launches") else 0)

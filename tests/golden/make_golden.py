@@ -1,0 +1,150 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference (oracle/_ref, compiled from
+/root/reference/proj/include by oracle/Makefile).  Run in the build container (the reference is
+absent on the GPU box):
+
+    python tests/golden/make_golden.py [--skip-solve]
+
+Outputs tests/golden/*.npz.  Every array is produced by calling the reference library; nothing here
+restates the algorithm.
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle import reflib  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **{k: np.asarray(v) for k, v in arrays.items()})
+    print("wrote", path, f"{os.path.getsize(path) / 1024:.1f} KiB")
+
+
+def kats():
+    out = {}
+    # filter coefficient KATs (filter_poly.hpp)
+    ints = [(-0.4, 0.4), (0.2, 0.4), (0.0, 0.3), (-0.5, 0.5), (-0.9, -0.85), (0.61, 0.62)]
+    for damp in ("none", "sigma", "jackson"):
+        for q, (a, b) in enumerate(ints):
+            f = reflib.find_pol(a, b, -1.0, 1.0, damping=damp)
+            out[f"findpol_{damp}_{q}_k"] = f["k"]
+            out[f"findpol_{damp}_{q}_scalars"] = [f["gamma"], f["ta"], f["tb"], f["bar"], f["c"], f["d"],
+                                                  float(f["cap_reached"])]
+            out[f"findpol_{damp}_{q}_mu"] = f["mu"]
+        for k in (1, 2, 8, 40):
+            out[f"damp_{damp}_{k}"] = reflib.damping_multipliers(k, damp)
+        for k, g in ((16, 0.3), (5, -0.7)):
+            out[f"ncoef_{damp}_{k}"] = reflib.normalized_coeffs(k, g, damp)
+    out["findpol_bounds"] = [0.0, 8.0]
+    for q, (a, b) in enumerate([(0.0, 0.5), (7.5, 8.0), (3.0, 4.0), (0.4, 1.0443178519)]):
+        f = reflib.find_pol(a, b, 0.0, 8.0)
+        out[f"findpol_b8_{q}_k"] = f["k"]
+        out[f"findpol_b8_{q}_mu"] = f["mu"]
+        out[f"findpol_b8_{q}_scalars"] = [f["gamma"], f["ta"], f["tb"], f["bar"], f["c"], f["d"],
+                                          float(f["cap_reached"])]
+    out["balance_16_02_04_sigma"] = reflib.balance_center(16, 0.2, 0.4, "sigma")
+    # rng streams (rng.hpp)
+    out["rng_normal_7"] = reflib.rng_vectors(7, "normal", 257, 3)
+    out["rng_rademacher_7"] = reflib.rng_vectors(7, "rademacher", 257, 3)
+    out["rng_uniform_7"] = reflib.rng_uniform(7, 100)
+    # matrices + analytic spectra (laplacian.hpp)
+    for dims in ([7], [5, 4], [4, 3, 5], [20, 20]):
+        tag = "x".join(map(str, dims))
+        rp, ci, v = reflib.laplacian(dims)
+        out[f"lap_{tag}_rp"], out[f"lap_{tag}_ci"], out[f"lap_{tag}_v"] = rp, ci, v
+        out[f"lapeig_{tag}"] = reflib.laplacian_eigs(dims)
+    # apply_pol / matvec on the 20x20 Laplacian (filter_poly.hpp:256-277)
+    rp, ci, v = reflib.laplacian([20, 20])
+    x = reflib.rng_vectors(3, "normal", 400, 1)[0]
+    out["ap_x"] = x
+    out["ap_Ax"] = reflib.matvec(rp, ci, v, x)
+    for damp in ("sigma", "jackson"):
+        f = reflib.find_pol(1.0, 1.5, 0.0, 8.0, damping=damp)
+        y, nmv = reflib.apply_pol(rp, ci, v, f["mu"], f["c"], f["d"], x)
+        out[f"ap_{damp}_mu"], out[f"ap_{damp}_cd"] = f["mu"], [f["c"], f["d"]]
+        out[f"ap_{damp}_y"], out[f"ap_{damp}_nmv"] = y, nmv
+    # KPM moments / curve / slicing on 25x25 (dos.hpp, slicer.hpp)
+    rp, ci, v = reflib.laplacian([25, 25])
+    for kind in ("rademacher", "normal"):
+        out[f"kpm25_zeta_{kind}"] = reflib.kpm_moments(rp, ci, v, 0.0, 8.0, 60, 8, 777, kind)
+    x25, y25, nev25 = reflib.kpm_dos(rp, ci, v, 0.0, 8.0, 60, 8, 300, 777)
+    out["kpm25_x"], out["kpm25_y"], out["kpm25_nev"] = x25, y25, nev25
+    out["kpm25_bp4"], out["kpm25_est4"] = reflib.slice_spectrum(x25, y25, 625, 0.0, 8.0, 4)
+    out["kpm25_count_1_3"] = reflib.dos_count(x25, y25, 625, 1.0, 3.0)
+    # CGS2 (orth.hpp:70-80)
+    rng = np.random.default_rng(0)
+    W = np.linalg.qr(rng.standard_normal((300, 25)))[0].T.copy()
+    t = rng.standard_normal(300)
+    out["cgs_W"], out["cgs_t"] = W, t
+    out["cgs_t_out"], out["cgs_h"] = reflib.paired_cgs2(W, t)
+    # small eigensolvers (tridiag_eig.hpp, dense_eig.hpp)
+    a = rng.standard_normal(30)
+    b = rng.standard_normal(29)
+    out["trid_a"], out["trid_b"] = a, b
+    out["trid_vals"], out["trid_vecs"] = reflib.sym_tridiag_eig(a, b, True)
+    S = rng.standard_normal((24, 24))
+    S = S + S.T
+    out["dense_S"] = S
+    out["dense_vals"], out["dense_vecs"] = reflib.dense_sym_eig(S, True)
+    # lanczos_run on 20x20 (lanczos.hpp:37-118)
+    rp, ci, v = reflib.laplacian([20, 20])
+    st = reflib.rng_vectors(5, "normal", 400, 1)[0]
+    lr = reflib.lanczos_run(rp, ci, v, st, 30)
+    out["lanczos_start"], out["lanczos_alpha"], out["lanczos_beta"] = st, lr["alpha"], lr["beta"]
+    out["lanczos_next_beta"] = lr["next_beta"]
+    save("kats", **out)
+
+
+def cfg1(skip_solve):
+    # BASELINE configs[0]: 100x100, KPM 80 x 20 Rademacher seed 0, [0.4,1.6] in 2, Jackson, NR 1e-8
+    rp, ci, v = reflib.laplacian([100, 100])
+    lo, hi = reflib.lan_tr_bounds(rp, ci, v, 1e-4, 60, 40, 0)
+    zeta = reflib.kpm_moments(rp, ci, v, lo, hi, 80, 20, 0, "rademacher")
+    x, y, nev = reflib.kpm_dos(rp, ci, v, lo, hi, 80, 20, 300, 0)
+    bp, est = reflib.slice_spectrum(x, y, 10000, 0.4, 1.6, 2)
+    degs = [reflib.find_pol(bp[i], bp[i + 1], lo, hi, damping="jackson")["k"] for i in range(2)]
+    out = dict(bounds=[lo, hi], zeta=zeta, x=x, y=y, nev=nev, bp=bp, est=est, degrees=degs)
+    if not skip_solve:
+        t0 = time.time()
+        r = reflib.solve(rp, ci, v, 0.4, 1.6, 2, "nr", "jackson", 80, 20, 300, "rademacher", 1e-8, 0,
+                         jobs=2)
+        print(f"cfg1 reference solve {time.time() - t0:.1f} s")
+        for i, s in enumerate(r["slices"]):
+            out[f"slice{i}_vals"] = s["eigenvalues"]
+            out[f"slice{i}_res"] = s["residuals"]
+            out[f"slice{i}_meta"] = [s["niter"], s["n_A_matvec"], s["degree"], int(s["hit_max_its"])]
+        out["solve_bp"] = r["breakpoints"]
+        out["solve_bounds"] = [r["lmin"], r["lmax"]]
+    save("cfg1", **out)
+
+
+def cfg2():
+    # BASELINE configs[1]: 64^3, KPM 100 x 40 Gaussian seed 1234, [0.6,1.2] in 8 (sigma damping)
+    rp, ci, v = reflib.laplacian([64, 64, 64])
+    t0 = time.time()
+    lo, hi = reflib.lan_tr_bounds(rp, ci, v, 1e-4, 60, 40, 1234)
+    zeta = reflib.kpm_moments(rp, ci, v, lo, hi, 100, 40, 1234, "normal")
+    x, y, nev = reflib.curve_from_moments(zeta / (40.0 * 262144), 262144, lo, hi, 300)
+    bp, est = reflib.slice_spectrum(x, y, 262144, 0.6, 1.2, 8)
+    degs = [reflib.find_pol(bp[i], bp[i + 1], lo, hi)["k"] for i in range(8)]
+    print(f"cfg2 bounds+kpm {time.time() - t0:.1f} s; degrees {degs}")
+    save("cfg2", bounds=[lo, hi], zeta=zeta, x=x, y=y, nev=nev, bp=bp, est=est, degrees=degs)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-solve", action="store_true")
+    ap.add_argument("--only", default="kats,cfg1,cfg2")
+    a = ap.parse_args()
+    only = a.only.split(",")
+    if "kats" in only:
+        kats()
+    if "cfg2" in only:
+        cfg2()
+    if "cfg1" in only:
+        cfg1(a.skip_solve)
