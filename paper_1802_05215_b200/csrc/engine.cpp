@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -351,6 +353,7 @@ struct Slice {
   double bar, xi, eta;
   Rng rng;
   se_counters cnt{};
+  double prof[4] = {0, 0, 0, 0};  // host seconds: stagnation checks, projected eig, candidates
   Vec lock_val, lock_res;
   int preloaded = 0;
   StepOp op;
@@ -374,6 +377,29 @@ struct Slice {
   }
 
   double bar_eff() const { return bar * (1.0 - 1e-4); }
+
+  // Ritz values >= bar of a tridiagonal projected matrix (ascending), for tnew.
+  double* chk_work = nullptr;
+  int chk_cap = 0;
+  void check_eigs(const Vec& d, const Vec& e, Vec& vals) {
+    const int m = (int)d.size();
+    if (m <= 64) {  // tiny: host QL (values only)
+      Vec all, unused;
+      sym_tridiag_eig(d, e, false, all, unused);
+      vals.clear();
+      for (double v : all)
+        if (v >= bar) vals.push_back(v);
+      return;
+    }
+    if (m > chk_cap) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      dev_free(chk_work);
+      chk_cap = grow(m);
+      chk_work = dev_alloc<double>(4 * (size_t)chk_cap + 8);
+    }
+    k::tridiag_eigs_above(c, m, d.data(), e.data(), bar, chk_work, vals);
+  }
+  ~Slice() { dev_free(chk_work); }
   double stagnation_tol(double tnew) const {
     return cfg.tau1 > 0.0 ? cfg.tau1 : std::max(1e-12, 1e-10 * std::abs(tnew));
   }
@@ -461,6 +487,12 @@ struct Slice {
     SE_CUDA(cudaStreamSynchronize(c.stream));
     add_timers();
     cnt.t_total += now_s() - t0;
+    if (std::getenv("SE_PROFILE"))
+      std::fprintf(stderr,
+                   "[se] n=%d its=%ld total %.3f mv %.3f orth %.3f check %.3f eig %.3f cand %.3f "
+                   "passes %lld\n",
+                   A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
+                   kr.get().passes_total);
     r->niter = its;
     r->hit_max_its = warn;
     r->counters = cnt;
@@ -519,7 +551,9 @@ std::unique_ptr<SliceResult> run_nr(Slice& s) {
       kr.download(kr.beta, (int)its - 1, be);
       if (!stagnant && !last) {
         Vec vals, vecs;
-        sym_tridiag_eig(al, be, false, vals, vecs);
+        const double tq = now_s();
+        s.check_eigs(al, be, vals);
+        s.prof[0] += now_s() - tq;
         const double tnew = sum_above(vals, s.bar);
         if (!std::isnan(told) && std::abs(tnew - told) < s.stagnation_tol(tnew)) stagnant = true;
         told = tnew;
@@ -530,12 +564,16 @@ std::unique_ptr<SliceResult> run_nr(Slice& s) {
         for (int i = 0; i < m; ++i) H[(size_t)i * m + i] = al[i];
         for (int i = 0; i + 1 < m; ++i) H[(size_t)i * m + i + 1] = H[(size_t)(i + 1) * m + i] = be[i];
         Vec vals;
+        double tq = now_s();
         const double* Y = s.eig.solve(m, H, vals);
+        s.prof[1] += now_s() - tq;
         int j0 = m;
         while (j0 > 0 && vals[j0 - 1] >= s.bar_eff()) --j0;
         const int ncand = m - j0;
         Vec st;
+        tq = now_s();
         if (ncand > 0) s.cand.eval(s.A, kr.W.p, m, Y + (size_t)j0 * m, m, ncand, st);
+        s.prof[2] += now_s() - tq;
         s.cnt.n_A_matvec += ncand;
         std::vector<int> accepted;
         bool pending = false;
@@ -617,7 +655,9 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
         for (int q = 1; q < steps - l; ++q) d.push_back(hd[q]);
         for (double b : be) e.push_back(b);
         Vec vals, unused;
-        sym_tridiag_eig(d, e, false, vals, unused);
+        const double tq = now_s();
+        s.check_eigs(d, e, vals);
+        s.prof[0] += now_s() - tq;
         const double tnew = sum_above(vals, s.bar);
         if (!std::isnan(told) && std::abs(tnew - told) < s.stagnation_tol(tnew)) break;
         told = tnew;
@@ -636,12 +676,16 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
     for (int q = l; q < steps; ++q) at(q, q) = hd[q - l];
     for (int q = l; q + 1 < steps; ++q) at(q + 1, q) = at(q, q + 1) = be[q - l];
     Vec vals;
+    double tq = now_s();
     const double* Y = s.eig.solve(steps, H, vals);
+    s.prof[1] += now_s() - tq;
     int j0 = steps;
     while (j0 > 0 && vals[j0 - 1] >= s.bar_eff()) --j0;
     const int ncand = steps - j0;
     Vec st;
+    tq = now_s();
     if (ncand > 0) s.cand.eval(s.A, kr.W.p, steps, Y + (size_t)j0 * steps, steps, ncand, st);
+    s.prof[2] += now_s() - tq;
     s.cnt.n_A_matvec += ncand;
     const Vec ylast = s.last_row(Y, steps, j0, ncand);
     struct TrC {

@@ -23,6 +23,7 @@ struct Ctl {
   double beta_prev;
   unsigned long long ts0, ts1;  // %globaltimer stamps (ns) for the Counters timers
   double t_mv_ns, t_orth_ns;    // accumulated filter / orthogonalisation device time
+  long long passes_total;       // CGS passes executed (DGKS statistics)
 };
 
 namespace k {
@@ -102,5 +103,14 @@ void scale_copy(Ctx& c, int n, double a, const double* src, double* dst);
 // Device-time stamps: which 0 = filter start, 1 = filter end / orth start, 2 = orth end.
 void stamp(Ctx& c, Ctl* ctl, int which);
 
+}  // namespace k
+}  // namespace se
+
+namespace se {
+namespace k {
+// Eigenvalues >= bar of the symmetric tridiagonal (d[m], e[m-1]) by device Sturm bisection
+// (stagnation checks, eigensolvers.hpp:436-444 / 562-572).  work: >= 4m + 8 device doubles.
+void tridiag_eigs_above(Ctx& c, int m, const double* d_host, const double* e_host, double bar,
+                        double* work, std::vector<double>& out);
 }  // namespace k
 }  // namespace se

@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_gemvn(int n, const double* __restr
   if (grid_sum(tr * tr, partial, cnt, &tot) && threadIdx.x == 0) {
     const double after = sqrt(tot);
     ctl->npass += 1;
+    ctl->passes_total += 1;
     if (!pass2) ctl->repass = after > kDgksEta * ctl->before ? 0 : 1;
     ctl->before = after;
     ctl->after = after;

@@ -44,6 +44,7 @@ class Plan:
     bounds: Optional[tuple] = None  # fixed (lmin, lmax) skips the bounds stage
     solver_m: int = 0              # SolverConfig.m override (0: reference default)
     jobs: int = 0                  # concurrent slices per rank (0: all of the rank's slices)
+    only: Optional[Sequence[int]] = None  # debug/profiling: solve only these slice indices
     want_vectors: bool = False
 
 
@@ -61,6 +62,8 @@ class SliceOutcome:
     n_A_matvec: int = 0
     hit_max_its: bool = False
     seconds: float = 0.0
+    t_mv: float = 0.0
+    t_orth: float = 0.0
     error: Optional[str] = None
     rank: int = 0
 
@@ -258,7 +261,8 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
     t2 = time.perf_counter()
     ns = len(est)
     delta = 1e-10 * (lmax - lmin)
-    mine_idx = [i for i in range(ns) if slice_owner(i, dist.world) == dist.rank]
+    mine_idx = [i for i in range(ns) if slice_owner(i, dist.world) == dist.rank
+                and (plan.only is None or i in plan.only)]
 
     def work(i):
         out = SliceOutcome(i, float(bp[i]), float(bp[i + 1]), float(est[i]), rank=dist.rank)
@@ -274,6 +278,7 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
             out.niter = r.niter
             out.n_A_matvec = r.counters.n_A_matvec
             out.hit_max_its = r.hit_max_its
+            out.t_mv, out.t_orth = r.counters.t_mv, r.counters.t_orth
         except Exception as e:  # per-slice failure is recorded (sliceeig_main.cpp:506-514)
             out.error = f"{type(e).__name__}: {e}"
         out.seconds = time.perf_counter() - ts

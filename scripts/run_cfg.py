@@ -16,12 +16,13 @@ ap.add_argument("cfg")
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--jobs", type=int, default=0)
 ap.add_argument("--solver", default=None)
+ap.add_argument("--only", default=None)
 a = ap.parse_args()
 c = CFGS[a.cfg]
 p = dict(c["plan"])
 if a.solver:
     p["solver"] = a.solver
-plan = Plan(**p, jobs=a.jobs)
+plan = Plan(**p, jobs=a.jobs, only=[int(q) for q in a.only.split(",")] if a.only else None)
 be = GpuBackend(dims=c["dims"])
 ev = api.laplacian_analytic_eigs(c["dims"])
 for rep in range(a.repeat):
@@ -40,5 +41,5 @@ for rep in range(a.repeat):
             cand = np.stack([ev[np.clip(idx-1,0,ev.size-1)], ev[np.clip(idx,0,ev.size-1)]])
             maxerr = float(np.min(np.abs(cand - s.eigenvalues), axis=0).max() / max(1e-300, np.abs(s.eigenvalues).max()))
         print(f"  slice {s.index} [{lo:.8f},{hi:.8f}] est {s.est:.1f} deg {s.degree} found {s.eigenvalues.size} truth {truth} "
-              f"niter {s.niter} nmv {s.n_A_matvec} {s.seconds:.2f}s maxrelerr {maxerr:.2e} maxres {s.residuals.max() if s.residuals.size else 0:.1e} err={s.error}")
+              f"niter {s.niter} nmv {s.n_A_matvec} {s.seconds:.2f}s (mv {s.t_mv:.2f} orth {s.t_orth:.2f}) maxrelerr {maxerr:.2e} maxres {s.residuals.max() if s.residuals.size else 0:.1e} err={s.error}")
 print("launches", be.launches())
