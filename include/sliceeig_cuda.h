@@ -130,6 +130,13 @@ SE_API int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, 
 SE_API int se_cheb_apply_dev(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec,
                       const double* d_v, double* d_out);
 
+/* Production timing of the fused filter kernels: one application captured as a CUDA graph and
+ * replayed `reps` times between CUDA events on ctx's stream.  Returns the total ms, the number
+ * of filter-kernel launches timed, and their algorithmic bytes (Abytes + 32n for the first
+ * degree, Abytes + 40n for each further degree). */
+SE_API int se_filter_bench(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int reps,
+                           double* ms, long* launches, double* bytes);
+
 /* ---- filters (host, filter_poly.hpp) -------------------------------------------------------- */
 SE_API int se_damping_multipliers(int k, int damping, double* out);            /* :41-60   */
 SE_API int se_chebyshev_coeffs(double gamma, int k, double* out);              /* :30-39   */

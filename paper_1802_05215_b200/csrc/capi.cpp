@@ -340,6 +340,22 @@ int se_cheb_apply_dev(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int
   });
 }
 
+int se_filter_bench(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int reps, double* ms,
+                    long* launches, double* bytes) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& m = M(a);
+    const PolyFilter pf = to_filter(f);
+    if (reps < 1) fail(SE_EINVAL, "se_filter_bench: reps must be positive");
+    double t = 0.0;
+    long nl = 0;
+    filter_bench(c, m, to_op(pf), reps, t, nl);
+    *ms = t;
+    *launches = nl;
+    *bytes = (double)reps * (m.abytes() + 32.0 * m.n + (pf.k - 1) * (m.abytes() + 40.0 * m.n));
+  });
+}
+
 int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
                   double* out, long* n_matvec) {
   return guard([&] {

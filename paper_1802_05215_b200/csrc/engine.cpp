@@ -930,3 +930,68 @@ std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter&
 }
 
 }  // namespace se
+
+namespace se {
+// Time the filter kernels as they run in production: one application (k fused SpMV launches)
+// captured in a CUDA graph, replayed `reps` times between CUDA events on the context's stream.
+void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& ms, long& launches) {
+  const int n = a.n;
+  double* v = dev_alloc<double>(n);
+  double* out = dev_alloc<double>(n);
+  double* fb[3];
+  for (double*& b : fb) b = dev_alloc<double>(n);
+  cudaGraphExec_t ge = nullptr;
+  try {
+    std::vector<double> h(n);
+    Rng rng(99);
+    rng.normal_fill(h.data(), n);
+    SE_CUDA(cudaMemcpyAsync(v, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    const long before = c.launches;
+    SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    k::ChebArgs a1;
+    a1.c = op.c;
+    a1.invd = op.invd;
+    a1.x = v;
+    a1.y = fb[0];
+    a1.out = out;
+    a1.mu0 = op.mu[0];
+    a1.muj = op.mu[1];
+    k::spmv_cheb(c, a, k::kFirst, a1);
+    int cur = 0, prv = -1, nxt = 1;
+    for (int j = 2; j <= op.k; ++j) {
+      k::ChebArgs b = a1;
+      b.x = fb[cur];
+      b.prev = prv < 0 ? v : fb[prv];
+      b.y = fb[nxt];
+      b.muj = op.mu[j];
+      k::spmv_cheb(c, a, k::kNext, b);
+      const int old = prv < 0 ? 2 : prv;
+      prv = cur;
+      cur = nxt;
+      nxt = old;
+    }
+    cudaGraph_t g;
+    SE_CUDA(cudaStreamEndCapture(c.stream, &g));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    const long per = c.launches - before;
+    SE_CUDA(cudaGraphLaunch(ge, c.stream));  // warm
+    SE_CUDA(cudaEventRecord(c.ev0, c.stream));
+    for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev1, c.stream));
+    SE_CUDA(cudaEventSynchronize(c.ev1));
+    float fms = 0.f;
+    SE_CUDA(cudaEventElapsedTime(&fms, c.ev0, c.ev1));
+    ms = fms;
+    launches = per * reps;
+    c.launches += per * (reps + 1);
+  } catch (...) {
+    if (ge) cudaGraphExecDestroy(ge);
+    for (void* p : {(void*)v, (void*)out, (void*)fb[0], (void*)fb[1], (void*)fb[2]}) dev_free(p);
+    throw;
+  }
+  cudaGraphExecDestroy(ge);
+  for (void* p : {(void*)v, (void*)out, (void*)fb[0], (void*)fb[1], (void*)fb[2]}) dev_free(p);
+}
+}  // namespace se

@@ -64,3 +64,7 @@ std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter&
                                       const char* who);
 
 }  // namespace se
+
+namespace se {
+void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& ms, long& launches);
+}

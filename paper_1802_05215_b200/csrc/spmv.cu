@@ -22,6 +22,15 @@ __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, 
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 struct KArgs {
   const double* x;
   const double* prev;
@@ -35,68 +44,88 @@ struct KArgs {
 };
 
 // One CTA = one tile of kRows consecutive rows.  The tile's nnz range [rp[r0], rp[r0+kRows]) is
-// contiguous in CSR, so it is staged into shared memory with fully coalesced loads; each thread
-// then sums its own row sequentially (reference order) gathering x through L1/L2.  Rows longer
-// than the stage are handled by carrying the accumulator across stage passes.
+// contiguous in CSR, so it is staged into shared memory with fully coalesced 16-byte loads; each
+// thread then sums its own row sequentially (reference order) gathering x through L1/L2.  Rows
+// longer than the stage are handled by carrying the accumulator across stage passes.
+// Latency structure (the kernel is latency-bound when A is L2-resident): one round trip for the
+// row pointers and every row-local operand (x[r], prev[r], out[r]), one for the staged tile,
+// one for the x gathers (8 in flight per thread).
 template <int MODE>
 __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restrict__ rp,
                                                       const int* __restrict__ ci,
                                                       const double* __restrict__ v, KArgs a) {
   if (a.halt && a.halt->halted) return;
-  __shared__ double s_v[kChunk];
-  __shared__ int s_c[kChunk];
+  __shared__ __align__(16) double s_v[kChunk + 8];
+  __shared__ __align__(16) int s_c[kChunk + 8];
   const size_t coff = (size_t)blockIdx.y * n;  // column of a column-major batch (kPlain)
   const size_t ioff = a.src_ctl ? (size_t)a.src_ctl->i * a.src_ld : 0;
   const double* __restrict__ x = a.x + coff + (a.x_indirect ? ioff : 0);
   const int r0 = blockIdx.x * kRows;
   const int r = r0 + threadIdx.x;
+  const bool live = r < n;
   const int rend = min(r0 + kRows, n);
+  // round trip 1: tile bounds, own row bounds, row-local operands
   const int base = __ldg(rp + r0), end = __ldg(rp + rend);
   int rs = end, re = end;
-  if (r < n) {
+  double xr = 0.0, pv = 0.0, ov = 0.0;
+  if (live) {
     rs = __ldg(rp + r);
     re = __ldg(rp + r + 1);
+    if (MODE != kPlain) xr = __ldg(x + r);
+    if (MODE == kNext) {
+      const double* __restrict__ prev = a.prev + (a.prev_indirect ? ioff : 0);
+      pv = __ldg(prev + r);
+      ov = a.out[r];
+    }
   }
   double acc = 0.0;
   for (int c0 = base; c0 < end; c0 += kChunk) {
     const int cn = min(kChunk, end - c0);
-    for (int q = threadIdx.x; q < cn; q += kRows) {
-      s_v[q] = __ldg(v + c0 + q);
-      s_c[q] = __ldg(ci + c0 + q);
+    // round trip 2: stage the chunk with cp.async (LDGSTS, 16-byte, zero-filled tails): every
+    // load of the tile is in flight at once and none occupies a register.
+    const int va = c0 & ~1, ca = c0 & ~3;
+    const int cend = c0 + cn;
+    const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
+    for (int q = threadIdx.x; q < nv16; q += kRows) {
+      const int valid = min(2, cend - (va + 2 * q));
+      cp_async16(&s_v[2 * q], v + va + 2 * q, 8 * valid);
     }
+    for (int q = threadIdx.x; q < nc16; q += kRows) {
+      const int valid = min(4, cend - (ca + 4 * q));
+      cp_async16(&s_c[4 * q], ci + ca + 4 * q, 4 * valid);
+    }
+    cp_async_wait_all();
     __syncthreads();
-    int p = max(rs, c0) - c0;
-    const int pe = min(re, c0 + cn) - c0;
-    for (; p + 4 <= pe; p += 4) {
-      const double x0 = __ldg(x + s_c[p]), x1 = __ldg(x + s_c[p + 1]);
-      const double x2 = __ldg(x + s_c[p + 2]), x3 = __ldg(x + s_c[p + 3]);
-      acc = add(acc, mul(s_v[p], x0));
-      acc = add(acc, mul(s_v[p + 1], x1));
-      acc = add(acc, mul(s_v[p + 2], x2));
-      acc = add(acc, mul(s_v[p + 3], x3));
+    // round trip 3: gathers, 8 in flight; sums stay in storage order
+    const int p0 = max(rs, c0), pend = min(re, cend);
+    const int dv = va, dc = ca;  // smem index = global index - chunk origin (per array)
+    for (int p = p0; p < pend; p += 8) {
+      double xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = (p + u < pend) ? __ldg(x + s_c[p + u - dc]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (p + u < pend) acc = add(acc, mul(s_v[p + u - dv], xv[u]));
     }
-    for (; p < pe; ++p) acc = add(acc, mul(s_v[p], __ldg(x + s_c[p])));
     __syncthreads();
   }
-  if (r >= n) return;
+  if (!live) return;
   double* __restrict__ y = a.y + coff;
   if (MODE == kPlain) {
     y[r] = acc;
     return;
   }
   // Ahat x = (A x - c x) * (1/d)   (filter_poly.hpp:265)
-  const double xr = x[r];
   const double t = mul(sub(acc, mul(a.c, xr)), a.invd);
   if (MODE == kFirst) {
     y[r] = t;
     // out = 0 + mu0 v ; out += mu1 T_1 v   (filter_poly.hpp:261-262, 269)
     a.out[r] = add(add(0.0, mul(a.mu0, xr)), mul(a.muj, t));
   } else {
-    const double* __restrict__ prev = a.prev + (a.prev_indirect ? ioff : 0);
     // T_j = 2 Ahat T_{j-1} - T_{j-2} ; out += mu_j T_j   (filter_poly.hpp:272-275)
-    const double tj = sub(mul(2.0, t), prev[r]);
+    const double tj = sub(mul(2.0, t), pv);
     y[r] = tj;
-    a.out[r] = add(a.out[r], mul(a.muj, tj));
+    a.out[r] = add(ov, mul(a.muj, tj));
   }
 }
 
