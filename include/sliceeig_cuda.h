@@ -188,6 +188,11 @@ SE_API int se_paired_cgs2(se_ctx* ctx, int n, int k, const double* W, double* t,
  * dense_eig.hpp:114-139).  vectors: m x m column-major, may be NULL when want == 0. */
 SE_API int se_sym_tridiag_eig(int m, const double* alpha, const double* beta, int want, double* values,
                        double* vectors);
+/* Thick-restart arrowhead (theta[l], s[l], tip alpha_l) reduced to tridiagonal form by Givens
+ * rotations on indices 0..l-1 (host, O(l^2)); diag[l+1], off[l].  Used for the device stagnation
+ * checks of cheb_lan_tr (eigensolvers.hpp:562-572). */
+SE_API int se_arrow_tridiag(int l, const double* theta, const double* s, double alpha_l,
+                            double* diag, double* off);
 SE_API int se_dense_sym_eig(int m, const double* a, int want, int size_guard, double* values,
                      double* vectors);
 

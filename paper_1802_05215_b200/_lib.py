@@ -90,6 +90,7 @@ SIGNATURES = {
     "se_lanczos_run": [_VP, _VP, _PD, C.c_int, _PD, _PD, _PI, _PI, _PD, _PD, _PD],
     "se_paired_cgs2": [_VP, C.c_int, C.c_int, _PD, _PD, _PD],
     "se_sym_tridiag_eig": [C.c_int, _PD, _PD, C.c_int, _PD, _PD],
+    "se_arrow_tridiag": [C.c_int, _PD, _PD, C.c_double, _PD, _PD],
     "se_dense_sym_eig": [C.c_int, _PD, C.c_int, C.c_int, _PD, _PD],
     "se_cheb_lan": [_VP, _VP, C.POINTER(SePolyFilter), C.c_double, C.c_double,
                     C.POINTER(SeSolverCfg), C.c_int, C.c_int, _PD, _PD, C.c_int, C.POINTER(_VP)],

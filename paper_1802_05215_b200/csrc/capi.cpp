@@ -702,6 +702,17 @@ int se_sym_tridiag_eig(int m, const double* alpha, const double* beta, int want,
   });
 }
 
+int se_arrow_tridiag(int l, const double* theta, const double* s, double alpha_l, double* diag,
+                     double* off) {
+  return guard([&] {
+    if (l < 0) fail(SE_EINVAL, "arrow_tridiag: negative size");
+    Vec d, o;
+    arrow_to_tridiag(Vec(theta, theta + l), Vec(s, s + l), alpha_l, d, o);
+    std::copy(d.begin(), d.end(), diag);
+    std::copy(o.begin(), o.end(), off);
+  });
+}
+
 int se_dense_sym_eig(int m, const double* a, int want, int size_guard, double* values,
                      double* vectors) {
   return guard([&] {

@@ -1,0 +1,276 @@
+"""GPU parity of the full path against the reference (golden fixtures from oracle/_ref) and the
+analytic Laplacian spectra; restates the reference's own driver/DOS/Krylov test cases
+(test_eigensolvers.cpp, test_dos.cpp, test_krylov.cpp) through the C ABI."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_1802_05215_b200 import api
+    return api
+
+
+def _pl():
+    from paper_1802_05215_b200 import pipeline
+    return pipeline
+
+
+def moments_ok(z_gpu, z_ref):
+    """Contract: |dz_k| <= 1e-12 max(|z_k|, |z_0|) for identical probes."""
+    return np.all(np.abs(z_gpu - z_ref) <= 1e-12 * np.maximum(np.abs(z_ref), abs(z_ref[0])))
+
+
+def test_cfg1_kpm_moments_and_slices(gpu_ctx, golden):
+    api, pl = _api(), _pl()
+    c = golden("cfg1")
+    a = api.gen_laplacian([100, 100])
+    lo, hi = c["bounds"]
+    z = api.kpm_moments(a, api.SpectralBounds(lo, hi), 80, 20, seed=0)
+    assert moments_ok(z / 2e5, c["zeta"] / 2e5)
+    curve = api.kpm_curve(z / 2e5, a.n, api.SpectralBounds(lo, hi), 300)
+    assert np.max(np.abs(curve.ydos - c["y"])) <= 1e-12 * np.max(c["y"])
+    bp, est = pl.slice_clipped(curve, 0.4, 1.6, 2)
+    assert np.array_equal(bp, c["bp"])
+    assert np.allclose(est, c["est"], rtol=1e-10)
+
+
+def test_cfg1_full_pipeline_matches_reference(gpu_ctx, golden):
+    """BASELINE configs[0] end to end: identical per-slice counts, eigenvalues within 1e-10
+    relative of the reference's, residuals under the reference tolerance."""
+    api, pl = _api(), _pl()
+    c = golden("cfg1")
+    plan = pl.Plan(xi=0.4, eta=1.6, ns=2, solver="nr", damping="jackson", dos_m=80, dos_nvec=20,
+                   probes="rademacher", tol=1e-8, seed=0)
+    res = pl.run(plan, pl.GpuBackend(dims=[100, 100]))
+    assert abs(res.lmin - c["bounds"][0]) <= 1e-10 and abs(res.lmax - c["bounds"][1]) <= 1e-10
+    assert np.allclose(res.breakpoints, c["solve_bp"], rtol=1e-12, atol=0)
+    for i, s in enumerate(res.slices):
+        ref = c[f"slice{i}_vals"]
+        assert s.error is None
+        assert s.eigenvalues.size == ref.size
+        assert np.all(np.abs(s.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+        assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
+        assert s.degree == int(c["degrees"][i]) == int(c[f"slice{i}_meta"][2])
+        assert not s.hit_max_its
+
+
+def test_cfg2_kpm_gaussian_moments_and_breakpoints(gpu_ctx, golden):
+    api, pl = _api(), _pl()
+    c = golden("cfg2")
+    A = api.DeviceCsr.laplacian([64, 64, 64])
+    lo, hi = c["bounds"]
+    pp = api.kpm_moments_probes(A, api.SpectralBounds(lo, hi), 100, 40, 1234, "gaussian")
+    z = np.zeros(101)
+    for row in pp:
+        z += row
+    assert moments_ok(z / (40 * 262144.0), c["zeta"] / (40 * 262144.0))
+    curve = api.kpm_curve(z / (40 * 262144.0), A.n, api.SpectralBounds(lo, hi), 300)
+    bp, est = pl.slice_clipped(curve, 0.6, 1.2, 8)
+    assert np.array_equal(bp, c["bp"])
+    degs = [api.find_pol(bp[i], bp[i + 1], api.SpectralBounds(lo, hi)).k for i in range(8)]
+    assert degs == list(c["degrees"])
+
+
+@pytest.mark.slow
+def test_cfg2_full_pipeline_exact_counts(gpu_ctx):
+    """BASELINE configs[1] end to end on one GPU: every slice returns exactly the analytic
+    eigenvalues (counts identical, |dlambda| <= 1e-10 |lambda|)."""
+    api, pl = _api(), _pl()
+    plan = pl.Plan(xi=0.6, eta=1.2, ns=8, solver="tr", damping="sigma", dos_m=100, dos_nvec=40,
+                   probes="gaussian", tol=1e-8, seed=1234)
+    res = pl.run(plan, pl.GpuBackend(dims=[64, 64, 64]))
+    ev = api.laplacian_analytic_eigs([64, 64, 64])
+    delta = 1e-10 * (res.lmax - res.lmin)
+    total = 0
+    for s in res.slices:
+        lo = s.lo + (delta if s.index > 0 else 0.0)
+        hi = s.hi + (delta if s.index < 7 else 0.0)
+        truth = ev[((ev > lo) if s.index > 0 else (ev >= lo)) & (ev <= hi)]
+        assert s.error is None and s.eigenvalues.size == truth.size, (s.index, s.eigenvalues.size, truth.size)
+        assert np.all(np.abs(s.eigenvalues - truth) <= 1e-10 * np.abs(truth))
+        assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
+        total += truth.size
+    assert total == api.count_in_interval(ev, 0.6, 1.2) == 4120
+
+
+def test_kpm_dos_bitwise_rerun_and_validation(gpu_ctx):
+    api = _api()
+    a = api.gen_laplacian([18, 18])
+    cfg = api.DosConfig(m=30, n_vec=8, seed=777)
+    k1 = api.kpm_dos(a, api.SpectralBounds(0.0, 8.0), cfg)
+    k2 = api.kpm_dos(a, api.SpectralBounds(0.0, 8.0), cfg)
+    assert np.array_equal(k1.ydos, k2.ydos)
+    l1 = api.lan_dos(a, api.SpectralBounds(0.0, 8.0), cfg)
+    l2 = api.lan_dos(a, api.SpectralBounds(0.0, 8.0), cfg)
+    assert np.array_equal(l1.ydos, l2.ydos)
+    l3 = api.lan_dos(a, api.SpectralBounds(0.0, 8.0), api.DosConfig(m=30, n_vec=8, seed=778))
+    assert not np.array_equal(l1.ydos, l3.ydos)
+    with pytest.raises(ValueError):
+        api.kpm_dos(a, api.SpectralBounds(1.0, 1.0), cfg)
+    with pytest.raises(ValueError):
+        api.kpm_dos(a, api.SpectralBounds(0.0, 2.0), api.DosConfig(npts=1))
+    with pytest.raises(ValueError):
+        api.kpm_dos(a, api.SpectralBounds(0.0, 2.0), api.DosConfig(n_vec=0))
+
+
+def test_dos_counts_within_15_percent(gpu_ctx):
+    # test_dos.cpp:55-65 (kpm, 60x60) and :101-114 (lanczos, 20^3)
+    api = _api()
+    a = api.gen_laplacian([60, 60])
+    c = api.kpm_dos(a, api.SpectralBounds(0.0, 8.0))
+    ev = api.laplacian_analytic_eigs([60, 60])
+    truth = api.count_in_interval(ev, 0.4, 0.6)
+    assert abs(api.dos_count(c, 0.4, 0.6) - truth) <= 0.15 * truth
+    assert abs(api.dos_count(c, 0.0, 8.0) - a.n) <= 0.1 * a.n
+    b = api.gen_laplacian([20, 20, 20])
+    cl = api.lan_dos(b, api.SpectralBounds(0.0, 12.0), api.DosConfig(method="lanczos"))
+    ev3 = api.laplacian_analytic_eigs([20, 20, 20])
+    for lo, hi in ((1.0, 2.0), (4.0, 6.0), (9.0, 11.0)):
+        t = api.count_in_interval(ev3, lo, hi)
+        assert abs(api.dos_count(cl, lo, hi) - t) <= max(0.15 * t, 10.0)
+
+
+def test_lanczos_run_matches_reference(gpu_ctx, golden):
+    api = _api()
+    g = golden("kats")
+    a = api.gen_laplacian([20, 20])
+    st = api.lanczos_run(a, g["lanczos_start"], 30)
+    assert st.steps == 30 and not st.breakdown
+    assert np.allclose(st.alpha, g["lanczos_alpha"], rtol=0, atol=1e-12)
+    assert np.allclose(st.beta, g["lanczos_beta"], rtol=0, atol=1e-12)
+    assert abs(st.next_beta - float(g["lanczos_next_beta"])) <= 1e-12
+    # full reorthogonalisation keeps the basis orthonormal (test_krylov.cpp:119-143)
+    st2 = api.lanczos_run(a, g["lanczos_start"], 60, want_basis=True)
+    Q = st2.basis.T
+    assert np.max(np.abs(Q.T @ Q - np.eye(st2.steps))) <= 1e-12
+    # breakdown on an exact eigenvector start (test_krylov.cpp:104-117)
+    k = 3
+    v = np.array([np.sin(k * np.pi * (i + 1) / 21.0) for i in range(20)])
+    one = api.gen_laplacian([20])
+    sb = api.lanczos_run(one, v, 10)
+    assert sb.breakdown and sb.steps == 1
+
+
+def test_paired_cgs2_matches_reference(gpu_ctx, golden):
+    api = _api()
+    g = golden("kats")
+    t, h = api.paired_cgs2(g["cgs_t"], g["cgs_W"], np.zeros(25))
+    assert np.max(np.abs(t - g["cgs_t_out"])) <= 1e-13
+    assert np.max(np.abs(h - g["cgs_h"])) <= 1e-13
+
+
+def test_empty_slice_two_restarts(gpu_ctx):
+    # test_eigensolvers.cpp:226-240: nothing in (4.2, 4.8) of diag(1..10)
+    api = _api()
+    a = api.CsrMatrix.diag(np.arange(1.0, 11.0))
+    f = api.find_pol(4.2, 4.8, api.SpectralBounds(0.5, 10.5))
+    cfg = api.SolverConfig(m=40)
+    tr = api.cheb_lan_tr(a, None, f, 4.2, 4.8, cfg)
+    assert tr.eigenvalues.size == 0 and tr.niter == 20 and not tr.hit_max_its
+    nr = api.cheb_lan_nr(a, None, f, 4.2, 4.8, cfg)
+    assert nr.eigenvalues.size == 0 and not nr.hit_max_its
+
+
+def test_deflation_complement(gpu_ctx):
+    # test_eigensolvers.cpp:242-283
+    api = _api()
+    a = api.gen_laplacian([400])
+    allv = api.laplacian_analytic_eigs([400])
+    xi, eta = 0.1, 0.13
+    oracle = allv[(allv >= xi) & (allv <= eta)]
+    assert oracle.size == 6
+    f = api.find_pol(xi, eta, api.SpectralBounds(allv[0] - 1e-9, allv[-1] + 1e-9))
+    cfg = api.SolverConfig(est_count=6)
+    full = api.cheb_lan_tr(a, None, f, xi, eta, cfg)
+    assert np.max(np.abs(full.eigenvalues - oracle)) <= 1e-8
+    half = api.DeflationSet(full.vectors[:, :3].copy(), full.eigenvalues[:3].copy())
+    rest = api.cheb_lan_tr(a, None, f, xi, eta, cfg, half)
+    assert rest.eigenvalues.size == 3
+    assert np.max(np.abs(rest.eigenvalues - full.eigenvalues[3:])) <= 1e-8
+    whole = api.DeflationSet(full.vectors.copy(), full.eigenvalues.copy())
+    assert api.cheb_lan_tr(a, None, f, xi, eta, cfg, whole).eigenvalues.size == 0
+    assert api.cheb_lan_nr(a, None, f, xi, eta, cfg, whole).eigenvalues.size == 0
+    bad = api.DeflationSet(np.stack([full.vectors[:, 0]] * 2, axis=1), full.eigenvalues[[0, 0]])
+    with pytest.raises(ValueError):
+        api.cheb_lan_tr(a, None, f, xi, eta, cfg, bad)
+
+
+def test_interval_growth_keeps_found(gpu_ctx):
+    # test_eigensolvers.cpp:331-357
+    api = _api()
+    a = api.gen_laplacian([400])
+    allv = api.laplacian_analytic_eigs([400])
+    b = api.SpectralBounds(allv[0] - 1e-9, allv[-1] + 1e-9)
+    found = []
+    for lo, hi in ((0.10, 0.12), (0.08, 0.14), (0.05, 0.20)):
+        oracle = allv[(allv >= lo) & (allv <= hi)]
+        r = api.cheb_lan_nr(a, None, api.find_pol(lo, hi, b), lo, hi,
+                            api.SolverConfig(est_count=int(oracle.size)))
+        assert r.eigenvalues.size == oracle.size
+        assert np.max(np.abs(r.eigenvalues - oracle)) <= 1e-8
+        found.append(r.eigenvalues)
+    for k in range(2):
+        for v in found[k]:
+            assert np.min(np.abs(found[k + 1] - v)) <= 1e-8
+
+
+def test_op_accounting_and_config_validation(gpu_ctx):
+    # test_eigensolvers.cpp:382-406 (100 applications book 100 k A-products) and :440-472
+    api = _api()
+    a = api.gen_laplacian([24])
+    f = api.find_pol(0.5, 1.0, api.SpectralBounds(0.0, 4.0))
+    v = np.random.default_rng(5).standard_normal(24)
+    cnt = api.Counters()
+    for _ in range(100):
+        api.apply_pol(f, a, v, cnt)
+    assert cnt.n_A_matvec == 100 * f.k
+    d = api.CsrMatrix.diag(np.arange(1.0, 11.0))
+    g = api.find_pol(2.5, 4.5, api.SpectralBounds(0.5, 10.5))
+    for bad in (dict(m=3), dict(ncycle=0), dict(res_tol=0.0), dict(est_count=-1)):
+        with pytest.raises(ValueError):
+            api.cheb_lan_tr(d, None, g, 2.5, 4.5, api.SolverConfig(**bad))
+    with pytest.raises(ValueError):
+        api.cheb_lan_nr(d, None, g, 4.5, 2.5)
+    with pytest.raises(ValueError):
+        api.cheb_lan_nr(d, api.CsrMatrix.identity(5), g, 2.5, 4.5)
+    r = api.cheb_lan_nr(d, None, g, 2.5, 4.5)
+    assert np.allclose(r.eigenvalues, [3.0, 4.0], atol=1e-10, rtol=0)
+    assert r.niter > 0 and r.counters.t_total > 0
+
+
+def pick_window(allv, start, count):
+    """acceptance.cpp:78-89: consecutive eigenvalues with both ends in clear gaps (1e-6)."""
+    min_gap = 1e-6
+    i0 = max(1, start)
+    while i0 + 1 < allv.size and allv[i0] - allv[i0 - 1] <= min_gap:
+        i0 += 1
+    i1 = min(allv.size - 2, i0 + count - 1)
+    while i1 + 1 < allv.size - 1 and allv[i1 + 1] - allv[i1] <= min_gap:
+        i1 += 1
+    return 0.5 * (allv[i0 - 1] + allv[i0]), 0.5 * (allv[i1] + allv[i1 + 1]), allv[i0:i1 + 1]
+
+
+@pytest.mark.parametrize("dims", [[16, 16, 16], [60, 60]])
+def test_acceptance_windows_all_drivers(gpu_ctx, dims):
+    # acceptance.cpp criterion 1 (polynomial drivers): windows near the bottom, middle and top,
+    # bounds from lan_tr_bounds(1e-4, 60, 40, 1234) (acceptance.cpp:65-69), res_tol 5e-10
+    api = _api()
+    a = api.gen_laplacian(dims)
+    allv = api.laplacian_analytic_eigs(dims)
+    n = a.n
+    b = api.lan_tr_bounds(a, 1e-4, 60, 40, 1234)
+    for start in (40, n // 2, n - 120):
+        xi, eta, oracle = pick_window(allv, start, 32)
+        assert 20 <= oracle.size <= 80
+        cfg = api.SolverConfig(est_count=int(oracle.size), res_tol=5e-10)
+        f = api.find_pol(xi, eta, b)
+        for drv in (api.cheb_lan_nr, api.cheb_lan_tr):
+            r = drv(a, None, f, xi, eta, cfg)
+            assert r.eigenvalues.size == oracle.size
+            assert np.max(np.abs(r.eigenvalues - oracle)) <= 1e-8
+            assert np.max(r.residuals) <= 1e-8
+            for i in range(0, oracle.size, 9):
+                lam, res = api.rayleigh_and_residual(a, None, r.vectors[:, i])
+                assert res <= 1e-8 and abs(lam - r.eigenvalues[i]) <= 1e-10
