@@ -1,0 +1,3 @@
+#pragma once
+// Drop-in name for proj/include/sliceeig/rng.hpp: the B200 facade (see sliceeig_b200.hpp).
+#include "sliceeig/sliceeig_b200.hpp"
