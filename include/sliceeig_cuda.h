@@ -137,6 +137,11 @@ SE_API int se_cheb_apply_dev(se_ctx* ctx, const se_csr* a, const se_poly_filter*
 SE_API int se_filter_bench(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int reps,
                            double* ms, long* launches, double* bytes);
 
+/* Production timing of one reorthogonalisation pass (orth.hpp:19-32: coef = W^T t, t -= W coef,
+ * ||t||) against an n x k basis, graph-captured and replayed `reps` times between CUDA events.
+ * Algorithmic bytes per pass: 16 n k + 24 n. */
+SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
+
 /* ---- filters (host, filter_poly.hpp) -------------------------------------------------------- */
 SE_API int se_damping_multipliers(int k, int damping, double* out);            /* :41-60   */
 SE_API int se_chebyshev_coeffs(double gamma, int k, double* out);              /* :30-39   */

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -356,6 +357,10 @@ int se_filter_bench(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int r
   });
 }
 
+int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms) {
+  return guard([&] { cgs_bench(C(ctx), n, k, reps, *ms); });
+}
+
 int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
                   double* out, long* n_matvec) {
   return guard([&] {
@@ -433,6 +438,7 @@ constexpr int kBlock = 16;
 void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, int n_vec,
                       int probe_kind, std::uint64_t seed, int first, int count, Vec& zeta,
                       Vec* per_probe = nullptr) {
+  static const bool doubling = std::getenv("SE_KPM_DIRECT") == nullptr;
   if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
   if (m < 1 || n_vec < 1) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
   if (a.n < 1) fail(SE_EINVAL, "dos: empty operator");
@@ -456,38 +462,83 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
   const size_t blk = (size_t)n * kBlock;
   double *V = dev_alloc<double>(blk), *X[3];
   for (double*& x : X) x = dev_alloc<double>(blk);
-  double* dz = dev_alloc<double>((size_t)(m + 1) * kBlock);
+  double* dz = dev_alloc<double>((size_t)(m + 3) * kBlock);
   k::Scratch s;
   s.cap = k::kpm_scratch_doubles(c, n);
   s.buf = dev_alloc<double>(s.cap);
   s.cnt = dev_alloc<unsigned>(1);
   s.ncnt = 1;
   SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned), c.stream));
-  double* hbuf = nullptr;
-  SE_CUDA(cudaMallocHost(&hbuf, sizeof(double) * blk));
-  Vec probe(n), hz((size_t)(m + 1) * kBlock);
-  try {
-    for (int b0 = 0; b0 < count; b0 += kBlock) {
-      const int b = std::min(kBlock, count - b0);
-      SE_CUDA(cudaStreamSynchronize(c.stream));  // hbuf reuse
+  // Two pinned staging buffers: the host draws block q+1 (one mt19937_64 stream, probe order)
+  // while the device runs the m-step recurrence of block q.
+  double* hb[2] = {nullptr, nullptr};
+  SE_CUDA(cudaMallocHost(&hb[0], sizeof(double) * blk));
+  SE_CUDA(cudaMallocHost(&hb[1], sizeof(double) * blk));
+  double* hbuf = hb[0];
+  Vec hz((size_t)(m + 3) * kBlock);
+  auto fill = [&](int b0, double* buf) {
+    // probe j = draws [j n, (j+1) n) of the one stream; written row-major (n x b) through a
+    // cache-blocked transpose
+    const int b = std::min(kBlock, count - b0);
+    std::vector<double> tmp((size_t)b * n);
+    for (int j = 0; j < b; ++j) draw(tmp.data() + (size_t)j * n, n);
+    constexpr int kRowBlk = 2048;
+    for (int i0 = 0; i0 < n; i0 += kRowBlk) {
+      const int i1 = std::min(n, i0 + kRowBlk);
       for (int j = 0; j < b; ++j) {
-        draw(probe.data(), n);
-        for (int i = 0; i < n; ++i) hbuf[(size_t)i * b + j] = probe[i];
+        const double* src = tmp.data() + (size_t)j * n;
+        for (int i = i0; i < i1; ++i) buf[(size_t)i * b + j] = src[i];
       }
+    }
+  };
+  std::future<void> next = std::async(std::launch::async, fill, 0, hb[0]);
+  try {
+    for (int b0 = 0, q = 0; b0 < count; b0 += kBlock, ++q) {
+      const int b = std::min(kBlock, count - b0);
+      next.get();
+      hbuf = hb[q & 1];
       SE_CUDA(cudaMemcpyAsync(V, hbuf, sizeof(double) * (size_t)n * b, cudaMemcpyHostToDevice, c.stream));
-      k::kpm_step(c, s, a, b, true, V, V, nullptr, X[0], cc, d, dz, 0);
+      SE_CUDA(cudaStreamSynchronize(c.stream));  // hbuf consumed; the other buffer is free
+      if (b0 + kBlock < count) next = std::async(std::launch::async, fill, b0 + kBlock, hb[(q + 1) & 1]);
+      if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
+      k::kpm_step(c, s, a, b, 1, V, V, nullptr, X[0], cc, d, dz, 0);
       const double* w0 = V;
       double *w1 = X[0], *tb = X[1], *spare = X[2];
-      for (int kk = 2; kk <= m; ++kk) {
-        k::kpm_step(c, s, a, b, false, V, w0, w1, tb, cc, d, dz, kk);
+      // doubling (default): step k gives w_{k+1} and the dots w_k.w_k, w_k.w_{k+1}, i.e. moments
+      // 2k and 2k+1 -- floor(m/2) SpMMs instead of m-1; direct: the reference's recurrence.
+      const int last = doubling ? m / 2 : m;
+      int launched = 1;
+      for (int kk = doubling ? 1 : 2; kk <= last; ++kk, ++launched) {
+        k::kpm_step(c, s, a, b, doubling ? 2 : 0, V, w0, w1, tb, cc, d, dz, kk);
         double* freed = (w0 == V) ? spare : const_cast<double*>(w0);  // w0 <- w1 <- t <- free
         w0 = w1;
         w1 = tb;
         tb = freed;
       }
-      SE_CUDA(cudaMemcpyAsync(hz.data(), dz, sizeof(double) * (size_t)(m + 1) * b,
+      if (c.time_filter) {
+        SE_CUDA(cudaEventRecord(c.ev1, c.stream));
+        SE_CUDA(cudaEventSynchronize(c.ev1));
+        float ms = 0.f;
+        SE_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+        c.filter_ms += ms;
+        c.filter_launches += launched;
+        // block-step bytes: direct Abytes + 32 n b; doubling drops the probe
+        // stream (Abytes + 24 n b)
+        c.filter_bytes += (double)launched * (a.abytes() + (doubling ? 24.0 : 32.0) * n * b);
+      }
+      const int slots = doubling ? 2 * (last + 1) : m + 1;
+      SE_CUDA(cudaMemcpyAsync(hz.data(), dz, sizeof(double) * (size_t)slots * b,
                               cudaMemcpyDeviceToHost, c.stream));
       SE_CUDA(cudaStreamSynchronize(c.stream));
+      if (doubling) {  // zeta_2k = 2 w_k.w_k - zeta_0, zeta_2k+1 = 2 w_k.w_k+1 - zeta_1
+        for (int j = 0; j < b; ++j) {
+          const double z0 = hz[j], z1 = hz[(size_t)b + j];
+          for (int kk = 2; kk <= m; ++kk) {
+            const double raw = hz[(size_t)kk * b + j];
+            hz[(size_t)kk * b + j] = 2.0 * raw - ((kk & 1) ? z1 : z0);
+          }
+        }
+      }
       for (int j = 0; j < b; ++j)  // probe order (dos.hpp:100-106)
         for (int kk = 0; kk <= m; ++kk) {
           zeta[kk] += hz[(size_t)kk * b + j];
@@ -495,12 +546,16 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
         }
     }
   } catch (...) {
-    cudaFreeHost(hbuf);
+    if (next.valid()) next.wait();
+    cudaStreamSynchronize(c.stream);
+    cudaFreeHost(hb[0]);
+    cudaFreeHost(hb[1]);
     for (void* p : {(void*)V, (void*)X[0], (void*)X[1], (void*)X[2], (void*)dz, (void*)s.buf, (void*)s.cnt})
       dev_free(p);
     throw;
   }
-  cudaFreeHost(hbuf);
+  cudaFreeHost(hb[0]);
+  cudaFreeHost(hb[1]);
   for (void* p : {(void*)V, (void*)X[0], (void*)X[1], (void*)X[2], (void*)dz, (void*)s.buf, (void*)s.cnt})
     dev_free(p);
 }

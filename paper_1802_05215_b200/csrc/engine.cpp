@@ -995,3 +995,61 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
   for (void* p : {(void*)v, (void*)out, (void*)fb[0], (void*)fb[1], (void*)fb[2]}) dev_free(p);
 }
 }  // namespace se
+
+namespace se {
+// Time one classical Gram-Schmidt pass (k_gemvt + k_gemvn with norm) against an n x k basis, as it
+// runs inside the Lanczos step graph (production path), replayed `reps` times between events.
+void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) {
+  if (n < 1 || kcols < 1 || reps < 1) fail(SE_EINVAL, "se_cgs_bench: bad sizes");
+  double* W = dev_alloc<double>((size_t)n * kcols);
+  double* t = dev_alloc<double>(n);
+  double* coef = dev_alloc<double>(kcols);
+  Ctl* ctl = dev_alloc<Ctl>(1);
+  k::Scratch s;
+  s.cap = k::cgs_scratch_doubles(c, n, kcols);
+  s.ncnt = k::cgs_counter_slots(kcols);
+  s.buf = dev_alloc<double>(s.cap);
+  s.cnt = dev_alloc<unsigned>(s.ncnt);
+  cudaGraphExec_t ge = nullptr;
+  auto cleanup = [&] {
+    if (ge) cudaGraphExecDestroy(ge);
+    for (void* p : {(void*)W, (void*)t, (void*)coef, (void*)ctl, (void*)s.buf, (void*)s.cnt}) dev_free(p);
+  };
+  try {
+    SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
+    // deterministic pseudo-random contents (values do not affect the traffic)
+    std::vector<double> h((size_t)n);
+    Rng rng(7);
+    rng.normal_fill(h.data(), n);
+    for (int j = 0; j < kcols; ++j)
+      SE_CUDA(cudaMemcpyAsync(W + (size_t)j * n, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    SE_CUDA(cudaMemcpyAsync(t, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    Ctl z{};
+    z.i = kcols - 1;
+    z.before = 1.0;
+    SE_CUDA(cudaMemcpyAsync(ctl, &z, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    SE_CUDA(cudaStreamSynchronize(c.stream));
+    const long before = c.launches;
+    SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    k::cgs_pass(c, s, n, t, W, false, false, ctl, nullptr, coef, kcols);
+    cudaGraph_t g;
+    SE_CUDA(cudaStreamEndCapture(c.stream, &g));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    const long per = c.launches - before;
+    SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev0, c.stream));
+    for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev1, c.stream));
+    SE_CUDA(cudaEventSynchronize(c.ev1));
+    float fms = 0.f;
+    SE_CUDA(cudaEventElapsedTime(&fms, c.ev0, c.ev1));
+    ms = fms;
+    c.launches += per * (reps + 1);
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+}  // namespace se

@@ -68,3 +68,6 @@ std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter&
 namespace se {
 void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& ms, long& launches);
 }
+namespace se {
+void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms);
+}

@@ -7,6 +7,7 @@
 // which are compiled for baseline x86-64 without FMA.  The filter application is therefore
 // bit-identical to the reference's on the same input vector.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -134,46 +135,104 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
 // j owns probe j and sums that row in storage order (bitwise the reference's per-probe matvec).
 // The moment dot v_j . T_k v_j is reduced deterministically: per-CTA partials + last-CTA sum.
 constexpr int kB = 16;
+constexpr int kKpmFirst = 1, kKpmDirect = 0, kKpmDoubling = 2;
 constexpr int kKpmThreads = 256;
 
+constexpr int kKRows = 32;   // rows per tile: 16 half-warps x 2 rows
+constexpr int kKSlots = 256; // A entries (and gathered probe rows) staged per pass
+
+// Tile kernel with the gathers done by cp.async: (1) the tile's A entries are staged into shared
+// memory; (2) every probe row they reference (16 doubles = 128 B) is copied into shared memory
+// with 16-byte cp.async -- all of a tile's gathers are in flight at once without occupying
+// registers; (3) each half-warp sums its rows from shared memory in storage order.
 __global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
     int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
-    int b, int first, const double* __restrict__ v, const double* __restrict__ w0,
+    int b, int mode, const double* __restrict__ v, const double* __restrict__ w0,
     const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
     double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
+  const bool first = mode == kKpmFirst;
+  const bool dbl = mode == kKpmDoubling;
+  __shared__ __align__(16) double s_v[kKSlots + 8];
+  __shared__ __align__(16) int s_c[kKSlots + 8];
+  __shared__ __align__(16) double s_x[kKSlots][kB];
   const int lane = threadIdx.x & (kB - 1);
-  const int hw = (blockIdx.x * kKpmThreads + threadIdx.x) / kB;  // global half-warp
-  const int nhw = gridDim.x * kKpmThreads / kB;
+  const int hw = threadIdx.x / kB;
   const bool live = lane < b;
-  double acc0 = 0.0, acc1 = 0.0;  // first: v.w0 and v.w1 ; next: v.t
-  for (int r = hw; r < n; r += nhw) {
-    const int s = __ldg(rp + r), e = __ldg(rp + r + 1);
-    const double* __restrict__ src = first ? w0 : w1;
-    double acc = 0.0;
-    if (live) {
-      int p = s;
-      for (; p + 2 <= e; p += 2) {
-        const int c0 = __ldg(ci + p), c1 = __ldg(ci + p + 1);
-        const double a0 = __ldg(vals + p), a1 = __ldg(vals + p + 1);
-        const double x0 = __ldg(src + (size_t)c0 * b + lane);
-        const double x1 = __ldg(src + (size_t)c1 * b + lane);
-        acc = add(acc, mul(a0, x0));
-        acc = add(acc, mul(a1, x1));
+  const double* __restrict__ src = first ? w0 : w1;
+  double acc0 = 0.0, acc1 = 0.0;
+  const int ntiles = (n + kKRows - 1) / kKRows;
+  const int parts = (b * 8 + 15) / 16;  // 16-byte pieces per probe row
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kKRows, rend = min(r0 + kKRows, n);
+    const int base = __ldg(rp + r0), end = __ldg(rp + rend);
+    int rs[2], re[2];
+    double xr[2], pr[2], vr[2], accr[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = r0 + hw + 16 * q;
+      rs[q] = re[q] = 0;
+      xr[q] = pr[q] = vr[q] = accr[q] = 0.0;
+      if (r < n) {
+        rs[q] = __ldg(rp + r);
+        re[q] = __ldg(rp + r + 1);
+        if (live) {
+          const size_t o = (size_t)r * b + lane;
+          xr[q] = __ldg(src + o);
+          if (!dbl) vr[q] = __ldg(v + o);
+          if (!first) pr[q] = __ldg(w0 + o);
+        }
       }
-      if (p < e) acc = add(acc, mul(__ldg(vals + p), __ldg(src + (size_t)__ldg(ci + p) * b + lane)));
-      const size_t o = (size_t)r * b + lane;
-      const double xr = src[o];
-      // (A w - c w) / d   (dos.hpp:99: division by d, unlike the filter's 1/d multiply)
-      const double m = __ddiv_rn(sub(acc, mul(cc, xr)), d);
-      const double vr = v[o];
-      if (first) {
-        t[o] = m;  // w1
-        acc0 = add(acc0, mul(vr, xr));
-        acc1 = add(acc1, mul(vr, m));
-      } else {
-        const double tk = sub(mul(2.0, m), w0[o]);
-        t[o] = tk;
-        acc0 = add(acc0, mul(vr, tk));
+    }
+    for (int c0 = base; c0 < end; c0 += kKSlots) {
+      const int cn = min(kKSlots, end - c0), cend = c0 + cn;
+      const int va = c0 & ~1, ca = c0 & ~3;
+      const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
+      __syncthreads();
+      for (int q = threadIdx.x; q < nv16; q += kKpmThreads)
+        cp_async16(&s_v[2 * q], vals + va + 2 * q, 8 * min(2, cend - (va + 2 * q)));
+      for (int q = threadIdx.x; q < nc16; q += kKpmThreads)
+        cp_async16(&s_c[4 * q], ci + ca + 4 * q, 4 * min(4, cend - (ca + 4 * q)));
+      cp_async_wait_all();
+      __syncthreads();
+      // gather the referenced probe rows (slot p <-> entry c0 + p)
+      for (int q = threadIdx.x; q < cn * parts; q += kKpmThreads) {
+        const int p = q / parts, part = q - p * parts;
+        const int col = s_c[c0 + p - ca];
+        const int bytes = min(16, b * 8 - part * 16);
+        cp_async16(&s_x[p][2 * part], src + (size_t)col * b + 2 * part, bytes);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int p0 = max(rs[q], c0), pend = min(re[q], cend);
+          for (int p = p0; p < pend; ++p) accr[q] = add(accr[q], mul(s_v[p - va], s_x[p - c0][lane]));
+        }
+      }
+    }
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = r0 + hw + 16 * q;
+        if (r >= n) continue;
+        const size_t o = (size_t)r * b + lane;
+        // (A w - c w) / d   (dos.hpp:99: division by d, unlike the filter's 1/d multiply)
+        const double m = __ddiv_rn(sub(accr[q], mul(cc, xr[q])), d);
+        if (first) {
+          t[o] = m;  // w1
+          acc0 = add(acc0, mul(vr[q], xr[q]));
+          acc1 = add(acc1, mul(vr[q], m));
+        } else {
+          const double tk = sub(mul(2.0, m), pr[q]);
+          t[o] = tk;
+          if (dbl) {  // w_k.w_k and w_k.w_{k+1} (T_2k = 2 T_k^2 - 1, T_2k+1 = 2 T_k T_k+1 - T_1)
+            acc0 = add(acc0, mul(xr[q], xr[q]));
+            acc1 = add(acc1, mul(xr[q], tk));
+          } else {
+            acc0 = add(acc0, mul(vr[q], tk));
+          }
+        }
       }
     }
   }
@@ -207,11 +266,12 @@ __global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
   if (sub8 == 0) {
     const int which = col / kB, j = col % kB;
     if (j < b) {
-      if (first) {
-        zeta[(size_t)(which) * b + j] = q;  // moments 0 and 1, probe j
-      } else if (which == 0) {
+      if (first)
+        zeta[(size_t)which * b + j] = q;  // v.v and v.w1, probe j
+      else if (dbl)
+        zeta[(size_t)(2 * kmom + which) * b + j] = q;  // w_k.w_k, w_k.w_{k+1}
+      else if (which == 0)
         zeta[(size_t)kmom * b + j] = q;
-      }
     }
   }
   if (threadIdx.x == 0) *counter = 0u;
@@ -298,17 +358,17 @@ void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
 }
 
 int kpm_blocks(const Ctx& c, int n) {
-  return std::max(1, std::min(c.num_sms * 8, (int)(((long)n * kB + kKpmThreads - 1) / kKpmThreads)));
+  return std::max(1, std::min(c.num_sms * 8, (n + kKRows - 1) / kKRows));
 }
 size_t kpm_scratch_doubles(const Ctx& c, int n) { return (size_t)2 * kB * kpm_blocks(c, n); }
 
-void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, bool first, const double* v,
+void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const double* v,
               const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
               int kmom) {
   const int blocks = kpm_blocks(c, a.n);
   if (kpm_scratch_doubles(c, a.n) > s.cap || s.ncnt < 1) fail(SE_EINVAL, "internal: kpm scratch");
-  k_kpm_step<<<blocks, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, first ? 1 : 0, v, w0,
-                                                   w1, t, cc, d, s.buf, s.cnt, zeta_dev, kmom);
+  k_kpm_step<<<blocks, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t,
+                                                   cc, d, s.buf, s.cnt, zeta_dev, kmom);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
