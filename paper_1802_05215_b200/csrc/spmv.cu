@@ -135,26 +135,27 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
 // j owns probe j and sums that row in storage order (bitwise the reference's per-probe matvec).
 // The moment dot v_j . T_k v_j is reduced deterministically: per-CTA partials + last-CTA sum.
 constexpr int kB = 16;
-constexpr int kKpmFirst = 1, kKpmDirect = 0, kKpmDoubling = 2;
+constexpr int kKpmFirst = 1, kKpmDoubling = 2;  // 0: direct recurrence
 constexpr int kKpmThreads = 256;
 
-constexpr int kKRows = 32;   // rows per tile: 16 half-warps x 2 rows
-constexpr int kKSlots = 256; // A entries (and gathered probe rows) staged per pass
+constexpr int kKRows = 64;   // rows per tile: 16 half-warps x 4 rows
+constexpr int kKSlots = 512; // A entries (and gathered probe rows) staged per pass
 
 // Tile kernel with the gathers done by cp.async: (1) the tile's A entries are staged into shared
 // memory; (2) every probe row they reference (16 doubles = 128 B) is copied into shared memory
 // with 16-byte cp.async -- all of a tile's gathers are in flight at once without occupying
 // registers; (3) each half-warp sums its rows from shared memory in storage order.
-__global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
+__global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_step(
     int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
     int b, int mode, const double* __restrict__ v, const double* __restrict__ w0,
     const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
     double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
   const bool first = mode == kKpmFirst;
   const bool dbl = mode == kKpmDoubling;
-  __shared__ __align__(16) double s_v[kKSlots + 8];
-  __shared__ __align__(16) int s_c[kKSlots + 8];
-  __shared__ __align__(16) double s_x[kKSlots][kB];
+  extern __shared__ __align__(16) unsigned char kpm_smem[];
+  double(*s_x)[kB] = reinterpret_cast<double(*)[kB]>(kpm_smem);
+  double* s_v = reinterpret_cast<double*>(kpm_smem + sizeof(double) * kKSlots * kB);
+  int* s_c = reinterpret_cast<int*>(kpm_smem + sizeof(double) * (kKSlots * kB + kKSlots + 8));
   const int lane = threadIdx.x & (kB - 1);
   const int hw = threadIdx.x / kB;
   const bool live = lane < b;
@@ -165,10 +166,10 @@ __global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int r0 = tile * kKRows, rend = min(r0 + kKRows, n);
     const int base = __ldg(rp + r0), end = __ldg(rp + rend);
-    int rs[2], re[2];
-    double xr[2], pr[2], vr[2], accr[2];
+    int rs[4], re[4];
+    double xr[4], pr[4], vr[4], accr[4];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 4; ++q) {
       const int r = r0 + hw + 16 * q;
       rs[q] = re[q] = 0;
       xr[q] = pr[q] = vr[q] = accr[q] = 0.0;
@@ -195,17 +196,23 @@ __global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
       cp_async_wait_all();
       __syncthreads();
       // gather the referenced probe rows (slot p <-> entry c0 + p)
-      for (int q = threadIdx.x; q < cn * parts; q += kKpmThreads) {
-        const int p = q / parts, part = q - p * parts;
-        const int col = s_c[c0 + p - ca];
-        const int bytes = min(16, b * 8 - part * 16);
-        cp_async16(&s_x[p][2 * part], src + (size_t)col * b + 2 * part, bytes);
+      if (b == kB) {  // full blocks: 8 x 16-byte pieces per 128-byte probe row
+        for (int q = threadIdx.x; q < cn * 8; q += kKpmThreads) {
+          const int p = q >> 3, part = q & 7;
+          cp_async16(&s_x[p][2 * part], src + (size_t)s_c[c0 + p - ca] * kB + 2 * part, 16);
+        }
+      } else {
+        for (int q = threadIdx.x; q < cn * parts; q += kKpmThreads) {
+          const int p = q / parts, part = q - p * parts;
+          const int bytes = min(16, b * 8 - part * 16);
+          cp_async16(&s_x[p][2 * part], src + (size_t)s_c[c0 + p - ca] * b + 2 * part, bytes);
+        }
       }
       cp_async_wait_all();
       __syncthreads();
       if (live) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < 4; ++q) {
           const int p0 = max(rs[q], c0), pend = min(re[q], cend);
           for (int p = p0; p < pend; ++p) accr[q] = add(accr[q], mul(s_v[p - va], s_x[p - c0][lane]));
         }
@@ -213,7 +220,7 @@ __global__ void __launch_bounds__(kKpmThreads) k_kpm_step(
     }
     if (live) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < 4; ++q) {
         const int r = r0 + hw + 16 * q;
         if (r >= n) continue;
         const size_t o = (size_t)r * b + lane;
@@ -367,8 +374,14 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
               int kmom) {
   const int blocks = kpm_blocks(c, a.n);
   if (kpm_scratch_doubles(c, a.n) > s.cap || s.ncnt < 1) fail(SE_EINVAL, "internal: kpm scratch");
-  k_kpm_step<<<blocks, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t,
-                                                   cc, d, s.buf, s.cnt, zeta_dev, kmom);
+  constexpr size_t smem = sizeof(double) * (kKSlots * kB + kKSlots + 8) + sizeof(int) * (kKSlots + 8);
+  static bool attr = false;
+  if (!attr) {
+    SE_CUDA(cudaFuncSetAttribute(k_kpm_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_kpm_step<<<blocks, kKpmThreads, smem, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t,
+                                                      cc, d, s.buf, s.cnt, zeta_dev, kmom);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
