@@ -235,7 +235,7 @@ int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, co
       SE_CUDA(cudaMemcpyAsync(a.ci, col_idx, sizeof(int) * a.nnz, cudaMemcpyHostToDevice, c.stream));
       SE_CUDA(cudaMemcpyAsync(a.v, vals, sizeof(double) * a.nnz, cudaMemcpyHostToDevice, c.stream));
     }
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     *out = h.release();
   });
 }
@@ -253,7 +253,7 @@ int se_csr_gen_laplacian(se_ctx* ctx, int ndims, const int* dims, se_csr** out) 
     auto h = std::make_unique<se_csr>();
     h->a.device = c.device;
     k::gen_laplacian(c, ndims, dims, h->a);
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     *out = h.release();
   });
 }
@@ -274,7 +274,7 @@ int se_csr_download(se_ctx* ctx, const se_csr* a, int* row_ptr, int* col_idx, do
       SE_CUDA(cudaMemcpyAsync(col_idx, m.ci, sizeof(int) * m.nnz, cudaMemcpyDeviceToHost, c.stream));
       SE_CUDA(cudaMemcpyAsync(vals, m.v, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, c.stream));
     }
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
   });
 }
 
@@ -285,7 +285,7 @@ int se_csr_scale_sym(se_ctx* ctx, se_csr* a, const double* d_host) {
     double* d = dev_alloc<double>(a->a.n);
     SE_CUDA(cudaMemcpyAsync(d, d_host, sizeof(double) * a->a.n, cudaMemcpyHostToDevice, c.stream));
     k::csr_scale_sym(c, a->a, d);
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     dev_free(d);
   });
 }
@@ -312,7 +312,7 @@ int se_spmv(se_ctx* ctx, const se_csr* a, const double* x, double* y) {
     StepOp op;
     apply_filter_dev(c, m, op, 1, dx, dy);
     SE_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * m.n, cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     dev_free(dx);
     dev_free(dy);
   });
@@ -373,7 +373,7 @@ int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nve
     SE_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, c.stream));
     apply_filter_dev(c, m, to_op(pf), nvec, dv, dout);
     SE_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     dev_free(dv);
     dev_free(dout);
     if (n_matvec) *n_matvec += (long)pf.k * nvec;
@@ -498,7 +498,7 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
       next.get();
       hbuf = hb[q & 1];
       SE_CUDA(cudaMemcpyAsync(V, hbuf, sizeof(double) * (size_t)n * b, cudaMemcpyHostToDevice, c.stream));
-      SE_CUDA(cudaStreamSynchronize(c.stream));  // hbuf consumed; the other buffer is free
+      ctx_sync(c);  // hbuf consumed; the other buffer is free
       if (b0 + kBlock < count) next = std::async(std::launch::async, fill, b0 + kBlock, hb[(q + 1) & 1]);
       if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
       k::kpm_step(c, s, a, b, 1, V, V, nullptr, X[0], cc, d, dz, 0);
@@ -529,7 +529,7 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
       const int slots = doubling ? 2 * (last + 1) : m + 1;
       SE_CUDA(cudaMemcpyAsync(hz.data(), dz, sizeof(double) * (size_t)slots * b,
                               cudaMemcpyDeviceToHost, c.stream));
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       if (doubling) {  // zeta_2k = 2 w_k.w_k - zeta_0, zeta_2k+1 = 2 w_k.w_k+1 - zeta_1
         for (int j = 0; j < b; ++j) {
           const double z0 = hz[j], z1 = hz[(size_t)b + j];
@@ -699,7 +699,7 @@ int se_paired_cgs2(se_ctx* ctx, int n, int kq, const double* W, double* t, doubl
     Ctl* ctl = dev_alloc<Ctl>(1);
     k::Scratch s;
     s.cap = k::cgs_scratch_doubles(c, n, kq);
-    s.ncnt = k::cgs_counter_slots(kq);
+    s.ncnt = k::cgs_counter_slots(n, kq);
     s.buf = dev_alloc<double>(s.cap);
     s.cnt = dev_alloc<unsigned>(s.ncnt);
     auto cleanup = [&] {
@@ -717,7 +717,7 @@ int se_paired_cgs2(se_ctx* ctx, int n, int kq, const double* W, double* t, doubl
       k::norm_before(c, s, n, dt, ctl);
       Ctl h0;
       SE_CUDA(cudaMemcpyAsync(&h0, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       // orth.hpp:72-73: nothing to do for a zero vector or an empty basis
       if (h0.before != 0.0 && kq > 0) {
         // h accumulates every coefficient: run passes with hdiag bookkeeping per column
@@ -728,14 +728,14 @@ int se_paired_cgs2(se_ctx* ctx, int n, int kq, const double* W, double* t, doubl
             Ctl hh;
             SE_CUDA(cudaMemcpyAsync(&hh, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
             SE_CUDA(cudaMemcpyAsync(cf.data(), coef, sizeof(double) * kq, cudaMemcpyDeviceToHost, c.stream));
-            SE_CUDA(cudaStreamSynchronize(c.stream));
+            ctx_sync(c);
             if (pass == 0 || hh.npass == 2)
               for (int j = 0; j < kq; ++j) h[j] += cf[j];
           }
         }
       }
       SE_CUDA(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
     } catch (...) {
       cleanup();
       throw;
@@ -853,7 +853,7 @@ int se_rayleigh_residual(se_ctx* ctx, const se_csr* a, const double* u, double* 
     k::candidate_stats(c, m.n, 1, du, dau, st);
     double h[3];
     SE_CUDA(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     for (void* p : {(void*)du, (void*)dau, (void*)st}) dev_free(p);
     if (!(h[2] > 0.0)) fail(SE_EINVAL, "rayleigh_and_residual: zero (or B-degenerate) vector");
     *lambda = h[0];

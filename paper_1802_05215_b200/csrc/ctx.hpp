@@ -15,7 +15,9 @@ namespace se {
 struct Ctx {
   int device = 0;
   int num_sms = 148;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // current launch stream (bulk Lanczos work: low priority)
+  cudaStream_t bulk = nullptr;     // the low-priority stream
+  cudaStream_t hstream = nullptr;  // high priority: latency-bound host-driven phases
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t solver = nullptr;
   long launches = 0;  // this library's kernel launches issued on `stream`
@@ -26,7 +28,29 @@ struct Ctx {
   long filter_launches = 0;
   double filter_bytes = 0.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evsync = nullptr;
+  cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // profiling of host-driven phases
+  double prof_kernel_ms = 0.0;
+  void* pinned = nullptr;  // staging for host<->device copies (pageable copies serialise
+  size_t pinned_bytes = 0; // across the slice threads sharing a GPU)  // blocking-sync event: host waits sleep instead of spinning
 };
+
+// Route this context's launches to the high-priority stream for a scope (projected eigensolves,
+// stagnation checks, Ritz extraction): with 8 slices sharing a GPU these short, synchronising
+// phases otherwise queue behind other slices' bandwidth-bound reorthogonalisation kernels.
+struct HiPrio {
+  Ctx& c;
+  explicit HiPrio(Ctx& cc) : c(cc) { c.stream = c.hstream; }
+  ~HiPrio() { c.stream = c.bulk; }
+};
+
+// Wait for the work queued on the context's current stream (the host thread blocks instead of
+// spin-polling, so the slice threads sharing a GPU leave the host cores to each other).
+void ctx_sync(Ctx& c);
+// Synchronous host<->device copies through the context's pinned staging buffer.
+void h2d(Ctx& c, void* dst, const void* src, size_t bytes);
+void* staging(Ctx& c, size_t bytes);  // the pinned staging buffer (>= bytes)
+void d2h(Ctx& c, void* dst, const void* src, size_t bytes);
 
 Ctx* ctx_create(int device);
 void ctx_destroy(Ctx* c);

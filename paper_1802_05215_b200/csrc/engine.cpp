@@ -46,7 +46,7 @@ struct Krylov {
     ctl = dev_alloc<Ctl>(1);
     dscal = dev_alloc<double>(4);
     Ctl z{};
-    SE_CUDA(cudaMemcpyAsync(ctl, &z, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    h2d(c, ctl, &z, sizeof(Ctl));
   }
   ~Krylov() {
     cudaStreamSynchronize(c.stream);
@@ -61,7 +61,7 @@ struct Krylov {
 
   void drop_graph() {
     if (gexec) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       cudaGraphExecDestroy(gexec);
     }
     gexec = nullptr;
@@ -81,12 +81,12 @@ struct Krylov {
       dirty = true;
     }
     if (W.cap > arr_cap) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       auto regrow = [&](double*& p) {
         double* q = dev_alloc<double>(W.cap);
         SE_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * W.cap, c.stream));
         if (p) SE_CUDA(cudaMemcpyAsync(q, p, sizeof(double) * arr_cap, cudaMemcpyDeviceToDevice, c.stream));
-        SE_CUDA(cudaStreamSynchronize(c.stream));
+        ctx_sync(c);
         dev_free(p);
         p = q;
       };
@@ -105,9 +105,9 @@ struct Krylov {
     }
     const int wide = std::max(W.cap, L.cap);
     const size_t need = k::cgs_scratch_doubles(c, n, wide);
-    const int slots = k::cgs_counter_slots(wide);
+    const int slots = k::cgs_counter_slots(n, wide);
     if (need > s.cap || slots > s.ncnt) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       dev_free(s.buf);
       dev_free(s.cnt);
       s.cap = need + need / 2;
@@ -122,13 +122,13 @@ struct Krylov {
 
   Ctl get() {
     Ctl h;
-    SE_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, &h, ctl, sizeof(Ctl));
+    ctx_sync(c);
     return h;
   }
   void put(const Ctl& h) {
-    SE_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    h2d(c, ctl, &h, sizeof(Ctl));
+    ctx_sync(c);
   }
   void begin(int i0) {  // new recurrence segment starting at column i0
     Ctl h = get();
@@ -224,17 +224,16 @@ struct Krylov {
   double dot(const double* x, const double* y) {
     k::dot_dev(c, s, n, x, y, dscal);
     double h = 0.0;
-    SE_CUDA(cudaMemcpyAsync(&h, dscal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, &h, dscal, sizeof(double));
+    ctx_sync(c);
     return h;
   }
 
   void download(const double* d, int count, Vec& out, int offset = 0) {
     out.resize(count);
     if (count <= 0) return;
-    SE_CUDA(cudaMemcpyAsync(out.data(), d + offset, sizeof(double) * count, cudaMemcpyDeviceToHost,
-                            c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, out.data(), d + offset, sizeof(double) * count);
+    ctx_sync(c);
   }
 };
 
@@ -257,8 +256,9 @@ struct DevEig {
   }
   // H: m x m column-major host.  Returns device pointer to eigenvectors (ld = m).
   const double* solve(int m, const Vec& H, Vec& values) {
+    HiPrio hp(c);
     if (m > cap) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       dev_free(dA);
       dev_free(dW);
       dev_free(info);
@@ -270,19 +270,17 @@ struct DevEig {
     if (m <= 160) {
       Vec vecs;
       dense_sym_eig(m, H.data(), true, values, vecs);
-      SE_CUDA(cudaMemcpyAsync(dA, vecs.data(), sizeof(double) * (size_t)m * m,
-                              cudaMemcpyHostToDevice, c.stream));
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      h2d(c, dA, vecs.data(), sizeof(double) * (size_t)m * m);
+      ctx_sync(c);
       return dA;
     }
-    SE_CUDA(cudaMemcpyAsync(dA, H.data(), sizeof(double) * (size_t)m * m, cudaMemcpyHostToDevice,
-                            c.stream));
+    h2d(c, dA, H.data(), sizeof(double) * (size_t)m * m);
     int lw = 0;
     if (cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
                                     dA, m, dW, &lw) != CUSOLVER_STATUS_SUCCESS)
       fail(SE_ECUDA, "cusolverDnDsyevd_bufferSize failed");
     if (lw > lwork) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       dev_free(work);
       lwork = lw;
       work = dev_alloc<double>(lwork);
@@ -293,9 +291,9 @@ struct DevEig {
     ++c.launches;
     int hinfo = 0;
     values.resize(m);
-    SE_CUDA(cudaMemcpyAsync(values.data(), dW, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, values.data(), dW, sizeof(double) * m);
+    d2h(c, &hinfo, info, sizeof(int));
+    ctx_sync(c);
     if (hinfo != 0) fail(SE_ENUMERIC, "dense_sym_eig: syevd did not converge");
     return dA;
   }
@@ -317,6 +315,7 @@ struct CandBuf {
   // U = W[:, :steps] Y (Y steps x nc, ld ldy), AU = A U, stats per column.
   void eval(const DevCsr& A, const double* W, int steps, const double* Y, int ldy, int nc,
             Vec& out3) {
+    HiPrio hp(c);
     const int n = A.n;
     devmat_reserve(c, U, n, nc, false);
     devmat_reserve(c, AU, n, nc, false);
@@ -339,9 +338,8 @@ struct CandBuf {
     }
     k::candidate_stats(c, n, nc, U.p, AU.p, stats);
     out3.resize(3 * (size_t)nc);
-    SE_CUDA(cudaMemcpyAsync(out3.data(), stats, sizeof(double) * 3 * nc, cudaMemcpyDeviceToHost,
-                            c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, out3.data(), stats, sizeof(double) * 3 * nc);
+    ctx_sync(c);
   }
 };
 
@@ -392,11 +390,12 @@ struct Slice {
       return;
     }
     if (m > chk_cap) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
+      ctx_sync(c);
       dev_free(chk_work);
       chk_cap = grow(m);
       chk_work = dev_alloc<double>(4 * (size_t)chk_cap + 8);
     }
+    HiPrio hp(c);
     k::tridiag_eigs_above(c, m, d.data(), e.data(), bar, chk_work, vals);
   }
   ~Slice() { dev_free(chk_work); }
@@ -417,7 +416,7 @@ struct Slice {
     for (int attempt = 0; attempt < 16; ++attempt) {
       rng.normal_fill(w.data(), n);
       double* d = kr.W.col(col);
-      SE_CUDA(cudaMemcpyAsync(d, w.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      h2d(c, d, w.data(), sizeof(double) * n);
       if (kr.nlock > 0) k::project_out(c, kr.s, n, kr.nlock, kr.L.p, d, kr.coef_l);
       const double nb = std::sqrt(kr.dot(d, d));
       if (nb > 1e-14) {
@@ -440,16 +439,16 @@ struct Slice {
     if (ndefl <= 0) return;
     const int n = A.n;
     kr.ensure(std::max(kr.W.cap, 1), ndefl);
-    SE_CUDA(cudaMemcpyAsync(kr.L.p, u, sizeof(double) * (size_t)n * ndefl, cudaMemcpyHostToDevice,
-                            c.stream));
+    HiPrio hp(c);
+    h2d(c, kr.L.p, u, sizeof(double) * (size_t)n * ndefl);
     double* G = dev_alloc<double>((size_t)ndefl * ndefl);
     const double one = 1.0, zero = 0.0;
     cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, ndefl, ndefl, n, &one, kr.L.p, n, kr.L.p, n,
                 &zero, G, ndefl);
     ++c.launches;
     Vec g((size_t)ndefl * ndefl);
-    SE_CUDA(cudaMemcpyAsync(g.data(), G, sizeof(double) * g.size(), cudaMemcpyDeviceToHost, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, g.data(), G, sizeof(double) * g.size());
+    ctx_sync(c);
     dev_free(G);
     for (int j = 0; j < ndefl; ++j)
       for (int i = 0; i <= j; ++i)
@@ -484,15 +483,15 @@ struct Slice {
       SE_CUDA(cudaMemcpyAsync(r->vectors.col(q), kr.L.col(src), sizeof(double) * A.n,
                               cudaMemcpyDeviceToDevice, c.stream));
     }
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     add_timers();
     cnt.t_total += now_s() - t0;
     if (std::getenv("SE_PROFILE"))
       std::fprintf(stderr,
                    "[se] n=%d its=%ld total %.3f mv %.3f orth %.3f check %.3f eig %.3f cand %.3f "
-                   "passes %lld\n",
+                   "passes %lld check_kernel_ms %.1f\n",
                    A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
-                   kr.get().passes_total);
+                   kr.get().passes_total, c.prof_kernel_ms);
     r->niter = its;
     r->hit_max_its = warn;
     r->counters = cnt;
@@ -501,12 +500,15 @@ struct Slice {
 
   // Candidate rows ylast for thick restart: Y[steps-1, j] for the candidate columns.
   Vec last_row(const double* Y, int steps, int j0, int nc) {
+    HiPrio hp(c);
     Vec out(nc);
     if (nc == 0) return out;
-    SE_CUDA(cudaMemcpy2DAsync(out.data(), sizeof(double), Y + (size_t)j0 * steps + (steps - 1),
+    double* p = static_cast<double*>(staging(c, sizeof(double) * nc));
+    SE_CUDA(cudaMemcpy2DAsync(p, sizeof(double), Y + (size_t)j0 * steps + (steps - 1),
                               sizeof(double) * steps, sizeof(double), nc, cudaMemcpyDeviceToHost,
                               c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
+    std::copy(p, p + nc, out.data());
     return out;
   }
 };
@@ -795,7 +797,7 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
         nxt = old;
       }
     }
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
   } catch (...) {
     for (double* b : fb) dev_free(b);
     throw;
@@ -810,7 +812,7 @@ LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m,
   StepOp op;  // plain A
   Krylov kr(c, a, op);
   kr.ensure(m + 1, 0);
-  SE_CUDA(cudaMemcpyAsync(kr.W.col(0), start_host, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+  h2d(c, kr.W.col(0), start_host, sizeof(double) * n);
   const double nb2 = kr.dot(kr.W.col(0), kr.W.col(0));
   if (nb2 <= 0.0) fail(SE_ENUMERIC, "lanczos_run: B-inner product is not positive");
   k::scale(c, n, 1.0 / std::sqrt(nb2), kr.W.col(0));
@@ -856,8 +858,7 @@ void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max
       if (k0 == 0) {
         Vec w(n);
         rng.normal_fill(w.data(), n);
-        SE_CUDA(cudaMemcpyAsync(kr.W.col(0), w.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
-                                c.stream));
+        h2d(c, kr.W.col(0), w.data(), sizeof(double) * n);
         const double nb = std::sqrt(kr.dot(kr.W.col(0), kr.W.col(0)));
         k::scale(c, n, 1.0 / nb, kr.W.col(0));
       }
@@ -899,9 +900,8 @@ void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max
       kept_theta = {vals[0], vals[steps - 1]};
       kept_s = {trailing * vecs[(size_t)0 * steps + steps - 1],
                 trailing * vecs[(size_t)(steps - 1) * steps + steps - 1]};
-      SE_CUDA(cudaMemcpyAsync(dY, vecs.data(), sizeof(double) * steps, cudaMemcpyHostToDevice, c.stream));
-      SE_CUDA(cudaMemcpyAsync(dY + steps, vecs.data() + (size_t)(steps - 1) * steps,
-                              sizeof(double) * steps, cudaMemcpyHostToDevice, c.stream));
+      h2d(c, dY, vecs.data(), sizeof(double) * steps);
+      h2d(c, dY + steps, vecs.data() + (size_t)(steps - 1) * steps, sizeof(double) * steps);
       Vec st;
       cand.eval(a, kr.W.p, steps, dY, steps, 2, st);
       // seed first (column steps -> 2), then the kept combinations into columns 0, 1
@@ -945,8 +945,8 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     std::vector<double> h(n);
     Rng rng(99);
     rng.normal_fill(h.data(), n);
-    SE_CUDA(cudaMemcpyAsync(v, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    h2d(c, v, h.data(), sizeof(double) * n);
+    ctx_sync(c);
     const long before = c.launches;
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     k::ChebArgs a1;
@@ -1007,7 +1007,7 @@ void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) {
   Ctl* ctl = dev_alloc<Ctl>(1);
   k::Scratch s;
   s.cap = k::cgs_scratch_doubles(c, n, kcols);
-  s.ncnt = k::cgs_counter_slots(kcols);
+  s.ncnt = k::cgs_counter_slots(n, kcols);
   s.buf = dev_alloc<double>(s.cap);
   s.cnt = dev_alloc<unsigned>(s.ncnt);
   cudaGraphExec_t ge = nullptr;
@@ -1022,13 +1022,13 @@ void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) {
     Rng rng(7);
     rng.normal_fill(h.data(), n);
     for (int j = 0; j < kcols; ++j)
-      SE_CUDA(cudaMemcpyAsync(W + (size_t)j * n, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
-    SE_CUDA(cudaMemcpyAsync(t, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      h2d(c, W + (size_t)j * n, h.data(), sizeof(double) * n);
+    h2d(c, t, h.data(), sizeof(double) * n);
     Ctl z{};
     z.i = kcols - 1;
     z.before = 1.0;
-    SE_CUDA(cudaMemcpyAsync(ctl, &z, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
-    SE_CUDA(cudaStreamSynchronize(c.stream));
+    h2d(c, ctl, &z, sizeof(Ctl));
+    ctx_sync(c);
     const long before = c.launches;
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     k::cgs_pass(c, s, n, t, W, false, false, ctl, nullptr, coef, kcols);

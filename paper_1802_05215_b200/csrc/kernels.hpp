@@ -74,7 +74,7 @@ struct Scratch {
 };
 // Doubles of scratch a CGS pass over up to `cap_cols` columns of an n-row basis needs.
 size_t cgs_scratch_doubles(const Ctx& c, int n, int cap_cols);
-int cgs_counter_slots(int cap_cols);
+int cgs_counter_slots(int n, int cap_cols);
 
 // ||t|| -> ctl->before/after; resets the DGKS flags.
 void norm_before(Ctx& c, const Scratch& s, int n, const double* t, Ctl* ctl);

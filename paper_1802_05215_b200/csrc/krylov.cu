@@ -19,7 +19,7 @@ constexpr double kDgksEta = 0.70710678118654752;  // orth.hpp:13
 constexpr int kThreads = 256;
 constexpr int kCW = 32;        // columns per GEMV-T work item
 constexpr int kMaxRch = 4096;  // rows per GEMV-T work item (t chunk in shared memory)
-constexpr int kCoefChunk = 4096;
+constexpr int kNW = 256;  // columns per GEMV-N chunk
 
 // Counter slot layout inside Ctx::counters.
 constexpr int kSlotNorm = 0;
@@ -158,104 +158,131 @@ __global__ void __launch_bounds__(kThreads) k_gemvt(int n, int rch, const double
                                                     const double* __restrict__ t, Ctl* ctl, int mode,
                                                     int pass2, int fixed, double* partial, int ldp,
                                                     unsigned* grp_cnt, double* coef, double* hdiag) {
+  // One work item per CTA (short-lived CTAs keep SM slots turning over, so the latency-bound
+  // kernels of other slices sharing the GPU are scheduled promptly).  Items beyond the current
+  // column count exit at once.
   if (ctl && pass_skip(ctl, pass2)) return;
   const int ncols = pass_ncols(ctl, mode, fixed);
-  if (ncols <= 0) return;
   const int nrb = (n + rch - 1) / rch;
-  const int ngrp = (ncols + kCW - 1) / kCW;
-  const int items = nrb * ngrp;
+  const int g = blockIdx.x / nrb, rb = blockIdx.x - g * nrb;
+  if (ncols <= 0 || g * kCW >= ncols) return;
   const int hcol = (hdiag && ctl) ? ctl->i : -1;
   __shared__ double s_t[kMaxRch];
   __shared__ bool s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    const int g = it / nrb, rb = it - g * nrb;
-    const int r0 = rb * rch, rn = min(rch, n - r0);
-    __syncthreads();
-    for (int q = threadIdx.x; q < rch; q += kThreads) s_t[q] = q < rn ? t[r0 + q] : 0.0;
-    __syncthreads();
-    for (int jj = warp; jj < kCW; jj += kThreads / 32) {
-      const int j = g * kCW + jj;
-      if (j >= ncols) break;
-      const double* __restrict__ qc = Q + (size_t)j * n + r0;
-      double acc = 0.0;
-      int q = lane;
-      for (; q + 7 * 32 < rn; q += 8 * 32) {
-        double w[8];
+  const int r0 = rb * rch, rn = min(rch, n - r0);
+  for (int q = threadIdx.x; q < rch; q += kThreads) s_t[q] = q < rn ? t[r0 + q] : 0.0;
+  __syncthreads();
+  for (int jj = warp; jj < kCW; jj += kThreads / 32) {
+    const int j = g * kCW + jj;
+    if (j >= ncols) break;
+    const double* __restrict__ qc = Q + (size_t)j * n + r0;
+    double acc = 0.0;
+    int q = lane;
+    for (; q + 7 * 32 < rn; q += 8 * 32) {
+      double w[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) w[u] = __ldcs(qc + q + 32 * u);
+      for (int u = 0; u < 8; ++u) w[u] = __ldcs(qc + q + 32 * u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = add(acc, mul(w[u], s_t[q + 32 * u]));
-      }
-      for (; q < rn; q += 32) acc = add(acc, mul(__ldcs(qc + q), s_t[q]));
-      acc = warp_sum(acc);
-      if (lane == 0) partial[(size_t)rb * ldp + j] = acc;
+      for (int u = 0; u < 8; ++u) acc = add(acc, mul(w[u], s_t[q + 32 * u]));
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&grp_cnt[g], 1u) == (unsigned)(nrb - 1);
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      // 8 threads per column, strided over row chunks, shuffle-combined in fixed order.
-      const int jj = threadIdx.x >> 3, sub8 = threadIdx.x & 7;
-      const int j = g * kCW + jj;
-      double q = 0.0;
-      if (j < ncols)
-        for (int b = sub8; b < nrb; b += 8) q = add(q, __ldcg(partial + (size_t)b * ldp + j));
-      for (int o = 4; o > 0; o >>= 1) q = add(q, __shfl_down_sync(0xffffffffu, q, o, 8));
-      if (sub8 == 0 && j < ncols) {
-        coef[j] = q;
-        if (j == hcol) hdiag[j] = add(hdiag[j], q);  // h[j] += c_j (orth.hpp:30), H(i,i) += h[i]
-      }
-      if (threadIdx.x == 0) grp_cnt[g] = 0u;
-    }
+    for (; q < rn; q += 32) acc = add(acc, mul(__ldcs(qc + q), s_t[q]));
+    acc = warp_sum(acc);
+    if (lane == 0) partial[(size_t)rb * ldp + j] = acc;
   }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&grp_cnt[g], 1u) == (unsigned)(nrb - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // 8 threads per column, strided over row chunks, shuffle-combined in fixed order.
+  const int jj = threadIdx.x >> 3, sub8 = threadIdx.x & 7;
+  const int j = g * kCW + jj;
+  double q = 0.0;
+  if (j < ncols)
+    for (int b = sub8; b < nrb; b += 8) q = add(q, __ldcg(partial + (size_t)b * ldp + j));
+  for (int o = 4; o > 0; o >>= 1) q = add(q, __shfl_down_sync(0xffffffffu, q, o, 8));
+  if (sub8 == 0 && j < ncols) {
+    coef[j] = q;
+    if (j == hcol) hdiag[j] = add(hdiag[j], q);  // h[j] += c_j (orth.hpp:30), H(i,i) += h[i]
+  }
+  if (threadIdx.x == 0) grp_cnt[g] = 0u;
 }
 
 // ---- CGS pass, part 2: t -= Q coef (orth.hpp:26-29) + ||t|| + DGKS decision (orth.hpp:76-78).
-// One thread per row; columns in reference order (t = t - c_j q_j, j ascending), 16 loads in
-// flight per thread.  mode 0: Krylov basis (norm + flags); 1: locked set (no norm); 2: plain.
+// CTA (row block of 256 rows, chunk of kNW columns): each thread sums its row over the chunk
+// (column order, 16 loads in flight) into P[chunk][row]; the last chunk CTA of a row block
+// subtracts the chunk partials in chunk order and adds the block's ||t||^2; the last row block
+// finishes the norm and the re-pass decision.  mode 0: Krylov basis (norm + flags); 1: locked
+// set; 2: plain (no norm).
 __global__ void __launch_bounds__(kThreads) k_gemvn(int n, const double* __restrict__ Q,
                                                     double* __restrict__ t, Ctl* ctl, int mode,
                                                     int pass2, int fixed,
                                                     const double* __restrict__ coef,
-                                                    double* partial, unsigned* cnt) {
+                                                    double* __restrict__ P, unsigned* rb_cnt,
+                                                    double* npart, unsigned* gcnt) {
   if (ctl && pass_skip(ctl, pass2)) return;
   const int ncols = pass_ncols(ctl, mode, fixed);
-  if (ncols <= 0) return;
-  __shared__ double s_c[kCoefChunk];
-  const int r = blockIdx.x * kThreads + threadIdx.x;
+  const int nchunks = (ncols + kNW - 1) / kNW;
+  const int rb = blockIdx.x, cc = blockIdx.y;
+  if (ncols <= 0 || cc >= nchunks) return;
+  __shared__ double s_c[kNW];
+  __shared__ bool s_last;
+  const int j0 = cc * kNW, jn = min(kNW, ncols - j0);
+  for (int q = threadIdx.x; q < jn; q += kThreads) s_c[q] = coef[j0 + q];
+  __syncthreads();
+  const int r = rb * kThreads + threadIdx.x;
   const bool live = r < n;
-  double tr = live ? t[r] : 0.0;
-  for (int j0 = 0; j0 < ncols; j0 += kCoefChunk) {
-    const int jn = min(kCoefChunk, ncols - j0);
-    __syncthreads();
-    for (int q = threadIdx.x; q < jn; q += kThreads) s_c[q] = coef[j0 + q];
-    __syncthreads();
-    if (live) {
-      const double* __restrict__ qr = Q + (size_t)j0 * n + r;
-      int j = 0;
-      for (; j + 16 <= jn; j += 16) {
-        double w[16];
+  if (live) {
+    const double* __restrict__ qr = Q + (size_t)j0 * n + r;
+    double p = 0.0;
+    int j = 0;
+    for (; j + 16 <= jn; j += 16) {
+      double w[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) w[u] = __ldcs(qr + (size_t)(j + u) * n);
+      for (int u = 0; u < 16; ++u) w[u] = __ldcs(qr + (size_t)(j + u) * n);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) tr = sub(tr, mul(s_c[j + u], w[u]));
-      }
-      for (; j < jn; ++j) tr = sub(tr, mul(s_c[j], __ldcs(qr + (size_t)j * n)));
+      for (int u = 0; u < 16; ++u) p = add(p, mul(s_c[j + u], w[u]));
     }
+    for (; j < jn; ++j) p = add(p, mul(s_c[j], __ldcs(qr + (size_t)j * n)));
+    P[(size_t)cc * n + r] = p;
   }
-  if (live) t[r] = tr;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&rb_cnt[rb], 1u) == (unsigned)(nchunks - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double tr = 0.0;
+  if (live) {
+    tr = t[r];
+    for (int q = 0; q < nchunks; ++q) tr = sub(tr, __ldcg(P + (size_t)q * n + r));
+    t[r] = tr;
+  }
+  if (threadIdx.x == 0) rb_cnt[rb] = 0u;
   if (mode != 0) return;
-  double tot;
-  if (grid_sum(tr * tr, partial, cnt, &tot) && threadIdx.x == 0) {
-    const double after = sqrt(tot);
+  // this row block's ||t||^2, then the last row block reduces all of them in order
+  __shared__ bool s_glast;
+  const double bs = block_sum(tr * tr);
+  if (threadIdx.x == 0) npart[rb] = bs;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_glast = atomicAdd(gcnt, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_glast) return;
+  __threadfence();
+  double q = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) q = add(q, __ldcg(npart + b));
+  q = block_sum(q);
+  if (threadIdx.x == 0) {
+    const double after = sqrt(q);
     ctl->npass += 1;
     ctl->passes_total += 1;
     if (!pass2) ctl->repass = after > kDgksEta * ctl->before ? 0 : 1;
     ctl->before = after;
     ctl->after = after;
+    *gcnt = 0u;
   }
 }
 
@@ -362,14 +389,19 @@ int rch_for(int n) { return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512
 
 }  // namespace
 
+// Scratch layout of a CGS pass: [GEMV-T partials nrb x cap][GEMV-N chunk partials nchunks x n]
+// [row-block norms]; counters: [group counters][row-block counters].
 size_t cgs_scratch_doubles(const Ctx& c, int n, int cap_cols) {
   const int rch = rch_for(n);
   const size_t nrb = (size_t)(n + rch - 1) / rch;
   const size_t gn = (size_t)(n + kThreads - 1) / kThreads;
-  return nrb * (size_t)std::max(cap_cols, 1) + gn + (size_t)c.num_sms * 8 + 64;
+  const size_t ncc = (size_t)(std::max(cap_cols, 1) + kNW - 1) / kNW;
+  return nrb * (size_t)std::max(cap_cols, 1) + ncc * (size_t)n + gn + (size_t)c.num_sms * 8 + 64;
 }
 
-int cgs_counter_slots(int cap_cols) { return kSlotGroups + (std::max(cap_cols, 1) + kCW - 1) / kCW; }
+int cgs_counter_slots(int n, int cap_cols) {
+  return kSlotGroups + (std::max(cap_cols, 1) + kCW - 1) / kCW + (n + kThreads - 1) / kThreads + 8;
+}
 
 static void need(const Scratch& s, size_t doubles, int slots) {
   if (doubles > s.cap || slots > s.ncnt) fail(SE_EINVAL, "internal: scratch too small");
@@ -409,16 +441,17 @@ static void cgs_impl(Ctx& c, const Scratch& s, int n, double* t, const double* Q
   const int nrb = (n + rch - 1) / rch;
   const int ngrp_max = (ldp + kCW - 1) / kCW;
   const int gn = (n + kThreads - 1) / kThreads;
-  need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(ldp));
+  need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
+  const int ncc = (ldp + kNW - 1) / kNW;
   double* part = s.buf;
-  double* npart = part + (size_t)nrb * ldp;
-  const int items_max = nrb * ngrp_max;
-  const int gt = std::max(1, std::min(items_max, c.num_sms * 6));
-  k_gemvt<<<gt, kThreads, 0, c.stream>>>(n, rch, Q, t, ctl, mode, pass2 ? 1 : 0, fixed, part, ldp,
-                                         s.cnt + kSlotGroups, coef, hdiag);
+  double* P = part + (size_t)nrb * ldp;
+  double* npart = P + (size_t)ncc * n;
+  k_gemvt<<<nrb * ngrp_max, kThreads, 0, c.stream>>>(n, rch, Q, t, ctl, mode, pass2 ? 1 : 0, fixed,
+                                                     part, ldp, s.cnt + kSlotGroups, coef, hdiag);
   ++c.launches;
-  k_gemvn<<<gn, kThreads, 0, c.stream>>>(n, Q, t, ctl, mode, pass2 ? 1 : 0, fixed, coef, npart,
-                                         s.cnt + kSlotMisc);
+  k_gemvn<<<dim3(gn, ncc), kThreads, 0, c.stream>>>(n, Q, t, ctl, mode, pass2 ? 1 : 0, fixed, coef, P,
+                                                    s.cnt + kSlotGroups + ngrp_max, npart,
+                                                    s.cnt + kSlotMisc);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }

@@ -399,11 +399,11 @@ void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
   SE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, a.rp, a.rp, n + 1, c.stream));
   void* tmp = dev_alloc<char>(tmp_bytes);
   SE_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, a.rp, a.rp, n + 1, c.stream));
-  SE_CUDA(cudaStreamSynchronize(c.stream));
+  ctx_sync(c);
   dev_free(tmp);
   int nnz = 0;
   SE_CUDA(cudaMemcpyAsync(&nnz, a.rp + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SE_CUDA(cudaStreamSynchronize(c.stream));
+  ctx_sync(c);
   a.nnz = nnz;
   a.ci = dev_alloc<int>(nnz);
   a.v = dev_alloc<double>(nnz);
@@ -428,7 +428,7 @@ int csr_max_row_nnz(Ctx& c, const DevCsr& a) {
   ++c.launches;
   int h = 0;
   SE_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SE_CUDA(cudaStreamSynchronize(c.stream));
+  ctx_sync(c);
   dev_free(d);
   return h;
 }

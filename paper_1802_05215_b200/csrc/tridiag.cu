@@ -12,9 +12,25 @@ namespace k {
 
 namespace {
 
+__device__ __forceinline__ int sturm_count(int m, const double* __restrict__ d,
+                                           const double* __restrict__ e, double x, double piv) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < piv) q = -piv;
+  cnt += q < 0.0;
+  for (int i = 1; i < m; ++i) {
+    q = (d[i] - x) - (e[i - 1] * e[i - 1]) / q;
+    if (fabs(q) < piv) q = -piv;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// One warp per wanted eigenvalue (ascending index idx = nbelow + warp): 32-point multisection,
+// each lane evaluating one Sturm count, so the bracket shrinks 33x per round (~10 rounds to
+// machine precision instead of ~55 bisection steps).
 __global__ void k_tridiag_above(int m, const double* __restrict__ d, const double* __restrict__ e,
-                                double bar, double* __restrict__ vals,
-                                int* __restrict__ count) {
+                                double bar, double* __restrict__ vals, int* __restrict__ count) {
   __shared__ double s_lo, s_hi, s_piv;
   __shared__ int s_below;
   if (threadIdx.x == 0) {
@@ -29,46 +45,30 @@ __global__ void k_tridiag_above(int m, const double* __restrict__ d, const doubl
     const double pad = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + s_piv;
     s_lo = lo - pad;
     s_hi = hi + pad;
+    s_below = sturm_count(m, d, e, bar, s_piv);
+    if (blockIdx.x == 0) *count = m - s_below;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // count of eigenvalues < bar, with e^2 formed on the fly
-    int cnt = 0;
-    double q = d[0] - bar;
-    if (fabs(q) < s_piv) q = -s_piv;
-    cnt += q < 0.0;
-    for (int i = 1; i < m; ++i) {
-      q = (d[i] - bar) - (e[i - 1] * e[i - 1]) / q;
-      if (fabs(q) < s_piv) q = -s_piv;
-      cnt += q < 0.0;
-    }
-    s_below = cnt;
-    if (blockIdx.x == 0) *count = m - cnt;
-  }
-  __syncthreads();
-  const int idx = s_below + blockIdx.x * blockDim.x + threadIdx.x;  // ascending index
+  const int lane = threadIdx.x & 31;
+  const int idx = s_below + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (idx >= m) return;
+  const double piv = s_piv;
   double a = fmax(bar, s_lo), b = s_hi;
   if (a > b) a = b;
-  const double piv = s_piv;
-  for (int it = 0; it < 200; ++it) {
-    const double mid = 0.5 * (a + b);
-    if (mid <= a || mid >= b || (b - a) <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b))) break;
-    int cnt = 0;
-    double q = d[0] - mid;
-    if (fabs(q) < piv) q = -piv;
-    cnt += q < 0.0;
-    for (int i = 1; i < m; ++i) {
-      q = (d[i] - mid) - (e[i - 1] * e[i - 1]) / q;
-      if (fabs(q) < piv) q = -piv;
-      cnt += q < 0.0;
-    }
-    if (cnt <= idx)
-      a = mid;
-    else
-      b = mid;
+  for (int round = 0; round < 40; ++round) {
+    if ((b - a) <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b)) + piv) break;
+    const double x = a + (b - a) * (double)(lane + 1) / 33.0;
+    const int c = sturm_count(m, d, e, x, piv);
+    // points with count <= idx lie left of the wanted eigenvalue
+    const unsigned left = __ballot_sync(0xffffffffu, c <= idx);
+    const int nl = __popc(left);  // points 0..nl-1 are left (counts are monotone in x)
+    const double na = nl > 0 ? __shfl_sync(0xffffffffu, x, nl - 1) : a;
+    const double nb = nl < 32 ? __shfl_sync(0xffffffffu, x, nl < 32 ? nl : 31) : b;
+    if (!(na >= a && nb <= b) || na == a && nb == b) break;
+    a = na;
+    b = nb;
   }
-  vals[idx - s_below] = 0.5 * (a + b);
+  if (lane == 0) vals[idx - s_below] = 0.5 * (a + b);
 }
 
 }  // namespace
@@ -83,20 +83,25 @@ void tridiag_eigs_above(Ctx& c, int m, const double* d_host, const double* e_hos
   double* e = work + m;
   double* vals = work + 3 * m;
   int* cnt = reinterpret_cast<int*>(work + 4 * m);
-  SE_CUDA(cudaMemcpyAsync(d, d_host, sizeof(double) * m, cudaMemcpyHostToDevice, c.stream));
+  h2d(c, d, d_host, sizeof(double) * m);
   if (m > 1)
-    SE_CUDA(cudaMemcpyAsync(e, e_host, sizeof(double) * (m - 1), cudaMemcpyHostToDevice, c.stream));
-  const int tb = 64;
-  k_tridiag_above<<<(m + tb - 1) / tb, tb, 0, c.stream>>>(m, d, e, bar, vals, cnt);
+    h2d(c, e, e_host, sizeof(double) * (m - 1));
+  const int tb = 128;  // 4 eigenvalues (warps) per CTA
+  SE_CUDA(cudaEventRecord(c.evk0, c.stream));
+  k_tridiag_above<<<(m + 3) / 4, tb, 0, c.stream>>>(m, d, e, bar, vals, cnt);
+  SE_CUDA(cudaEventRecord(c.evk1, c.stream));
   ++c.launches;
   SE_CUDA(cudaGetLastError());
   int h = 0;
-  SE_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SE_CUDA(cudaStreamSynchronize(c.stream));
+  d2h(c, &h, cnt, sizeof(int));
+  ctx_sync(c);
+  float kms = 0.f;
+  SE_CUDA(cudaEventElapsedTime(&kms, c.evk0, c.evk1));
+  c.prof_kernel_ms += kms;
   out.resize(h);
   if (h)
-    SE_CUDA(cudaMemcpyAsync(out.data(), vals, sizeof(double) * h, cudaMemcpyDeviceToHost, c.stream));
-  SE_CUDA(cudaStreamSynchronize(c.stream));
+    d2h(c, out.data(), vals, sizeof(double) * h);
+  ctx_sync(c);
 }
 
 }  // namespace k

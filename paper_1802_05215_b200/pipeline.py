@@ -62,6 +62,7 @@ class SliceOutcome:
     n_A_matvec: int = 0
     hit_max_its: bool = False
     seconds: float = 0.0
+    t_start: float = 0.0  # relative to the start of the solve stage
     t_mv: float = 0.0
     t_orth: float = 0.0
     error: Optional[str] = None
@@ -267,6 +268,7 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
     def work(i):
         out = SliceOutcome(i, float(bp[i]), float(bp[i + 1]), float(est[i]), rank=dist.rank)
         ts = time.perf_counter()
+        out.t_start = ts - t2
         try:
             k, r = backend.solve_slice(plan, lmin, lmax, out.lo, out.hi, out.est)
             keep = trim_to_slice(r.eigenvalues, r.residuals, i, ns, out.lo, out.hi, delta)

@@ -41,5 +41,5 @@ for rep in range(a.repeat):
             cand = np.stack([ev[np.clip(idx-1,0,ev.size-1)], ev[np.clip(idx,0,ev.size-1)]])
             maxerr = float(np.min(np.abs(cand - s.eigenvalues), axis=0).max() / max(1e-300, np.abs(s.eigenvalues).max()))
         print(f"  slice {s.index} [{lo:.8f},{hi:.8f}] est {s.est:.1f} deg {s.degree} found {s.eigenvalues.size} truth {truth} "
-              f"niter {s.niter} nmv {s.n_A_matvec} {s.seconds:.2f}s (mv {s.t_mv:.2f} orth {s.t_orth:.2f}) maxrelerr {maxerr:.2e} maxres {s.residuals.max() if s.residuals.size else 0:.1e} err={s.error}")
+              f"niter {s.niter} nmv {s.n_A_matvec} {s.seconds:.2f}s (start {s.t_start:.2f} mv {s.t_mv:.2f} orth {s.t_orth:.2f}) maxrelerr {maxerr:.2e} maxres {s.residuals.max() if s.residuals.size else 0:.1e} err={s.error}")
 print("launches", be.launches())
