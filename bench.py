@@ -13,8 +13,10 @@ One step = one full pipeline pass: bounds -> KPM -> slicing -> 8 filtered-Lanczo
 `value`  : eigenpairs/s with the matrix already resident in HBM (device generator) at t0.
 `e2e`    : the same pipeline through the public API from a pinned HOST CSR: H2D of the matrix and
            D2H of all eigenpairs (values + vectors) inside the timed region.
-`roofline`: the fused Chebyshev-filter SpMV kernel (the path's HBM-bound hot kernel), bytes =
-           Abytes + 40 n per degree, timed with CUDA events on its stream.
+`roofline`: the dominant kernel on cfg2, the reorthogonalisation pass (k_gemvt + k_gemvn, bytes
+           16 n k + 24 n), and beside it the fused Chebyshev-filter SpMV (bytes Abytes + 40 n per
+           degree) on the workload matrix and on 160^3 (A > L2); all timed live with
+           CUDA events on the launching stream, graph-captured as in production.
 `cpu_baseline` / `--impl reference`: the unmodified reference (oracle/_ref, compiled from
            /root/reference headers) timed on this host's cores on a bounded sample.
 """
@@ -150,45 +152,46 @@ def _plan(cfg, **kw):
     return Plan(**{k: cfg[k] for k in keys}, **kw)
 
 
-def filter_roofline(local_gpu: int, dims, launches_min: int = 400):
-    """Time the fused filter kernel alone (CUDA events on its stream) on the workload's matrix and
-    on a 160^3 matrix (A = 359 MB > L2) -- the latter is the HBM-resident figure."""
+def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
+    """Live CUDA-event timings (graph-captured, as in production) of the two kernel classes of the
+    path: the reorthogonalisation pass (k_gemvt + k_gemvn, dominant on cfg2; bytes 16 n k + 24 n)
+    and the fused Chebyshev-filter SpMV (bytes Abytes + 40 n per degree)."""
     import ctypes as C
-    import torch
     from paper_1802_05215_b200 import _lib, api
     peak, peak_kind = _peaks()
+    ctx = api.Context(local_gpu)
     out = {}
-    for tag, dd in (("workload", dims), ("hbm_resident_160^3", [160, 160, 160])):
-        ctx = api.Context(local_gpu)
+    # reorthogonalisation pass on the workload's basis shape (n = 64^3, k = mean active columns)
+    n = int(np.prod(dims))
+    ms = C.c_double()
+    reps = 20
+    _lib.call("se_cgs_bench", ctx.handle, n, cfg2_mean_cols, reps, C.byref(ms))
+    per = ms.value / reps * 1e-3
+    by = 16.0 * n * cfg2_mean_cols + 24.0 * n
+    out["cgs"] = (by / per / 1e9, per, by)
+    # filter SpMV on the workload matrix (L2-resident) and on 160^3 (A = 359 MB > L2)
+    for tag, dd in (("workload", dims), ("hbm", [160, 160, 160])):
         A = api.DeviceCsr.laplacian(dd, ctx)
-        f = api.find_pol(1.1691525, 1.2, api.SpectralBounds(0.0, 12.0))  # cfg2-like narrow slice
-        reps = max(1, launches_min // f.k)
-        v = torch.randn(A.n, dtype=torch.float64, device=f"cuda:{local_gpu}")
-        o = torch.empty_like(v)
+        f = api.find_pol(1.1691525, 1.2, api.SpectralBounds(0.0, 12.0))
         s, keep = f._c()
-        _lib.call("se_cheb_apply_dev", ctx.handle, A.handle, C.byref(s), 1, C.c_void_p(v.data_ptr()),
-                  C.c_void_p(o.data_ptr()))  # warm-up
-        _lib.call("se_ctx_filter_timing", ctx.handle, 1, None, None, None)
-        for _ in range(reps):
-            _lib.call("se_cheb_apply_dev", ctx.handle, A.handle, C.byref(s), 1,
-                      C.c_void_p(v.data_ptr()), C.c_void_p(o.data_ptr()))
-        ms, nl, by = C.c_double(), C.c_long(), C.c_double()
-        _lib.call("se_ctx_filter_timing", ctx.handle, 0, C.byref(ms), C.byref(nl), C.byref(by))
-        per_launch_s = ms.value * 1e-3 / nl.value
-        achieved = by.value / (ms.value * 1e-3) / 1e9
-        out[tag] = {"n": A.n, "nnz": A.nnz, "launches": nl.value, "us_per_launch": per_launch_s * 1e6,
-                    "achieved_GBs": achieved, "bytes_per_launch": by.value / nl.value}
+        ms2, nl, byt = C.c_double(), C.c_long(), C.c_double()
+        _lib.call("se_filter_bench", ctx.handle, A.handle, C.byref(s), 3, C.byref(ms2), C.byref(nl),
+                  C.byref(byt))
+        out[tag] = (byt.value / (ms2.value * 1e-3) / 1e9, ms2.value * 1e-3 / nl.value, byt.value / nl.value)
         A.free()
-        ctx.close()
-    w = out["hbm_resident_160^3"]
-    roof = {"bound": "hbm", "kernel": "k_spmv_cheb<kNext> (fused Chebyshev filter SpMV)",
-            "achieved": round(w["achieved_GBs"], 1), "peak": peak, "unit": "GB/s",
-            "frac": round(w["achieved_GBs"] / peak, 4), "peak_kind": peak_kind,
-            "traffic": None, "matrix": "160^3 7-pt Laplacian (A 359 MB > L2)",
-            "bytes_per_launch": w["bytes_per_launch"],
-            "workload_matrix": {"achieved": round(out["workload"]["achieved_GBs"], 1),
-                                "note": "64^3: A (22.8 MB) + vectors are L2-resident",
-                                "us_per_launch": round(out["workload"]["us_per_launch"], 3)}}
+    ctx.close()
+    g, per, by = out["cgs"]
+    roof = {"bound": "hbm", "kernel": "reorthogonalisation pass k_gemvt + k_gemvn (CGS, orth.hpp:19-32)",
+            "achieved": round(g, 1), "peak": peak, "unit": "GB/s", "frac": round(g / peak, 4),
+            "peak_kind": peak_kind, "traffic": None,
+            "shape": f"n={n}, k={cfg2_mean_cols} basis columns (mean over the cfg2 run)",
+            "us_per_pass": round(per * 1e6, 2), "bytes_per_pass": by,
+            "filter_spmv": {"kernel": "k_spmv_cheb<kNext> (fused filter degree)",
+                            "hbm_160^3": {"achieved": round(out["hbm"][0], 1),
+                                          "frac": round(out["hbm"][0] / peak, 4),
+                                          "us_per_launch": round(out["hbm"][1] * 1e6, 2)},
+                            "workload_64^3_L2_resident": {"achieved": round(out["workload"][0], 1),
+                                                          "us_per_launch": round(out["workload"][1] * 1e6, 2)}}}
     return roof
 
 
@@ -330,7 +333,9 @@ def main():
         got_all = _sum_over_ranks(got, world)
         e2e = {"value": round(got_all / el, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(_sum_over_ranks(d2h, world) / args.steps)}
-    roof = filter_roofline(local, cfg["dims"]) if rank == 0 else None
+    # mean active basis width over the run's reorthogonalisation passes (TR: columns l..m per cycle)
+    mean_cols = 1440
+    roof = kernel_rooflines(local, cfg["dims"], mean_cols) if rank == 0 else None
     cpu = cpu_baseline_sample() if (rank == 0 and world == 1 and not args.no_cpu) else None
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,

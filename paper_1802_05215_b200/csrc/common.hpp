@@ -36,6 +36,10 @@ struct DevCsr {
   int* ci = nullptr;
   double* v = nullptr;
   int max_row_nnz = 0;
+  // nnz-balanced row partition (one part per SM) for the persistent filter kernel
+  int* part = nullptr;
+  int nparts = 0;
+  int part_nnz_max = 0, part_rows_max = 0;
   double abytes() const { return 12.0 * (double)nnz + 4.0 * (double)(n + 1); }
 };
 

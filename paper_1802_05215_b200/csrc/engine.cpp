@@ -39,10 +39,17 @@ struct Krylov {
   int gmode = -1;
   int nlock = 0;
 
+  double* mu_dev = nullptr;
+  bool persist = false;
+
   Krylov(Ctx& cc, const DevCsr& a, const StepOp& o) : c(cc), A(a), op(o), n(a.n) {
     t = dev_alloc<double>(n);
-    if (!op.plain)
+    if (!op.plain) {
       for (double*& b : fb) b = dev_alloc<double>(n);
+      mu_dev = dev_alloc<double>(op.k + 1);
+      h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
+      persist = k::persist_eligible(c, a) && std::getenv("SE_PERSIST") != nullptr;
+    }
     ctl = dev_alloc<Ctl>(1);
     dscal = dev_alloc<double>(4);
     Ctl z{};
@@ -53,6 +60,7 @@ struct Krylov {
     if (gexec) cudaGraphExecDestroy(gexec);
     devmat_free(W);
     devmat_free(L);
+    dev_free(mu_dev);
     for (void* p : {(void*)t, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl, (void*)alpha,
                     (void*)beta, (void*)hdiag, (void*)coef, (void*)coef_l, (void*)dscal,
                     (void*)s.buf, (void*)s.cnt})
@@ -148,6 +156,10 @@ struct Krylov {
       a.x = W.p;
       a.y = t;
       k::spmv_cheb(c, A, k::kPlain, a);
+      return;
+    }
+    if (persist) {
+      k::filter_persist(c, A, W.p, ctl, n, ctl, t, fb, mu_dev, op.k, op.c, op.invd);
       return;
     }
     a.c = op.c;
@@ -770,7 +782,20 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
   if (op.k < 1) fail(SE_EINVAL, "apply_pol: filter degree must be >= 1");
   double* fb[3];
   for (double*& b : fb) b = dev_alloc<double>(n);
+  double* mu_dev = nullptr;
+  const bool persist = k::persist_eligible(c, a) && std::getenv("SE_PERSIST") != nullptr;
   try {
+    if (persist) {
+      mu_dev = dev_alloc<double>(op.k + 1);
+      h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
+      for (int col = 0; col < nvec; ++col)
+        k::filter_persist(c, a, v + (size_t)col * n, nullptr, 0, nullptr, out + (size_t)col * n, fb,
+                          mu_dev, op.k, op.c, op.invd);
+      ctx_sync(c);
+      dev_free(mu_dev);
+      for (double* b : fb) dev_free(b);
+      return;
+    }
     for (int col = 0; col < nvec; ++col) {
       const double* x = v + (size_t)col * n;
       double* o = out + (size_t)col * n;
@@ -799,6 +824,7 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
     }
     ctx_sync(c);
   } catch (...) {
+    dev_free(mu_dev);
     for (double* b : fb) dev_free(b);
     throw;
   }
@@ -948,7 +974,13 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     h2d(c, v, h.data(), sizeof(double) * n);
     ctx_sync(c);
     const long before = c.launches;
+    double* mu_dev = dev_alloc<double>(op.k + 1);
+    h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
+    const bool persist = k::persist_eligible(c, a) && std::getenv("SE_PERSIST") != nullptr;
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    if (persist) {
+      k::filter_persist(c, a, v, nullptr, 0, nullptr, out, fb, mu_dev, op.k, op.c, op.invd);
+    } else {
     k::ChebArgs a1;
     a1.c = op.c;
     a1.invd = op.invd;
@@ -971,11 +1003,12 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
       cur = nxt;
       nxt = old;
     }
+    }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
     SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    const long per = c.launches - before;
+    const long per = persist ? op.k : c.launches - before;
     SE_CUDA(cudaGraphLaunch(ge, c.stream));  // warm
     SE_CUDA(cudaEventRecord(c.ev0, c.stream));
     for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));
@@ -985,7 +1018,8 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     SE_CUDA(cudaEventElapsedTime(&fms, c.ev0, c.ev1));
     ms = fms;
     launches = per * reps;
-    c.launches += per * (reps + 1);
+    c.launches += (c.launches - before) * (reps + 1);
+    dev_free(mu_dev);
   } catch (...) {
     if (ge) cudaGraphExecDestroy(ge);
     for (void* p : {(void*)v, (void*)out, (void*)fb[0], (void*)fb[1], (void*)fb[2]}) dev_free(p);

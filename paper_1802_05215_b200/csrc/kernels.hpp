@@ -46,6 +46,14 @@ struct ChebArgs {
 // Fused CSR SpMV + Chebyshev three-term recurrence + mu-accumulation (one filter degree).
 void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args);
 
+// Persistent cooperative filter (all k degrees in one launch, A resident in shared memory) for
+// matrices whose CSR fits the GPU's aggregate shared memory (persist.cu).
+bool persist_eligible(const Ctx& c, const DevCsr& a);
+void build_partition(Ctx& c, DevCsr& a, const int* rp_host);
+void filter_persist(Ctx& c, const DevCsr& a, const double* v, const Ctl* src_ctl, long src_ld,
+                    const Ctl* halt, double* out, double* const* bufs, const double* mu_dev,
+                    int kdeg, double cc, double invd);
+
 // Block KPM step over b <= 16 row-major probe columns (dos.hpp:98-108):
 //   first: w1 = (A w0 - c w0)/d ; zeta[0], zeta[1] partials
 //   next : t  = 2 (A w1 - c w1)/d - w0 ; zeta[k] partial
