@@ -142,6 +142,10 @@ SE_API int se_filter_bench(se_ctx* ctx, const se_csr* a, const se_poly_filter* f
  * Algorithmic bytes per pass: 16 n k + 24 n. */
 SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
 
+/* Production timing of kdeg degrees of the multi-vector filter (nv <= 8 recurrences sharing one
+ * staging of A per degree), graph-captured and replayed `reps` times.  Returns total ms. */
+SE_API int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int reps, double* ms);
+
 /* ---- filters (host, filter_poly.hpp) -------------------------------------------------------- */
 SE_API int se_damping_multipliers(int k, int damping, double* out);            /* :41-60   */
 SE_API int se_chebyshev_coeffs(double gamma, int k, double* out);              /* :30-39   */

@@ -366,6 +366,10 @@ int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms) {
   return guard([&] { cgs_bench(C(ctx), n, k, reps, *ms); });
 }
 
+int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int reps, double* ms) {
+  return guard([&] { multi_filter_bench(C(ctx), M(a), nv, kdeg, reps, *ms); });
+}
+
 int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
                   double* out, long* n_matvec) {
   return guard([&] {

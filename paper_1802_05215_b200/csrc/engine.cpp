@@ -1087,3 +1087,63 @@ void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) {
   cleanup();
 }
 }  // namespace se
+
+namespace se {
+// Time k degrees of the multi-vector filter over nv vectors (graph-captured, replayed).
+void multi_filter_bench(Ctx& c, const DevCsr& a, int nv, int kdeg, int reps, double& ms) {
+  if (nv < 1 || nv > 8 || kdeg < 2 || reps < 1) fail(SE_EINVAL, "se_multi_filter_bench: bad sizes");
+  const int n = a.n;
+  std::vector<double*> bufs;
+  auto alloc = [&]() {
+    double* p = dev_alloc<double>(n);
+    SE_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * n, c.stream));
+    bufs.push_back(p);
+    return p;
+  };
+  double *V[8], *O[8], *B[8][3];
+  for (int q = 0; q < nv; ++q) {
+    V[q] = alloc();
+    O[q] = alloc();
+    for (int r = 0; r < 3; ++r) B[q][r] = alloc();
+  }
+  cudaGraphExec_t ge = nullptr;
+  try {
+    ctx_sync(c);
+    SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    for (int j = 1; j <= kdeg; ++j) {
+      k::MultiArgs m{};
+      m.nv = nv;
+      m.c = 6.0;
+      m.invd = 1.0 / 6.0;
+      for (int q = 0; q < nv; ++q) {
+        m.x[q] = j == 1 ? V[q] : B[q][(j - 2) % 3];
+        m.prev[q] = j == 2 ? V[q] : B[q][j % 3];
+        m.y[q] = B[q][(j - 1) % 3];
+        m.out[q] = O[q];
+        m.mu0[q] = 0.5;
+        m.muj[q] = 0.1;
+        m.first[q] = j == 1;
+      }
+      k::spmv_cheb_multi(c, a, m);
+    }
+    cudaGraph_t g;
+    SE_CUDA(cudaStreamEndCapture(c.stream, &g));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev0, c.stream));
+    for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev1, c.stream));
+    SE_CUDA(cudaEventSynchronize(c.ev1));
+    float f = 0.f;
+    SE_CUDA(cudaEventElapsedTime(&f, c.ev0, c.ev1));
+    ms = f;
+  } catch (...) {
+    if (ge) cudaGraphExecDestroy(ge);
+    for (double* p : bufs) dev_free(p);
+    throw;
+  }
+  cudaGraphExecDestroy(ge);
+  for (double* p : bufs) dev_free(p);
+}
+}  // namespace se

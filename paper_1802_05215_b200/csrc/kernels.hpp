@@ -46,6 +46,23 @@ struct ChebArgs {
 // Fused CSR SpMV + Chebyshev three-term recurrence + mu-accumulation (one filter degree).
 void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args);
 
+// One filter degree for up to 8 independent recurrences sharing A (the slices of one GPU):
+// per vector q, first[q] selects the j = 1 update, x/prev may be W[:, ctl[q]->i] (x_ind/prev_ind),
+// and a halted ctl[q] skips the vector.
+struct MultiArgs {
+  const double* x[8];
+  const double* prev[8];
+  double* y[8];
+  double* out[8];
+  double mu0[8], muj[8];
+  const Ctl* ctl[8];
+  int x_ind[8], prev_ind[8], first[8];
+  long ld;
+  double c, invd;
+  int nv;
+};
+void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args);
+
 // Persistent cooperative filter (all k degrees in one launch, A resident in shared memory) for
 // matrices whose CSR fits the GPU's aggregate shared memory (persist.cu).
 bool persist_eligible(const Ctx& c, const DevCsr& a);

@@ -1,0 +1,13 @@
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1802_05215_b200 import _lib, api
+ctx = api.default_context(0)
+for spec in sys.argv[1].split(";"):
+    dims = [int(x) for x in spec.split(",")]
+    A = api.DeviceCsr.laplacian(dims, ctx)
+    for nv in (1, 2, 4, 8):
+        ms = C.c_double()
+        _lib.call("se_multi_filter_bench", ctx.handle, A.handle, nv, 100, 5, C.byref(ms))
+        per = ms.value / 500 * 1e3
+        print(f"{dims} nv={nv}: {per:.2f} us/degree ({per/nv:.2f} us per vector-degree)")
+    A.free()
