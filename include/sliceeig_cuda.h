@@ -108,6 +108,15 @@ SE_API int se_ctx_filter_timing(se_ctx* ctx, int enable, double* ms, long* launc
 SE_API int se_laplacian_host(int ndims, const int* dims, int* n, long* nnz, int* rp, int* ci, double* v);
 /* Closed-form spectrum, sorted ascending (laplacian.hpp:51-86). */
 SE_API int se_laplacian_eigs(int ndims, const int* dims, double* out);
+/* BASELINE cfg4 generator (the reference has none; SURVEY.md §8d defines it): symmetric n x n,
+ * band |i-j| <= halfband plus `extras` distinct uniformly random off-band columns per row (drawn
+ * in row order from Rng(seed).uniform(), resampled on collision, mirrored), one N(0,1) value per
+ * unordered off-diagonal pair (row-major order, then diagonal N(0,1) per row) and diagonal +=
+ * diag_frac * sum_j |a_ij|.  Call with rp == NULL for n/nnz, then again to fill. */
+SE_API int se_gen_random_sparse(int n, uint64_t seed, int halfband, int extras, double diag_frac,
+                                long* nnz, int* rp, int* ci, double* v);
+/* BASELINE cfg5 scaling vector: b_i = 0.5 + Rng(seed).uniform(), d_i = 1/sqrt(b_i) (host). */
+SE_API int se_mass_scaling(int n, uint64_t seed, double* b, double* d);
 /* Upload a host CSR (int32 row_ptr[n+1], int32 col_idx[nnz], f64 vals[nnz]). */
 SE_API int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, const double* vals,
                   se_csr** out);

@@ -58,6 +58,8 @@ SIGNATURES = {
     "se_ctx_filter_timing": [_VP, C.c_int, _PD, _PL, _PD],
     "se_laplacian_host": [C.c_int, _PI, _PI, _PL, _PI, _PI, _PD],
     "se_laplacian_eigs": [C.c_int, _PI, _PD],
+    "se_gen_random_sparse": [C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_double, _PL, _PI, _PI, _PD],
+    "se_mass_scaling": [C.c_int, C.c_uint64, _PD, _PD],
     "se_csr_upload": [_VP, C.c_int, _PI, _PI, _PD, C.POINTER(_VP)],
     "se_csr_gen_laplacian": [_VP, C.c_int, _PI, C.POINTER(_VP)],
     "se_csr_info": [_VP, _PI, _PL],

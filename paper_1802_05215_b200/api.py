@@ -236,6 +236,34 @@ def gen_laplacian(dims: Sequence[int]) -> CsrMatrix:
     return CsrMatrix(n.value, rp, ci, v)
 
 
+def gen_random_sparse(n: int, seed: int = 1234, halfband: int = 3, extras: int = 8,
+                      diag_frac: float = 0.1) -> CsrMatrix:
+    """BASELINE cfg4 generator (random banded + extras, symmetric; see sliceeig_cuda.h)."""
+    nnz = C.c_long()
+    call("se_gen_random_sparse", n, seed, halfband, extras, diag_frac, C.byref(nnz), None, None, None)
+    rp = np.empty(n + 1, np.int32)
+    ci = np.empty(nnz.value, np.int32)
+    v = np.empty(nnz.value, np.float64)
+    call("se_gen_random_sparse", n, seed, halfband, extras, diag_frac, C.byref(nnz), _pi(rp), _pi(ci),
+         _pd(v))
+    return CsrMatrix(n, rp, ci, v)
+
+
+def mass_scaling(n: int, seed: int = 1234):
+    """BASELINE cfg5: lumped mass b_i = 0.5 + uniform (Rng(seed)), d = b^-1/2."""
+    b = np.empty(n)
+    d = np.empty(n)
+    call("se_mass_scaling", n, seed, _pd(b), _pd(d))
+    return b, d
+
+
+def scale_sym_host(a: CsrMatrix, d) -> CsrMatrix:
+    """Host D A D (vals[p] = (a_ij d_i) d_j), the reference of DeviceCsr.scale_sym."""
+    d = _f64(d)
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    return CsrMatrix(a.n, a.row_ptr, a.col_idx, (a.vals * d[rows]) * d[a.col_idx])
+
+
 def laplacian_analytic_eigs(dims: Sequence[int]) -> np.ndarray:
     """laplacian.hpp:51-86."""
     d = np.asarray(list(dims), np.int32)

@@ -214,6 +214,79 @@ int se_laplacian_eigs(int ndims, const int* dims, double* out) {
   });
 }
 
+int se_gen_random_sparse(int n, uint64_t seed, int halfband, int extras, double diag_frac,
+                         long* nnz, int* rp, int* ci, double* v) {
+  return guard([&] {
+    if (n < 1 || halfband < 0 || extras < 0) fail(SE_EINVAL, "gen_random_sparse: bad parameters");
+    if (extras > 0 && n - (2 * halfband + 1) < extras * 4)
+      fail(SE_EINVAL, "gen_random_sparse: matrix too small for the requested extras");
+    // pattern (row lists kept sorted)
+    std::vector<std::vector<int>> nb(n);
+    for (int i = 0; i < n; ++i) {
+      nb[i].reserve(2 * halfband + 2 * extras + 8);
+      for (int j = std::max(0, i - halfband); j <= std::min(n - 1, i + halfband); ++j)
+        if (j != i) nb[i].push_back(j);
+    }
+    Rng rng(seed);
+    auto has = [&](int i, int j) { return std::binary_search(nb[i].begin(), nb[i].end(), j); };
+    auto insert = [&](int i, int j) { nb[i].insert(std::upper_bound(nb[i].begin(), nb[i].end(), j), j); };
+    for (int i = 0; i < n; ++i) {
+      int got = 0;
+      while (got < extras) {
+        const int j = (int)(rng.uniform() * n);
+        if (std::abs(i - j) <= halfband || has(i, j)) continue;  // resample collisions
+        insert(i, j);
+        insert(j, i);
+        ++got;
+      }
+    }
+    long total = n;
+    for (int i = 0; i < n; ++i) total += (long)nb[i].size();
+    *nnz = total;
+    if (!rp) return;
+    // values: one N(0,1) per unordered pair (i < j) in row-major order, then the diagonal
+    std::vector<long> start(n + 1, 0);
+    for (int i = 0; i < n; ++i) start[i + 1] = start[i] + (long)nb[i].size() + 1;
+    rp[0] = 0;
+    for (int i = 0; i < n; ++i) rp[i + 1] = (int)start[i + 1];
+    auto pos = [&](int i, int j) {  // index of column j in row i (diagonal included in order)
+      const auto it = std::lower_bound(nb[i].begin(), nb[i].end(), j);
+      const long k = it - nb[i].begin();
+      return start[i] + k + (j > i ? 1 : 0);
+    };
+    for (int i = 0; i < n; ++i) {
+      const long dpos = start[i] + (std::lower_bound(nb[i].begin(), nb[i].end(), i) - nb[i].begin());
+      ci[dpos] = i;
+      for (int j : nb[i]) ci[pos(i, j)] = j;
+    }
+    std::vector<double> rowabs(n, 0.0);
+    for (int i = 0; i < n; ++i)
+      for (int j : nb[i])
+        if (j > i) {
+          const double val = rng.normal();
+          v[pos(i, j)] = val;
+          v[pos(j, i)] = val;
+          rowabs[i] += std::abs(val);
+          rowabs[j] += std::abs(val);
+        }
+    for (int i = 0; i < n; ++i) {
+      const long dpos = start[i] + (std::lower_bound(nb[i].begin(), nb[i].end(), i) - nb[i].begin());
+      v[dpos] = rng.normal() + diag_frac * rowabs[i];
+    }
+  });
+}
+
+int se_mass_scaling(int n, uint64_t seed, double* b, double* d) {
+  return guard([&] {
+    if (n < 0) fail(SE_EINVAL, "mass_scaling: negative size");
+    Rng rng(seed);
+    for (int i = 0; i < n; ++i) {
+      b[i] = 0.5 + rng.uniform();
+      d[i] = 1.0 / std::sqrt(b[i]);
+    }
+  });
+}
+
 int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, const double* vals,
                   se_csr** out) {
   return guard([&] {

@@ -4,8 +4,9 @@ absent on the GPU box):
 
     python tests/golden/make_golden.py [--skip-solve]
 
-Outputs tests/golden/*.npz.  Every array is produced by calling the reference library; nothing here
-restates the algorithm.
+Outputs tests/golden/*.npz.  Every eigen/DOS/filter array is produced by calling the reference
+library; the cfg4/cfg5 input matrices (generators the reference lacks) come from
+the product's host-only generator, whose structural properties tests/test_configs.py checks.
 """
 import argparse
 import os
@@ -136,10 +137,57 @@ def cfg2():
     save("cfg2", bounds=[lo, hi], zeta=zeta, x=x, y=y, nev=nev, bp=bp, est=est, degrees=degs)
 
 
+def cfg4p():
+    """BASELINE configs[3] proxy: random banded + 8 extras, n = 20,000 (seed 4); window = middle 2%
+    of the KPM DOS (first grid points with cumulative mass >= 0.49 / 0.51, npts 3000), 8 slices,
+    ChebLanTr tol 1e-9; the reference's slice 3 solve."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1802_05215_b200 import api  # host-only generator (no GPU needed)
+    a = api.gen_random_sparse(20000, 4)
+    rp, ci, v = a.row_ptr, a.col_idx, a.vals
+    lo, hi = reflib.lan_tr_bounds(rp, ci, v, 1e-4, 60, 40, 4)
+    zeta = reflib.kpm_moments(rp, ci, v, lo, hi, 60, 40, 4, "rademacher")
+    x, y, nev = reflib.curve_from_moments(zeta / (40.0 * 20000), 20000, lo, hi, 3000)
+    cum = np.concatenate([[0.0], np.cumsum(0.5 * (y[1:] + y[:-1]) * np.diff(x))])
+    cum /= cum[-1]
+    w0, w1 = x[np.argmax(cum >= 0.49)], x[np.argmax(cum >= 0.51)]
+    bp, est = reflib.slice_spectrum(x, y, 20000, w0, w1, 8)
+    t0 = time.time()
+    r = reflib.cheb_lan(rp, ci, v, "tr", bp[3], bp[4], lo, hi, res_tol=1e-9,
+                        est_count=int(np.ceil(est[3])), seed=4)
+    print(f"cfg4p slice 3: {len(r['eigenvalues'])} pairs, deg {r['degree']}, {time.time() - t0:.0f} s")
+    save("cfg4p", bounds=[lo, hi], zeta=zeta, window=[w0, w1], bp=bp, est=est,
+         slice3_vals=r["eigenvalues"], slice3_res=r["residuals"],
+         slice3_meta=[r["niter"], r["n_A_matvec"], r["degree"]], nnz=a.nnz,
+         rp_check=[int(rp[-1]), int(ci.sum() % 1000003)], v_check=[float(v.sum()), float(np.abs(v).sum())])
+
+
+def cfg5p():
+    """BASELINE configs[4] proxy: 24^3 Laplacian scaled to D A D, d = (0.5 + uniform)^-1/2
+    (seed 5); [1, 2] in 8 DOS slices; the reference's ChebLanTr on slices 2 and 7 (tol 1e-8)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1802_05215_b200 import api
+    L = api.gen_laplacian([24, 24, 24])
+    b, d = api.mass_scaling(L.n, 5)
+    S = api.scale_sym_host(L, d)
+    rp, ci, v = S.row_ptr, S.col_idx, S.vals
+    lo, hi = reflib.lan_tr_bounds(rp, ci, v, 1e-4, 60, 40, 5)
+    zeta = reflib.kpm_moments(rp, ci, v, lo, hi, 60, 40, 5, "rademacher")
+    x, y, nev = reflib.curve_from_moments(zeta / (40.0 * L.n), L.n, lo, hi, 300)
+    bp, est = reflib.slice_spectrum(x, y, L.n, 1.0, 2.0, 8)
+    out = dict(bounds=[lo, hi], zeta=zeta, bp=bp, est=est, d=d, vals_scaled=v)
+    for s in (2, 7):
+        r = reflib.cheb_lan(rp, ci, v, "tr", bp[s], bp[s + 1], lo, hi, res_tol=1e-8,
+                            est_count=int(np.ceil(est[s])), seed=5)
+        out[f"slice{s}_vals"] = r["eigenvalues"]
+        out[f"slice{s}_res"] = r["residuals"]
+    save("cfg5p", **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-solve", action="store_true")
-    ap.add_argument("--only", default="kats,cfg1,cfg2")
+    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p")
     a = ap.parse_args()
     only = a.only.split(",")
     if "kats" in only:
@@ -148,3 +196,7 @@ if __name__ == "__main__":
         cfg2()
     if "cfg1" in only:
         cfg1(a.skip_solve)
+    if "cfg4p" in only:
+        cfg4p()
+    if "cfg5p" in only:
+        cfg5p()

@@ -274,3 +274,48 @@ def test_acceptance_windows_all_drivers(gpu_ctx, dims):
             for i in range(0, oracle.size, 9):
                 lam, res = api.rayleigh_and_residual(a, None, r.vectors[:, i])
                 assert res <= 1e-8 and abs(lam - r.eigenvalues[i]) <= 1e-10
+
+
+def test_cfg4_proxy_slice_matches_reference(gpu_ctx, golden):
+    """BASELINE configs[3] proxy (random banded + 8 extras, n = 20,000): the reference-solved
+    slice 3 of the middle-2% window -- identical count, |dlambda| <= 1e-10 |lambda|, res <= 1e-9."""
+    api = _api()
+    g = golden("cfg4p")
+    a = api.gen_random_sparse(20000, 4)
+    lo, hi = g["bounds"]
+    bp, est = g["bp"], g["est"]
+    # the device KPM + slicer reproduce the reference's breakpoints on the 3000-point grid
+    z = api.kpm_moments(a, api.SpectralBounds(lo, hi), 60, 40, seed=4)
+    assert moments_ok(z / (40 * 20000.0), g["zeta"] / (40 * 20000.0))
+    curve = api.kpm_curve(z / (40 * 20000.0), a.n, api.SpectralBounds(lo, hi), 3000)
+    s = api.slice_spectrum(curve, *g["window"], 8)
+    assert np.array_equal(s.breakpoints, bp)
+    f = api.find_pol(bp[3], bp[4], api.SpectralBounds(lo, hi))
+    assert f.k == int(g["slice3_meta"][2])
+    r = api.cheb_lan_tr(a, None, f, bp[3], bp[4],
+                        api.SolverConfig(res_tol=1e-9, est_count=int(np.ceil(est[3])), seed=4))
+    ref = g["slice3_vals"]
+    assert r.eigenvalues.size == ref.size
+    assert np.all(np.abs(r.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+    assert np.all(r.residuals <= 1e-9 * np.maximum(1.0, np.abs(r.eigenvalues)))
+
+
+def test_cfg5_proxy_scaled_slices_match_reference(gpu_ctx, golden):
+    """BASELINE configs[4] proxy (24^3 Laplacian, lumped mass by diagonal scaling D A D): device
+    scaling bit-identical to the host's; slices 2 and 7 of [1,2] match the reference."""
+    api = _api()
+    g = golden("cfg5p")
+    A = api.DeviceCsr.laplacian([24, 24, 24])
+    A.scale_sym(g["d"])
+    host = A.download()
+    assert np.array_equal(host.vals, g["vals_scaled"])
+    lo, hi = g["bounds"]
+    bp, est = g["bp"], g["est"]
+    for s in (2, 7):
+        f = api.find_pol(bp[s], bp[s + 1], api.SpectralBounds(lo, hi))
+        r = api.cheb_lan_tr(A, None, f, bp[s], bp[s + 1],
+                            api.SolverConfig(res_tol=1e-8, est_count=int(np.ceil(est[s])), seed=5))
+        ref = g[f"slice{s}_vals"]
+        assert r.eigenvalues.size == ref.size, (s, r.eigenvalues.size, ref.size)
+        assert np.all(np.abs(r.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+        assert np.all(r.residuals <= 1e-8 * np.maximum(1.0, np.abs(r.eigenvalues)))
