@@ -155,6 +155,31 @@ def slice_owner(index: int, world: int) -> int:
     return index % world
 
 
+def slice_cost(est: float, degree: int, n: int, nnz: int) -> float:
+    """Modelled device bytes of one slice solve: ~3.7 est Lanczos steps (measured on cfg2), each
+    k filter degrees (12 nnz + 40 n bytes) plus two CGS passes over ~m/2 = 2 est columns
+    (32 n * 2 est bytes)."""
+    steps = 3.7 * max(est, 1.0)
+    return steps * (degree * (12.0 * nnz + 40.0 * n) + 64.0 * n * max(est, 1.0))
+
+
+def assign_lpt(costs: Sequence[float], world: int) -> List[int]:
+    """Longest-processing-time-first assignment of slices to ranks (ties -> lowest rank), so the
+    makespan of uneven DOS slices is balanced when there are more slices than GPUs.  With one
+    slice per rank or more ranks than slices this is the identity / round-robin."""
+    if world <= 1:
+        return [0] * len(costs)
+    if len(costs) <= world:
+        return [i % world for i in range(len(costs))]
+    load = [0.0] * world
+    owner = [0] * len(costs)
+    for i in sorted(range(len(costs)), key=lambda q: (-costs[q], q)):
+        r = min(range(world), key=lambda q: (load[q], q))
+        owner[i] = r
+        load[r] += costs[i]
+    return owner
+
+
 def trim_to_slice(vals, res, index: int, ns: int, lo: float, hi: float, delta: float):
     """sliceeig_main.cpp:422-442: an eigenvalue within delta of an interior breakpoint belongs to
     the slice below it.  Returns the kept positions."""
@@ -262,7 +287,12 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
     t2 = time.perf_counter()
     ns = len(est)
     delta = 1e-10 * (lmax - lmin)
-    mine_idx = [i for i in range(ns) if slice_owner(i, dist.world) == dist.rank
+    # LPT over modelled slice costs (degrees are cheap host computations, identical on every rank)
+    degs = [api.find_pol(bp[i], bp[i + 1], api.SpectralBounds(lmin, lmax),
+                         api.PolyOpts(damping=plan.damping)).k for i in range(ns)]
+    nnz = getattr(getattr(backend, "A", None), "nnz", 7 * backend.n)
+    owners = assign_lpt([slice_cost(est[i], degs[i], backend.n, nnz) for i in range(ns)], dist.world)
+    mine_idx = [i for i in range(ns) if owners[i] == dist.rank
                 and (plan.only is None or i in plan.only)]
 
     def work(i):
