@@ -264,10 +264,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--proxy", action="store_true", help="run the GPU arm on the CPU proxy size")
     args = ap.parse_args()
-    rank, world, local = _dist_init() if args.impl == "ours" or int(os.environ.get("WORLD_SIZE", "1")) > 1 else (0, 1, 0)
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        # the reference is CPU code: rank 0 runs it on the host cores, other ranks exit at once
+        run_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return
+    rank, world, local = _dist_init()
     import torch
     from paper_1802_05215_b200 import api
     from paper_1802_05215_b200.pipeline import Dist, GpuBackend, run

@@ -623,6 +623,18 @@ class EigenResults:
     hit_max_its: bool
 
 
+def _host_buffer(shape):
+    """Page-locked host array when torch is importable (D2H of eigenvectors at PCIe speed), else
+    an ordinary numpy array."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:
+        pass
+    return np.empty(shape, np.float64)
+
+
 def _cheb_lan(solver: int, a, b, f: PolynomialFilter, xi, eta, cfg: SolverConfig,
               locked: Optional[DeflationSet], want_vectors: bool) -> EigenResults:
     who = "cheb_lan_tr" if solver == 1 else "cheb_lan_nr"
@@ -654,7 +666,7 @@ def _cheb_lan(solver: int, a, b, f: PolynomialFilter, xi, eta, cfg: SolverConfig
         k = nev.value
         vals = np.empty(k)
         res = np.empty(k)
-        vecs = np.empty((k, d.n)) if (want_vectors and k) else None
+        vecs = _host_buffer((k, d.n)) if (want_vectors and k) else None
         call("se_results_copy", h, _pd(vals) if k else None, _pd(res) if k else None,
              _pd(vecs) if vecs is not None else None)
         niter, hit = C.c_long(), C.c_int()

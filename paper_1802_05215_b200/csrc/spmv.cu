@@ -136,73 +136,74 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
 // as in k_spmv_cheb, so each vector's result is bit-identical to its single-vector filter).
 constexpr int kMV = 8;
 
-__global__ void __launch_bounds__(kRows) k_spmv_cheb_multi(int n, const int* __restrict__ rp,
-                                                            const int* __restrict__ ci,
-                                                            const double* __restrict__ v,
-                                                            MultiArgs a) {
-  __shared__ __align__(16) double s_v[kChunk + 8];
-  __shared__ __align__(16) int s_c[kChunk + 8];
-  const int r0 = blockIdx.x * kRows;
-  const int r = r0 + threadIdx.x;
-  const bool live = r < n;
-  const int rend = min(r0 + kRows, n);
+constexpr int kMRows = 64;  // rows per tile; one warp-pair per vector: 64 x kMV threads
+
+// CTA = 64-row tile x nv vectors (thread = (vector, row)); the tile's A entries are staged once
+// with cp.async and shared by every vector's row sums (each warp: 32 consecutive rows of one
+// vector, so gathers coalesce exactly as in the single-vector kernel).
+__global__ void __launch_bounds__(kMRows * kMV) k_spmv_cheb_multi(int n, const int* __restrict__ rp,
+                                                                  const int* __restrict__ ci,
+                                                                  const double* __restrict__ v,
+                                                                  MultiArgs a) {
+  __shared__ __align__(16) double s_v[kMRows * 16 + 8];
+  __shared__ __align__(16) int s_c[kMRows * 16 + 8];
+  constexpr int kStage = kMRows * 16;
+  const int q = threadIdx.x / kMRows;  // vector
+  const int lr = threadIdx.x - q * kMRows;
+  const int r0 = blockIdx.x * kMRows;
+  const int r = r0 + lr;
+  const int rend = min(r0 + kMRows, n);
   const int base = __ldg(rp + r0), end = __ldg(rp + rend);
+  const bool on = q < a.nv && !(a.ctl[q] && a.ctl[q]->halted);
+  const bool live = on && r < n;
+  size_t ioff = 0;
+  const double* __restrict__ x = nullptr;
   int rs = end, re = end;
+  double xr = 0.0, pv = 0.0, ov = 0.0;
   if (live) {
+    ioff = a.ctl[q] ? (size_t)a.ctl[q]->i * a.ld : 0;
+    x = a.x[q] + (a.x_ind[q] ? ioff : 0);
     rs = __ldg(rp + r);
     re = __ldg(rp + r + 1);
+    xr = __ldg(x + r);
+    if (!a.first[q]) {
+      pv = __ldg(a.prev[q] + (a.prev_ind[q] ? ioff : 0) + r);
+      ov = a.out[q][r];
+    }
   }
-  const double* xs[kMV];
-  bool on[kMV];
-  double acc[kMV];
-#pragma unroll
-  for (int q = 0; q < kMV; ++q) {
-    on[q] = q < a.nv && !(a.ctl[q] && a.ctl[q]->halted);
-    const size_t ioff = (on[q] && a.ctl[q]) ? (size_t)a.ctl[q]->i * a.ld : 0;
-    xs[q] = on[q] ? a.x[q] + (a.x_ind[q] ? ioff : 0) : nullptr;
-    acc[q] = 0.0;
-  }
-  for (int c0 = base; c0 < end; c0 += kChunk) {
-    const int cn = min(kChunk, end - c0), cend = c0 + cn;
+  double acc = 0.0;
+  for (int c0 = base; c0 < end; c0 += kStage) {
+    const int cn = min(kStage, end - c0), cend = c0 + cn;
     const int va = c0 & ~1, ca = c0 & ~3;
     const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
-    for (int q = threadIdx.x; q < nv16; q += kRows)
-      cp_async16(&s_v[2 * q], v + va + 2 * q, 8 * min(2, cend - (va + 2 * q)));
-    for (int q = threadIdx.x; q < nc16; q += kRows)
-      cp_async16(&s_c[4 * q], ci + ca + 4 * q, 4 * min(4, cend - (ca + 4 * q)));
+    __syncthreads();
+    for (int t = threadIdx.x; t < nv16; t += kMRows * kMV)
+      cp_async16(&s_v[2 * t], v + va + 2 * t, 8 * min(2, cend - (va + 2 * t)));
+    for (int t = threadIdx.x; t < nc16; t += kMRows * kMV)
+      cp_async16(&s_c[4 * t], ci + ca + 4 * t, 4 * min(4, cend - (ca + 4 * t)));
     cp_async_wait_all();
     __syncthreads();
-    const int p0 = max(rs, c0), pend = min(re, cend);
-#pragma unroll
-    for (int q = 0; q < kMV; ++q) {
-      if (!on[q]) continue;
+    if (live) {
+      const int p0 = max(rs, c0), pend = min(re, cend);
       for (int p = p0; p < pend; p += 8) {
         double xv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = (p + u < pend) ? __ldg(xs[q] + s_c[p + u - ca]) : 0.0;
+        for (int u = 0; u < 8; ++u) xv[u] = (p + u < pend) ? __ldg(x + s_c[p + u - ca]) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (p + u < pend) acc[q] = add(acc[q], mul(s_v[p + u - va], xv[u]));
+          if (p + u < pend) acc = add(acc, mul(s_v[p + u - va], xv[u]));
       }
     }
-    __syncthreads();
   }
   if (!live) return;
-#pragma unroll
-  for (int q = 0; q < kMV; ++q) {
-    if (!on[q]) continue;
-    const size_t ioff = a.ctl[q] ? (size_t)a.ctl[q]->i * a.ld : 0;
-    const double xr = xs[q][r];
-    const double t = mul(sub(acc[q], mul(a.c, xr)), a.invd);
-    if (a.first[q]) {
-      a.y[q][r] = t;
-      a.out[q][r] = add(add(0.0, mul(a.mu0[q], xr)), mul(a.muj[q], t));
-    } else {
-      const double* __restrict__ prev = a.prev[q] + (a.prev_ind[q] ? ioff : 0);
-      const double tj = sub(mul(2.0, t), prev[r]);
-      a.y[q][r] = tj;
-      a.out[q][r] = add(a.out[q][r], mul(a.muj[q], tj));
-    }
+  const double t = mul(sub(acc, mul(a.c, xr)), a.invd);
+  if (a.first[q]) {
+    a.y[q][r] = t;
+    a.out[q][r] = add(add(0.0, mul(a.mu0[q], xr)), mul(a.muj[q], t));
+  } else {
+    const double tj = sub(mul(2.0, t), pv);
+    a.y[q][r] = tj;
+    a.out[q][r] = add(ov, mul(a.muj[q], tj));
   }
 }
 
@@ -448,7 +449,8 @@ size_t kpm_scratch_doubles(const Ctx& c, int n) { return (size_t)2 * kB * kpm_bl
 void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args) {
   if (a.n == 0 || args.nv == 0) return;
   if (args.nv > kMV) fail(SE_EINVAL, "spmv_cheb_multi: too many vectors");
-  k_spmv_cheb_multi<<<(a.n + kRows - 1) / kRows, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, args);
+  k_spmv_cheb_multi<<<(a.n + kMRows - 1) / kMRows, kMRows * kMV, 0, c.stream>>>(a.n, a.rp, a.ci,
+                                                                                a.v, args);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
