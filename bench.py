@@ -263,6 +263,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--proxy", action="store_true", help="run the GPU arm on the CPU proxy size")
+    ap.add_argument("--jobs", type=int, default=0, help="concurrent slices per GPU (0: all)")
     args = ap.parse_args()
     if args.impl == "reference":
         # the reference is CPU code: rank 0 runs it on the host cores, other ranks exit at once
@@ -276,7 +277,7 @@ def main():
     cfg = PROXY if args.proxy else CFG2
     dist = Dist.from_torch() if world > 1 else Dist()
     backend = GpuBackend(device=local, dims=cfg["dims"])
-    plan = _plan(cfg)
+    plan = _plan(cfg, jobs=args.jobs)
     for _ in range(args.warmup):
         res = run(plan, backend, dist)
     # ---- timed region: matrix resident in HBM ------------------------------------------------
