@@ -443,6 +443,13 @@ int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int re
   return guard([&] { multi_filter_bench(C(ctx), M(a), nv, kdeg, reps, *ms); });
 }
 
+int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms) {
+  return guard([&] {
+    if (mode == 1 && !k::cgs_mid_supported(n, k)) fail(SE_EINVAL, "se_cgs2_bench: k too large for the fused path");
+    cgs2_bench(C(ctx), n, k, reps, mode, *ms);
+  });
+}
+
 int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
                   double* out, long* n_matvec) {
   return guard([&] {

@@ -41,6 +41,11 @@ struct Krylov {
 
   double* mu_dev = nullptr;
   bool persist = false;
+  // fused CGS2 middle (cgs_mid.cu): second coefficient vector + its own scratch and counter
+  double* coef2 = nullptr;
+  double* mid_scratch = nullptr;
+  unsigned* mid_cnt = nullptr;
+  int mid_cap = 0;
 
   Krylov(Ctx& cc, const DevCsr& a, const StepOp& o) : c(cc), A(a), op(o), n(a.n) {
     t = dev_alloc<double>(n);
@@ -61,6 +66,9 @@ struct Krylov {
     devmat_free(W);
     devmat_free(L);
     dev_free(mu_dev);
+    dev_free(coef2);
+    dev_free(mid_scratch);
+    dev_free(mid_cnt);
     for (void* p : {(void*)t, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl, (void*)alpha,
                     (void*)beta, (void*)hdiag, (void*)coef, (void*)coef_l, (void*)dscal,
                     (void*)s.buf, (void*)s.cnt})
@@ -125,7 +133,28 @@ struct Krylov {
       SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
       dirty = true;
     }
+    if (W.cap > mid_cap && k::cgs_mid_supported(n, W.cap) && std::getenv("SE_CGS_FUSED")) {
+      SE_CUDA(cudaStreamSynchronize(c.stream));
+      dev_free(coef2);
+      dev_free(mid_scratch);
+      if (!mid_cnt) {
+        mid_cnt = dev_alloc<unsigned>(1);
+        SE_CUDA(cudaMemsetAsync(mid_cnt, 0, sizeof(unsigned), c.stream));
+      }
+      coef2 = dev_alloc<double>(W.cap);
+      mid_scratch = dev_alloc<double>(k::cgs_mid_scratch_doubles(c, W.cap));
+      mid_cap = W.cap;
+      dirty = true;
+    }
     if (dirty) drop_graph();
+  }
+
+  bool fused() const {
+    // Opt-in (SE_CGS_FUSED=1): the fused middle saves one of four reads of W per step but stages
+    // narrow (R x 8-byte) column segments, and the per-SM request rate caps it below the two
+    // full-width unfused passes at basis widths above a few hundred ("CGS2 fusion").
+    static const bool want = std::getenv("SE_CGS_FUSED") != nullptr;
+    return want && mid_cap >= W.cap && k::cgs_mid_supported(n, W.cap);
   }
 
   Ctl get() {
@@ -201,8 +230,14 @@ struct Krylov {
       k::norm_before(c, s, n, t, ctl);
     }
     double* h = mode == 1 ? hdiag : nullptr;
-    k::cgs_pass(c, s, n, t, W.p, false, false, ctl, h, coef, W.cap);
-    k::cgs_pass(c, s, n, t, W.p, false, true, ctl, h, coef, W.cap);
+    if (fused()) {  // CGS2 with three reads of W: T1, fused N1 + norm + T2, N2
+      k::gemvt_only(c, s, n, t, W.p, false, ctl, h, coef, W.cap);
+      k::cgs_mid(c, n, t, W.p, ctl, coef, coef2, h, W.cap, mid_scratch, mid_cnt);
+      k::gemvn_only(c, s, n, t, W.p, true, ctl, coef2, W.cap);
+    } else {
+      k::cgs_pass(c, s, n, t, W.p, false, false, ctl, h, coef, W.cap);
+      k::cgs_pass(c, s, n, t, W.p, false, true, ctl, h, coef, W.cap);
+    }
     k::normalize_next(c, s, n, t, W.p, ctl, beta);
     k::stamp(c, ctl, 2);
   }
@@ -501,9 +536,9 @@ struct Slice {
     if (std::getenv("SE_PROFILE"))
       std::fprintf(stderr,
                    "[se] n=%d its=%ld total %.3f mv %.3f orth %.3f check %.3f eig %.3f cand %.3f "
-                   "passes %lld check_kernel_ms %.1f\n",
+                   "passes %lld check_kernel_ms %.1f wcap %d fused %d\n",
                    A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
-                   kr.get().passes_total, c.prof_kernel_ms);
+                   kr.get().passes_total, c.prof_kernel_ms, kr.W.cap, (int)kr.fused());
     r->niter = its;
     r->hit_max_its = warn;
     r->counters = cnt;
@@ -1033,24 +1068,34 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
 namespace se {
 // Time one classical Gram-Schmidt pass (k_gemvt + k_gemvn with norm) against an n x k basis, as it
 // runs inside the Lanczos step graph (production path), replayed `reps` times between events.
-void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) {
+void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) { cgs2_bench(c, n, kcols, reps, -1, ms); }
+
+// mode -1: one unfused pass; 0: a CGS2 step as two unfused passes; 1: the fused CGS2 step
+// (T1 + cgs_mid + N2).  The re-pass is forced (before = 1e300) so both paths do full work.
+void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
   if (n < 1 || kcols < 1 || reps < 1) fail(SE_EINVAL, "se_cgs_bench: bad sizes");
   double* W = dev_alloc<double>((size_t)n * kcols);
   double* t = dev_alloc<double>(n);
   double* coef = dev_alloc<double>(kcols);
-  Ctl* ctl = dev_alloc<Ctl>(1);
+  double* coef2 = dev_alloc<double>(kcols);
+  Ctl* ctl = dev_alloc<Ctl>(2);  // [0] live, [1] the state every replay starts from
   k::Scratch s;
   s.cap = k::cgs_scratch_doubles(c, n, kcols);
   s.ncnt = k::cgs_counter_slots(n, kcols);
   s.buf = dev_alloc<double>(s.cap);
   s.cnt = dev_alloc<unsigned>(s.ncnt);
+  double* mid = mode == 1 ? dev_alloc<double>(k::cgs_mid_scratch_doubles(c, kcols)) : nullptr;
+  unsigned* mcnt = dev_alloc<unsigned>(1);
   cudaGraphExec_t ge = nullptr;
   auto cleanup = [&] {
     if (ge) cudaGraphExecDestroy(ge);
-    for (void* p : {(void*)W, (void*)t, (void*)coef, (void*)ctl, (void*)s.buf, (void*)s.cnt}) dev_free(p);
+    for (void* p : {(void*)W, (void*)t, (void*)coef, (void*)coef2, (void*)ctl, (void*)s.buf, (void*)s.cnt,
+                    (void*)mid, (void*)mcnt})
+      dev_free(p);
   };
   try {
     SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
+    SE_CUDA(cudaMemsetAsync(mcnt, 0, sizeof(unsigned), c.stream));
     // deterministic pseudo-random contents (values do not affect the traffic)
     std::vector<double> h((size_t)n);
     Rng rng(7);
@@ -1060,12 +1105,23 @@ void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) {
     h2d(c, t, h.data(), sizeof(double) * n);
     Ctl z{};
     z.i = kcols - 1;
-    z.before = 1.0;
+    z.before = mode < 0 ? 1.0 : 1e300;
     h2d(c, ctl, &z, sizeof(Ctl));
+    h2d(c, ctl + 1, &z, sizeof(Ctl));
     ctx_sync(c);
     const long before = c.launches;
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
-    k::cgs_pass(c, s, n, t, W, false, false, ctl, nullptr, coef, kcols);
+    SE_CUDA(cudaMemcpyAsync(ctl, ctl + 1, sizeof(Ctl), cudaMemcpyDeviceToDevice, c.stream));
+    if (mode < 0) {
+      k::cgs_pass(c, s, n, t, W, false, false, ctl, nullptr, coef, kcols);
+    } else if (mode == 0) {
+      k::cgs_pass(c, s, n, t, W, false, false, ctl, nullptr, coef, kcols);
+      k::cgs_pass(c, s, n, t, W, false, true, ctl, nullptr, coef, kcols);
+    } else {
+      k::gemvt_only(c, s, n, t, W, false, ctl, nullptr, coef, kcols);
+      k::cgs_mid(c, n, t, W, ctl, coef, coef2, nullptr, kcols, mid, mcnt);
+      k::gemvn_only(c, s, n, t, W, true, ctl, coef2, kcols);
+    }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
     SE_CUDA(cudaGraphInstantiate(&ge, g, 0));

@@ -70,6 +70,7 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
 }
 namespace se {
 void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms);
+void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms);
 }
 namespace se {
 void multi_filter_bench(Ctx& c, const DevCsr& a, int nv, int kdeg, int reps, double& ms);

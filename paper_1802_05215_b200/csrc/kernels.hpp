@@ -114,6 +114,20 @@ void nr_sub_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, C
 // hdiag[i] += coef[i] (TR's H(i,i) += h[i], eigensolvers.hpp:534).  cap = max column count.
 void cgs_pass(Ctx& c, const Scratch& s, int n, double* t, const double* Q, bool use_lock,
               bool pass2, Ctl* ctl, double* hdiag, double* coef, int cap);
+// Split CGS pass launchers (same scratch layout as cgs_pass): GEMV-T (coef = Q^T t) only, and
+// GEMV-N (t -= Q coef, norm, DGKS flags) only.
+void gemvt_only(Ctx& c, const Scratch& s, int n, const double* t, const double* Q, bool pass2,
+                Ctl* ctl, double* hdiag, double* coef, int cap);
+void gemvn_only(Ctx& c, const Scratch& s, int n, double* t, const double* Q, bool pass2, Ctl* ctl,
+                const double* coef, int cap);
+// Fused middle of CGS2 (cgs_mid.cu): t1 = t - Q coef1, ||t1||, DGKS flag, coef2 = Q^T t1 with one
+// read of Q.  Needs an even n, a basis narrow enough for two-row blocks in shared memory
+// (cgs_mid_supported) and its own scratch (cgs_mid_scratch_doubles).
+constexpr int kMaxFusedCols = 3200;
+size_t cgs_mid_scratch_doubles(const Ctx& c, int cap_cols);
+bool cgs_mid_supported(int n, int cap_cols);
+void cgs_mid(Ctx& c, int n, double* t, const double* Q, Ctl* ctl, const double* coef1,
+             double* coef2, double* hdiag, int cap, double* scratch, unsigned* cnt);
 // t -= Q (Q^T t) with a host-side column count (project_x, eigensolvers.hpp:223-227).
 void project_out(Ctx& c, const Scratch& s, int n, int kq, const double* Q, double* t,
                  double* coef);

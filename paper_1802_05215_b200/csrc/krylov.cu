@@ -456,6 +456,39 @@ static void cgs_impl(Ctx& c, const Scratch& s, int n, double* t, const double* Q
   SE_CUDA(cudaGetLastError());
 }
 
+void gemvt_only(Ctx& c, const Scratch& s, int n, const double* t, const double* Q, bool pass2,
+                Ctl* ctl, double* hdiag, double* coef, int cap) {
+  if (n == 0) return;
+  const int ldp = std::max(cap, 1);
+  const int rch = rch_for(n);
+  const int nrb = (n + rch - 1) / rch;
+  const int ngrp_max = (ldp + kCW - 1) / kCW;
+  need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
+  k_gemvt<<<nrb * ngrp_max, kThreads, 0, c.stream>>>(n, rch, Q, t, ctl, 0, pass2 ? 1 : 0, -1, s.buf,
+                                                     ldp, s.cnt + kSlotGroups, coef, hdiag);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+void gemvn_only(Ctx& c, const Scratch& s, int n, double* t, const double* Q, bool pass2, Ctl* ctl,
+                const double* coef, int cap) {
+  if (n == 0) return;
+  const int ldp = std::max(cap, 1);
+  const int rch = rch_for(n);
+  const int nrb = (n + rch - 1) / rch;
+  const int ngrp_max = (ldp + kCW - 1) / kCW;
+  const int gn = (n + kThreads - 1) / kThreads;
+  const int ncc = (ldp + kNW - 1) / kNW;
+  need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
+  double* P = s.buf + (size_t)nrb * ldp;
+  double* npart = P + (size_t)ncc * n;
+  k_gemvn<<<dim3(gn, ncc), kThreads, 0, c.stream>>>(n, Q, t, ctl, 0, pass2 ? 1 : 0, -1, coef, P,
+                                                    s.cnt + kSlotGroups + ngrp_max, npart,
+                                                    s.cnt + kSlotMisc);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
 void cgs_pass(Ctx& c, const Scratch& s, int n, double* t, const double* Q, bool use_lock,
               bool pass2, Ctl* ctl, double* hdiag, double* coef, int cap) {
   cgs_impl(c, s, n, t, Q, use_lock ? 1 : 0, pass2, ctl, -1, std::max(cap, 1), hdiag, coef);
