@@ -179,6 +179,11 @@ SE_API int se_kpm_moments(se_ctx* ctx, const se_csr* a, double lmin, double lmax
 SE_API int se_kpm_moments_probes(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m,
                                  int n_vec, int probe_kind, uint64_t seed, int first, int count,
                                  double* per_probe);
+/* Host probe generation: probes [first, first+count) of Rng(seed)'s stream (probe l = the next n
+ * values, rng.hpp:43-58 normal_vec / rademacher_vec), written row-major n x count (the layout
+ * the device block kernels read).  Host threads start their probes by MT19937-64 jump-ahead
+ * where that is exact; the values equal the serial draw bit for bit.  No GPU needed. */
+SE_API int se_probe_block(uint64_t seed, int probe_kind, int n, long first, int count, double* out);
 /* Jackson-damped curve from normalised moments (dos.hpp:112-131 + dos_finalize :54-60). */
 SE_API int se_kpm_curve(int m, const double* zeta, int n, double lmin, double lmax, int npts, double* x,
                  double* y, double* nev_est);

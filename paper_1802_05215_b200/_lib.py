@@ -84,6 +84,7 @@ SIGNATURES = {
                        C.c_int, C.c_int, _PD],
     "se_kpm_moments_probes": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                               C.c_uint64, C.c_int, C.c_int, _PD],
+    "se_probe_block": [C.c_uint64, C.c_int, C.c_int, C.c_long, C.c_int, _PD],
     "se_kpm_curve": [C.c_int, _PD, C.c_int, C.c_double, C.c_double, C.c_int, _PD, _PD, _PD],
     "se_kpm_dos": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
                    _PD, _PD, _PD],

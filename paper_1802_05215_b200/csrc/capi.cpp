@@ -538,16 +538,8 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
   if (per_probe) per_probe->assign((size_t)count * (m + 1), 0.0);
   if (count == 0) return;
   Rng rng(seed);
-  auto draw = [&](double* out, long len) {
-    if (probe_kind == SE_PROBE_GAUSSIAN)
-      rng.normal_fill(out, len);
-    else
-      rng.rademacher_fill(out, len);
-  };
-  {  // advance the stream past the probes owned by other ranks
-    Vec skip(n);
-    for (int l = 0; l < first; ++l) draw(skip.data(), n);
-  }
+  const bool gaussian = probe_kind == SE_PROBE_GAUSSIAN;
+  skip_probes(rng, gaussian, n, first);  // the probes owned by other ranks (jump-ahead)
   const size_t blk = (size_t)n * kBlock;
   double *V = dev_alloc<double>(blk), *X[3];
   for (double*& x : X) x = dev_alloc<double>(blk);
@@ -566,19 +558,9 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
   double* hbuf = hb[0];
   Vec hz((size_t)(m + 3) * kBlock);
   auto fill = [&](int b0, double* buf) {
-    // probe j = draws [j n, (j+1) n) of the one stream; written row-major (n x b) through a
-    // cache-blocked transpose
-    const int b = std::min(kBlock, count - b0);
-    std::vector<double> tmp((size_t)b * n);
-    for (int j = 0; j < b; ++j) draw(tmp.data() + (size_t)j * n, n);
-    constexpr int kRowBlk = 2048;
-    for (int i0 = 0; i0 < n; i0 += kRowBlk) {
-      const int i1 = std::min(n, i0 + kRowBlk);
-      for (int j = 0; j < b; ++j) {
-        const double* src = tmp.data() + (size_t)j * n;
-        for (int i = i0; i < i1; ++i) buf[(size_t)i * b + j] = src[i];
-      }
-    }
+    // probe j = the next n values of the one stream (probe order), probe-major; the device
+    // transposes the block to the row-major layout the kernels read
+    fill_probes(rng, gaussian, n, std::min(kBlock, count - b0), buf);
   };
   std::future<void> next = std::async(std::launch::async, fill, 0, hb[0]);
   try {
@@ -586,7 +568,8 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
       const int b = std::min(kBlock, count - b0);
       next.get();
       hbuf = hb[q & 1];
-      SE_CUDA(cudaMemcpyAsync(V, hbuf, sizeof(double) * (size_t)n * b, cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(double) * (size_t)n * b, cudaMemcpyHostToDevice, c.stream));
+      k::transpose_probes(c, X[2], V, n, b);
       ctx_sync(c);  // hbuf consumed; the other buffer is free
       if (b0 + kBlock < count) next = std::async(std::launch::async, fill, b0 + kBlock, hb[(q + 1) & 1]);
       if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
@@ -666,6 +649,25 @@ int se_kpm_moments_probes(se_ctx* ctx, const se_csr* a, double lmin, double lmax
     Vec z, pp;
     kpm_moments_impl(C(ctx), M(a), lmin, lmax, m, n_vec, probe_kind, seed, first, count, z, &pp);
     std::copy(pp.begin(), pp.end(), per_probe);
+  });
+}
+
+int se_probe_block(uint64_t seed, int probe_kind, int n, long first, int count, double* out) {
+  return guard([&] {
+    if (n < 1 || first < 0 || count < 0) fail(SE_EINVAL, "se_probe_block: bad sizes");
+    if (probe_kind != SE_PROBE_GAUSSIAN && probe_kind != SE_PROBE_RADEMACHER)
+      fail(SE_EINVAL, "se_probe_block: unknown probe kind");
+    Rng rng(seed);
+    const bool gaussian = probe_kind == SE_PROBE_GAUSSIAN;
+    skip_probes(rng, gaussian, n, first);
+    std::vector<double> blk;
+    for (int b0 = 0; b0 < count; b0 += 16) {  // the device's probe blocks
+      const int b = std::min(16, count - b0);
+      blk.resize((size_t)n * b);
+      fill_probes(rng, gaussian, n, b, blk.data());
+      for (int l = 0; l < b; ++l)
+        for (int i = 0; i < n; ++i) out[(size_t)i * count + b0 + l] = blk[(size_t)l * n + i];
+    }
   });
 }
 

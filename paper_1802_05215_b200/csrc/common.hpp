@@ -36,6 +36,7 @@ struct DevCsr {
   int* ci = nullptr;
   double* v = nullptr;
   int max_row_nnz = 0;
+  int tile32_nnz_max = 0;  // max nnz over aligned 32-row tiles (pipelined KPM kernel precondition)
   // nnz-balanced row partition (one part per SM) for the persistent filter kernel
   int* part = nullptr;
   int nparts = 0;

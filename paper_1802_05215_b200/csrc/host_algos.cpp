@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <thread>
 
 namespace se {
 
@@ -20,16 +21,58 @@ double Rng::normal() {
     spare_ok_ = false;
     return spare_;
   }
-  double u1;
-  do {
+  double u1 = uniform();
+  while (u1 <= 0.0) {
+    ++rejections_;
     u1 = uniform();
-  } while (u1 <= 0.0);
+  }
   const double u2 = uniform();
   const double rad = std::sqrt(-2.0 * std::log(u1));
   const double ang = 2.0 * kPi * u2;
   spare_ = rad * std::sin(ang);
   spare_ok_ = true;
   return rad * std::cos(ang);
+}
+
+void fill_probes(Rng& rng, bool gaussian, int n, int b, double* out) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const bool exact = !gaussian || (n % 2 == 0 && !rng.spare_pending());
+  const bool par = exact && b > 1 && hw > 1 && (long)n * b >= (1L << 21);
+  auto draw = [&](Rng& r, double* dst) {
+    if (gaussian)
+      r.normal_fill(dst, n);
+    else
+      r.rademacher_fill(dst, n);
+  };
+  if (par) {
+    // probe l starts l n draws after the block start (both kinds: exact by the test above)
+    std::vector<Rng> loc((size_t)b, rng);
+    std::vector<std::thread> th;
+    th.reserve((size_t)b);
+    for (int l = 0; l < b; ++l)
+      th.emplace_back([&, l] {
+        if (l) loc[(size_t)l].jump_draws(jump_poly((std::uint64_t)l * (std::uint64_t)n));
+        draw(loc[(size_t)l], out + (size_t)l * n);
+      });
+    for (auto& t : th) t.join();
+    long rej = 0;
+    for (const Rng& r : loc) rej += r.rejections() - rng.rejections();
+    if (rej == 0) {
+      rng = loc[(size_t)b - 1];
+      return;
+    }
+  }
+  for (int l = 0; l < b; ++l) draw(rng, out + (size_t)l * n);
+}
+
+void skip_probes(Rng& rng, bool gaussian, int n, long count) {
+  if (count <= 0) return;
+  if (!gaussian || (n % 2 == 0 && !rng.spare_pending())) {
+    rng.discard_draws((std::uint64_t)count * (std::uint64_t)n);
+    return;
+  }
+  std::vector<double> skip((size_t)n);
+  for (long l = 0; l < count; ++l) rng.normal_fill(skip.data(), n);
 }
 
 // ---- filters ------------------------------------------------------------------------------

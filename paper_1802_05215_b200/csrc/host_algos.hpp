@@ -3,10 +3,10 @@
 #pragma once
 
 #include <cstdint>
-#include <random>
 #include <vector>
 
 #include "common.hpp"
+#include "mt64.hpp"
 
 namespace se {
 
@@ -25,12 +25,26 @@ class Rng {
   void rademacher_fill(double* out, long n) {
     for (long i = 0; i < n; ++i) out[i] = rademacher();
   }
+  // advance the engine by j draws (jump-ahead for large j); the Box-Muller spare is untouched
+  void discard_draws(std::uint64_t j) { g_.discard(j); }
+  void jump_draws(const std::vector<std::uint64_t>& g) { g_.jump(g); }
+  bool spare_pending() const { return spare_ok_; }
+  long rejections() const { return rejections_; }
 
  private:
-  std::mt19937_64 g_;
+  Mt64 g_;
   bool spare_ok_ = false;
   double spare_ = 0.0;
+  long rejections_ = 0;  // u1 <= 0 redraws (shift the draw count; rng.hpp:36-41)
 };
+
+// Probes [0, b) of the stream (probe l = the next n draws: rademacher, or n normals), stored
+// probe-major (out[l n + i]); rng ends where the serial draw would.  Host threads start their
+// probes by jump-ahead when that is exact (Rademacher; Gaussian with n even and no pending
+// spare -- then every probe is exactly n draws); otherwise, or on a Box-Muller redraw, serial.
+void fill_probes(Rng& rng, bool gaussian, int n, int b, double* out);
+// Skip `count` probes of n values each (jump-ahead when exact, else serial draws).
+void skip_probes(Rng& rng, bool gaussian, int n, long count);
 
 // ---- filter_poly.hpp ----------------------------------------------------------------------
 struct PolyFilter {

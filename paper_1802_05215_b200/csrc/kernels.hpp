@@ -79,6 +79,8 @@ struct Scratch;
 size_t kpm_scratch_doubles(const Ctx& c, int n);
 // mode 1: first step (w1 = Ahat v; v.v, v.w1); 0: direct (t = 2 Ahat w1 - w0; v.t -> moment kmom);
 // 2: doubling (t = w_{k+1}; w_k.w_k -> slot 2 kmom, w_k.w_{k+1} -> slot 2 kmom + 1).
+// rm[i b + l] = pm[l n + i]: a probe-major host block to the row-major device layout
+void transpose_probes(Ctx& c, const double* pm, double* rm, int n, int b);
 void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const double* v,
               const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
               int kmom);

@@ -164,6 +164,9 @@ void build_partition(Ctx& c, DevCsr& a, const int* rp_host) {
     mx_nz = std::max(mx_nz, rp_host[part[q + 1]] - rp_host[part[q]]);
     mx_rows = std::max(mx_rows, part[q + 1] - part[q]);
   }
+  int t32 = 0;
+  for (long r0 = 0; r0 < a.n; r0 += 32) t32 = std::max(t32, rp_host[std::min<long>(r0 + 32, a.n)] - rp_host[r0]);
+  a.tile32_nnz_max = t32;
   a.part = dev_alloc<int>(P + 1);
   h2d(c, a.part, part.data(), sizeof(int) * (P + 1));
   a.nparts = P;
