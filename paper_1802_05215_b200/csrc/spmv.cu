@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -604,12 +605,13 @@ __global__ void __launch_bounds__(kKpmThreads, 4) k_kpm_direct(
 // the 4 rows' entries are contiguous -- are in flight while batch k's probe rows are gathered
 // and reduced.  Entries reach their row's lanes by warp shuffles.  Batches whose rows exceed U
 // entries (or 32 together) take the plain per-lane loop.  Same storage-order sums.
-template <int U>
+template <int U, int BC>
 __global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_stream(
     int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
-    int b, int mode, const double* __restrict__ v, const double* __restrict__ w0,
+    int b_rt, int mode, const double* __restrict__ v, const double* __restrict__ w0,
     const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
     double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
+  const int b = BC > 0 ? BC : b_rt;  // compile-time probe count for the common block widths
   const bool first = mode == kKpmFirst;
   const bool dbl = mode == kKpmDoubling;
   const int lane = threadIdx.x & 31, g = lane >> 3, l8 = lane & 7;
@@ -899,12 +901,21 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
   if (variant == 4 && b % 2 == 0) {
     static const int per_sm = [] {
       int v = 0;
-      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_stream<8>, kKpmThreads, 0));
+      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_stream<8, 0>, kKpmThreads, 0));
       return std::max(1, v);
     }();
     const int grid = std::max(1, std::min(c.num_sms * per_sm, (a.n + 31) / 32));
-    k_kpm_stream<8><<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc, d,
-                                                        s.buf, s.cnt, zeta_dev, kmom);
+    // U = entries gathered per row in one round: the matrix's row length (stencils: 5 or 7)
+    using KFn = decltype(&k_kpm_stream<8, 0>);
+    auto pick = [&](auto u) -> KFn {
+      constexpr int U = decltype(u)::value;
+      return b == 16 ? k_kpm_stream<U, 16> : b == 8 ? k_kpm_stream<U, 8> : k_kpm_stream<U, 0>;
+    };
+    const KFn kern = a.max_row_nnz <= 5 ? pick(std::integral_constant<int, 5>{})
+                     : a.max_row_nnz <= 7 ? pick(std::integral_constant<int, 7>{})
+                                          : pick(std::integral_constant<int, 8>{});
+    kern<<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc, d, s.buf,
+                                             s.cnt, zeta_dev, kmom);
     ++c.launches;
     SE_CUDA(cudaGetLastError());
     return;
