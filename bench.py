@@ -179,6 +179,17 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
                   C.byref(byt))
         out[tag] = (byt.value / (ms2.value * 1e-3) / 1e9, ms2.value * 1e-3 / nl.value, byt.value / nl.value)
         A.free()
+    # KPM block-step (K3) on BASELINE cfg3's matrix (160^3, 16 Rademacher probes per block,
+    # doubling recurrence: bytes Abytes + 24 n b per step)
+    A = api.DeviceCsr.laplacian([160, 160, 160], ctx)
+    b3 = api.SpectralBounds(0.0, 12.0)
+    api.kpm_moments(A, b3, 8, 16, seed=0)  # warm
+    _lib.call("se_ctx_filter_timing", ctx.handle, 1, None, None, None)
+    api.kpm_moments(A, b3, 80, 16, seed=0)
+    ms3, nl3, by3 = C.c_double(), C.c_long(), C.c_double()
+    _lib.call("se_ctx_filter_timing", ctx.handle, 0, C.byref(ms3), C.byref(nl3), C.byref(by3))
+    out["kpm"] = (by3.value / (ms3.value * 1e-3) / 1e9, ms3.value * 1e-3 / nl3.value, by3.value / nl3.value)
+    A.free()
     ctx.close()
     g, per, by = out["cgs"]
     roof = {"bound": "hbm", "kernel": "reorthogonalisation pass k_gemvt + k_gemvn (CGS, orth.hpp:19-32)",
@@ -191,7 +202,12 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
                                           "frac": round(out["hbm"][0] / peak, 4),
                                           "us_per_launch": round(out["hbm"][1] * 1e6, 2)},
                             "workload_64^3_L2_resident": {"achieved": round(out["workload"][0], 1),
-                                                          "us_per_launch": round(out["workload"][1] * 1e6, 2)}}}
+                                                          "us_per_launch": round(out["workload"][1] * 1e6, 2)}},
+            "kpm_block_step": {"kernel": "k_kpm_stream (16-probe block, doubling; dos.hpp:96-110)",
+                               "shape": "160^3 (BASELINE cfg3 matrix), b=16",
+                               "achieved": round(out["kpm"][0], 1), "frac": round(out["kpm"][0] / peak, 4),
+                               "us_per_step": round(out["kpm"][1] * 1e6, 2),
+                               "bytes_per_step": round(out["kpm"][2])}}
     return roof
 
 

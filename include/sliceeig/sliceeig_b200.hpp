@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -37,13 +38,21 @@ namespace detail {
 inline void ok(int rc) {
   if (rc != SE_OK) raise(rc);
 }
-// One context per host thread (one CUDA stream + library handles), on device SLICEEIG_DEVICE
-// or 0.
+// One context per host thread (one CUDA stream + library handles), on the device chosen by
+// set_thread_device() before the thread's first call, else SLICEEIG_DEVICE, else 0.
+inline int& thread_device() {
+  thread_local int d = -1;
+  return d;
+}
 struct ThreadCtx {
   se_ctx* c = nullptr;
   ThreadCtx() {
-    const char* d = std::getenv("SLICEEIG_DEVICE");
-    ok(se_ctx_create(d ? std::atoi(d) : 0, &c));
+    int dev = thread_device();
+    if (dev < 0) {
+      const char* d = std::getenv("SLICEEIG_DEVICE");
+      dev = d ? std::atoi(d) : 0;
+    }
+    ok(se_ctx_create(dev, &c));
   }
   ~ThreadCtx() { se_ctx_destroy(c); }
 };
@@ -52,6 +61,10 @@ inline se_ctx* ctx() {
   return t.c;
 }
 }  // namespace detail
+
+// B200 extension: pin the calling host thread to a GPU (before its first library call); the
+// CLI's slice pool uses it to spread slices over the GPUs of a node.
+inline void set_thread_device(int device) { detail::thread_device() = device; }
 
 // ---- vecops.hpp ----------------------------------------------------------------------------
 inline double dot(const Vec& x, const Vec& y) {
@@ -218,25 +231,52 @@ class CsrMatrix {
     matvec(x, y);
     return y;
   }
-  // Device copy (uploaded once per thread context, cached).
+  bool is_symmetric(double tol = 1e-14) const {
+    for (int i = 0; i < n_; ++i)
+      for (int k = rp_[i]; k < rp_[i + 1]; ++k) {
+        const double aij = v_[k], aji = coeff(ci_[k], i);
+        if (std::abs(aij - aji) > tol * std::max(1.0, std::abs(aij))) return false;
+      }
+    return true;
+  }
+  double one_norm() const {
+    Vec colsum(n_, 0.0);
+    for (int i = 0; i < n_; ++i)
+      for (int k = rp_[i]; k < rp_[i + 1]; ++k) colsum[ci_[k]] += std::abs(v_[k]);
+    double m = 0.0;
+    for (double s : colsum) m = std::max(m, s);
+    return m;
+  }
+  std::vector<Triplet> to_triplets() const {
+    std::vector<Triplet> t;
+    t.reserve(v_.size());
+    for (int i = 0; i < n_; ++i)
+      for (int k = rp_[i]; k < rp_[i + 1]; ++k) t.push_back({i, ci_[k], v_[k]});
+    return t;
+  }
+  // Device copy for the calling thread's context (uploaded once per context and cached; safe
+  // for concurrent use by several threads, each with its own context).
   se_csr* device() const {
     se_ctx* c = detail::ctx();
-    if (!dev_ || dev_ctx_ != c) {
-      se_csr* h = nullptr;
-      detail::ok(se_csr_upload(c, n_, rp_.data(), ci_.data(), v_.data(), &h));
-      dev_ = std::shared_ptr<se_csr>(h, [](se_csr* p) { se_csr_free(p); });
-      dev_ctx_ = c;
-    }
-    return dev_.get();
+    std::lock_guard<std::mutex> lk(dev_->mu);
+    for (const auto& e : dev_->copies)
+      if (e.first == c) return e.second.get();
+    se_csr* h = nullptr;
+    detail::ok(se_csr_upload(c, n_, rp_.data(), ci_.data(), v_.data(), &h));
+    dev_->copies.emplace_back(c, std::shared_ptr<se_csr>(h, [](se_csr* p) { se_csr_free(p); }));
+    return h;
   }
 
  private:
+  struct DevCopies {
+    std::mutex mu;
+    std::vector<std::pair<se_ctx*, std::shared_ptr<se_csr>>> copies;
+  };
   int n_ = 0;
   std::vector<int> rp_{0};
   std::vector<int> ci_;
   Vec v_;
-  mutable std::shared_ptr<se_csr> dev_;
-  mutable se_ctx* dev_ctx_ = nullptr;
+  std::shared_ptr<DevCopies> dev_ = std::make_shared<DevCopies>();
 };
 
 // ---- laplacian.hpp ------------------------------------------------------------------------------

@@ -65,9 +65,30 @@ def build(force: bool = False, verbose: bool = True) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli(force)
     if verbose:
         print(f"built {LIB}")
     return LIB
+
+
+CLI_SRC = os.path.join(ROOT, "tools", "sliceeig_b200_main.cpp")
+CLI = os.path.join(ROOT, "tools", "sliceeig_b200")
+
+
+def build_cli(force: bool = False) -> str:
+    """tools/sliceeig_b200: the C++ command-line caller (host code over the facade + the .so)."""
+    deps = [CLI_SRC, os.path.join(ROOT, "tools", "json_out.hpp"), LIB,
+            *[os.path.join(ROOT, "include", "sliceeig", f)
+              for f in os.listdir(os.path.join(ROOT, "include", "sliceeig"))]]
+    if not force and os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(d) for d in deps):
+        return CLI
+    cmd = ["g++", "-O2", "-std=c++17", "-pthread", f"-I{os.path.join(ROOT, 'include')}",
+           f"-I{os.path.join(CUDA, 'include')}", CLI_SRC, "-o", CLI, f"-L{PKG}", "-lsliceeig_cuda",
+           "-Wl,-rpath,$ORIGIN/../paper_1802_05215_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

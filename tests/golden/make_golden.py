@@ -184,10 +184,28 @@ def cfg5p():
     save("cfg5p", **out)
 
 
+def cli():
+    """`sliceeig solve --dims 30,30 --interval 0.4,0.6 --slices 4 [--solver tr]` with the CLI
+    defaults (KPM deg 60 x 40 Rademacher probes, sigma damping, tol 1e-8, seed 1234): the
+    reference's cmd_solve semantics (tools/sliceeig_main.cpp:464-619) via the harness."""
+    rp, ci, v = reflib.laplacian([30, 30])
+    out = {}
+    for solver in ("nr", "tr"):
+        r = reflib.solve(rp, ci, v, 0.4, 0.6, 4, solver=solver, jobs=4)
+        out[f"{solver}_bp"] = r["breakpoints"]
+        out[f"{solver}_est"] = r["est_counts"]
+        out[f"{solver}_bounds"] = [r["lmin"], r["lmax"]]
+        for i, s in enumerate(r["slices"]):
+            assert s["error"] is None
+            out[f"{solver}_slice{i}_vals"] = s["eigenvalues"]
+            out[f"{solver}_slice{i}_meta"] = [s["niter"], s["n_A_matvec"], s["degree"], int(s["hit_max_its"])]
+    save("cli", **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-solve", action="store_true")
-    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p")
+    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli")
     a = ap.parse_args()
     only = a.only.split(",")
     if "kats" in only:
@@ -200,3 +218,5 @@ if __name__ == "__main__":
         cfg4p()
     if "cfg5p" in only:
         cfg5p()
+    if "cli" in only:
+        cli()
