@@ -644,6 +644,7 @@ inline std::pair<double, double> rayleigh_and_residual(const CsrMatrix& a, const
 }
 
 namespace detail {
+inline EigenResults collect(se_results* r, int n);
 inline EigenResults cheb_lan(int solver, const CsrMatrix& a, const CsrMatrix* b,
                              const PolynomialFilter& f, double xi, double eta,
                              const SolverConfig& cfg, const DeflationSet* locked) {
@@ -662,13 +663,16 @@ inline EigenResults cheb_lan(int solver, const CsrMatrix& a, const CsrMatrix* b,
   se_results* r = nullptr;
   ok(se_cheb_lan(ctx(), a.device(), &s, xi, eta, &c, solver, nd, nd ? locked->u.data() : nullptr,
                  nd ? locked->values.data() : nullptr, 1, &r));
+  return collect(r, a.n());
+}
+inline EigenResults collect(se_results* r, int n) {
   std::unique_ptr<se_results, int (*)(se_results*)> guard(r, se_results_free);
   int nev = 0;
   ok(se_results_count(r, &nev));
   EigenResults out;
   out.eigenvalues.resize(nev);
   out.residuals.resize(nev);
-  out.vectors = DenseMat(a.n(), nev);
+  out.vectors = DenseMat(n, nev);
   ok(se_results_copy(r, out.eigenvalues.data(), out.residuals.data(), out.vectors.data()));
   se_counters cn{};
   int hit = 0;
@@ -691,6 +695,17 @@ inline EigenResults cheb_lan_tr(const CsrMatrix& a, const CsrMatrix* b, const Po
                                 double xi, double eta, const SolverConfig& cfg = {},
                                 const DeflationSet* locked = nullptr) {
   return detail::cheb_lan(1, a, b, f, xi, eta, cfg, locked);
+}
+// Filtered subspace iteration (eigensolvers.hpp:760-940), standard problems on the device.
+inline EigenResults cheb_si(const CsrMatrix& a, const CsrMatrix* b, const PolynomialFilter& f,
+                            double xi, double eta, int est_count, const SolverConfig& cfg = {}) {
+  if (b && b->n() != a.n()) throw std::invalid_argument("cheb_si: pencil size mismatch");
+  if (b) throw std::invalid_argument("cheb_si: generalized pencils are outside the device path");
+  const se_poly_filter s = detail::to_c(f);
+  const se_solver_cfg c{cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed};
+  se_results* r = nullptr;
+  detail::ok(se_cheb_si(detail::ctx(), a.device(), &s, xi, eta, est_count, &c, &r));
+  return detail::collect(r, a.n());
 }
 
 }  // namespace sliceeig

@@ -229,6 +229,11 @@ SE_API int se_dense_sym_eig(int m, const double* a, int want, int size_guard, do
 SE_API int se_cheb_lan(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi, double eta,
                 const se_solver_cfg* cfg, int solver, int ndefl, const double* defl_u,
                 const double* defl_vals, int want_vectors, se_results** out);
+/* cheb_si (eigensolvers.hpp:760-940): filtered subspace iteration on a block of
+ * ceil(1.3 est_count) + 8 vectors (filter sweep on the multi-vector kernel, CGS2 re-orthonormal-
+ * isation, Rayleigh-Ritz by DGEMM + syevd); SE_ENUMERIC when the block saturates above the bar. */
+SE_API int se_cheb_si(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi, double eta,
+                      int est_count, const se_solver_cfg* cfg, se_results** out);
 SE_API int se_results_count(const se_results* r, int* nev);
 /* eigenvalues/residuals (nev each, ascending by eigenvalue), vectors (n x nev, may be NULL). */
 SE_API int se_results_copy(const se_results* r, double* eigenvalues, double* residuals, double* vectors);

@@ -437,8 +437,9 @@ void* ref_cheb_lan(int n, const int* rp, const int* ci, const double* v, int sol
     cfg.est_count = est_count;
     cfg.seed = (unsigned long)seed;
     rs->degrees.push_back(f.k);
-    rs->slices.push_back(solver == 1 ? cheb_lan_tr(a, nullptr, f, xi, eta, cfg)
-                                     : cheb_lan_nr(a, nullptr, f, xi, eta, cfg));
+    rs->slices.push_back(solver == 2   ? cheb_si(a, nullptr, f, xi, eta, est_count, cfg)
+                         : solver == 1 ? cheb_lan_tr(a, nullptr, f, xi, eta, cfg)
+                                       : cheb_lan_nr(a, nullptr, f, xi, eta, cfg));
   });
   if (rc != 0) {
     delete rs;
@@ -526,7 +527,8 @@ void* ref_solve(int n, const int* rp, const int* ci, const double* v, double xi,
           po.damping = damping_of(damping);
           PolynomialFilter f = find_pol(t.lo, t.hi, bounds, po);
           rs->degrees[i] = f.k;
-          EigenResults r = solver == 1 ? cheb_lan_tr(a, nullptr, f, t.lo, t.hi, cfg)
+          EigenResults r = solver == 2   ? cheb_si(a, nullptr, f, t.lo, t.hi, cfg.est_count, cfg)
+                           : solver == 1 ? cheb_lan_tr(a, nullptr, f, t.lo, t.hi, cfg)
                                        : cheb_lan_nr(a, nullptr, f, t.lo, t.hi, cfg);
           // trim_to_slice (sliceeig_main.cpp:422-442)
           EigenResults out;

@@ -24,7 +24,7 @@ _PI = C.POINTER(C.c_int)
 _PL = C.POINTER(C.c_long)
 
 DAMPING = {"none": 0, "sigma": 1, "jackson": 2}
-SOLVER = {"nr": 0, "tr": 1}
+SOLVER = {"nr": 0, "tr": 1, "si": 2}
 PROBES = {"rademacher": 0, "normal": 1}
 
 

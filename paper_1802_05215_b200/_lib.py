@@ -98,6 +98,8 @@ SIGNATURES = {
     "se_sym_tridiag_eig": [C.c_int, _PD, _PD, C.c_int, _PD, _PD],
     "se_arrow_tridiag": [C.c_int, _PD, _PD, C.c_double, _PD, _PD],
     "se_dense_sym_eig": [C.c_int, _PD, C.c_int, C.c_int, _PD, _PD],
+    "se_cheb_si": [_VP, _VP, C.POINTER(SePolyFilter), C.c_double, C.c_double, C.c_int,
+                   C.POINTER(SeSolverCfg), C.POINTER(_VP)],
     "se_cheb_lan": [_VP, _VP, C.POINTER(SePolyFilter), C.c_double, C.c_double,
                     C.POINTER(SeSolverCfg), C.c_int, C.c_int, _PD, _PD, C.c_int, C.POINTER(_VP)],
     "se_results_count": [_VP, _PI],

@@ -660,6 +660,10 @@ def _cheb_lan(solver: int, a, b, f: PolynomialFilter, xi, eta, cfg: SolverConfig
     call("se_cheb_lan", d.ctx.handle, d.handle, C.byref(s), xi, eta, C.byref(c), solver, nd,
          du.ctypes.data_as(_PD) if nd else None, _pd(dv) if nd else None, int(want_vectors),
          C.byref(h))
+    return _collect_results(h, d, want_vectors)
+
+
+def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
     try:
         nev = C.c_int()
         call("se_results_count", h, C.byref(nev))
@@ -678,6 +682,22 @@ def _cheb_lan(solver: int, a, b, f: PolynomialFilter, xi, eta, cfg: SolverConfig
                         cn.t_orth, cn.t_sv, cn.t_total)
     return EigenResults(vals, vecs.T if vecs is not None else (np.zeros((d.n, 0)) if want_vectors else None),
                         res, niter.value, counters, bool(hit.value))
+
+
+def cheb_si(a, b, f: PolynomialFilter, xi: float, eta: float, est_count: int,
+            cfg: SolverConfig = SolverConfig(), want_vectors: bool = True) -> EigenResults:
+    """Filtered subspace iteration on a block of ceil(1.3 est_count) + 8 vectors
+    (eigensolvers.hpp:760-940); raises RuntimeError when the block saturates above the bar."""
+    d = _dev(a)
+    if b is not None:
+        if getattr(b, "n", d.n) != d.n:
+            raise ValueError("cheb_si: pencil size mismatch")
+        raise ValueError("cheb_si: generalized pencils (b != nullptr) are outside the device path")
+    s, _keep = f._c()
+    c = _lib.SeSolverCfg(cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed)
+    h = C.c_void_p()
+    call("se_cheb_si", d.ctx.handle, d.handle, C.byref(s), xi, eta, int(est_count), C.byref(c), C.byref(h))
+    return _collect_results(h, d, want_vectors)
 
 
 def cheb_lan_nr(a, b, f: PolynomialFilter, xi: float, eta: float, cfg: SolverConfig = SolverConfig(),

@@ -460,7 +460,10 @@ int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nve
     double* dv = dev_alloc<double>((size_t)m.n * nvec);
     double* dout = dev_alloc<double>((size_t)m.n * nvec);
     SE_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, c.stream));
-    apply_filter_dev(c, m, to_op(pf), nvec, dv, dout);
+    if (nvec > 1)
+      apply_filter_block(c, m, to_op(pf), nvec, dv, dout);  // 8 columns per fused launch
+    else
+      apply_filter_dev(c, m, to_op(pf), nvec, dv, dout);
     SE_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c.stream));
     ctx_sync(c);
     dev_free(dv);
@@ -886,6 +889,23 @@ int se_cheb_lan(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi
     auto res = std::make_unique<se_results>();
     res->device = c.device;
     res->r = cheb_lan(c, M(a), pf, xi, eta, sc, solver == 1, ndefl, defl_u, defl_vals, who);
+    *out = res.release();
+  });
+}
+
+int se_cheb_si(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi, double eta,
+               int est_count, const se_solver_cfg* cfg, se_results** out) {
+  return guard([&] {
+    *out = nullptr;
+    Ctx& c = C(ctx);
+    if (!(eta > xi)) fail(SE_EINVAL, "cheb_si: degenerate interval");
+    if (est_count < 0) fail(SE_EINVAL, "cheb_si: negative est_count");
+    se_solver_cfg rc = *cfg;  // est_count = max(cfg.est_count, est_count) (eigensolvers.hpp:770-772)
+    rc.est_count = std::max(cfg->est_count, est_count);
+    const SolverCfg sc = resolve_config(&rc, "cheb_si");
+    auto res = std::make_unique<se_results>();
+    res->device = c.device;
+    res->r = cheb_si(c, M(a), to_filter(f), xi, eta, est_count, sc);
     *out = res.release();
   });
 }

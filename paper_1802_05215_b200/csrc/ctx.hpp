@@ -38,10 +38,11 @@ struct Ctx {
 // Route this context's launches to the high-priority stream for a scope (projected eigensolves,
 // stagnation checks, Ritz extraction): with 8 slices sharing a GPU these short, synchronising
 // phases otherwise queue behind other slices' bandwidth-bound reorthogonalisation kernels.
-struct HiPrio {
+struct HiPrio {  // nests: restores whichever stream was current
   Ctx& c;
-  explicit HiPrio(Ctx& cc) : c(cc) { c.stream = c.hstream; }
-  ~HiPrio() { c.stream = c.bulk; }
+  cudaStream_t prev;
+  explicit HiPrio(Ctx& cc) : c(cc), prev(cc.stream) { c.stream = c.hstream; }
+  ~HiPrio() { c.stream = prev; }
 };
 
 // Wait for the work queued on the context's current stream (the host thread blocks instead of

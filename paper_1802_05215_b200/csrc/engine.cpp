@@ -990,6 +990,251 @@ std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter&
   return thick_restart ? run_tr(s) : run_nr(s);
 }
 
+// ---- filtered subspace iteration (cheb_si, eigensolvers.hpp:760-940; standard problem) ---------
+// Filter nvec columns (ld n) through the multi-vector fused kernel, 8 columns per launch:
+// out_j = sum_k mu_k T_k(Ahat) v_j (apply_pol, filter_poly.hpp:256-277, column by column).
+void apply_filter_block(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const double* v, double* out) {
+  const int n = a.n;
+  if (op.k < 2) {
+    apply_filter_dev(c, a, op, nvec, v, out);
+    return;
+  }
+  double* buf = dev_alloc<double>((size_t)n * 24);
+  try {
+    for (int c0 = 0; c0 < nvec; c0 += 8) {
+      const int nv = std::min(8, nvec - c0);
+      for (int j = 1; j <= op.k; ++j) {
+        k::MultiArgs m{};
+        m.nv = nv;
+        m.c = op.c;
+        m.invd = op.invd;
+        for (int q = 0; q < nv; ++q) {
+          const double* vq = v + (size_t)(c0 + q) * n;
+          double* B[3] = {buf + (size_t)(3 * q) * n, buf + (size_t)(3 * q + 1) * n, buf + (size_t)(3 * q + 2) * n};
+          m.x[q] = j == 1 ? vq : B[(j - 2) % 3];
+          m.prev[q] = j == 2 ? vq : B[j % 3];
+          m.y[q] = B[(j - 1) % 3];
+          m.out[q] = out + (size_t)(c0 + q) * n;
+          m.mu0[q] = op.mu[0];
+          m.muj[q] = op.mu[j];
+          m.first[q] = j == 1;
+        }
+        k::spmv_cheb_multi(c, a, m);
+      }
+    }
+    ctx_sync(c);
+  } catch (...) {
+    ctx_sync(c);
+    dev_free(buf);
+    throw;
+  }
+  dev_free(buf);
+}
+
+namespace {
+// cgs2_orthogonalize (orth.hpp:39-61) of t against the first k columns of Q, in place:
+// returns the final norm (t normalised) or 0.0 on breakdown (t untouched beyond the passes).
+struct Orth {
+  Ctx& c;
+  k::Scratch s;
+  Ctl* ctl = nullptr;
+  double* coef = nullptr;
+  int n, cap;
+  Orth(Ctx& cc, int n_, int cap_) : c(cc), n(n_), cap(cap_) {
+    s.cap = k::cgs_scratch_doubles(c, n, cap);
+    s.ncnt = k::cgs_counter_slots(n, cap);
+    s.buf = dev_alloc<double>(s.cap);
+    s.cnt = dev_alloc<unsigned>(s.ncnt);
+    ctl = dev_alloc<Ctl>(1);
+    coef = dev_alloc<double>(std::max(cap, 1));
+    SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
+    ctx_sync(c);
+  }
+  ~Orth() {
+    cudaStreamSynchronize(c.stream);
+    for (void* p : {(void*)s.buf, (void*)s.cnt, (void*)ctl, (void*)coef}) dev_free(p);
+  }
+  double run(double* t, const double* Q, int kq) {
+    Ctl h{};
+    h.i = kq - 1;
+    h2d(c, ctl, &h, sizeof(Ctl));
+    k::norm_before(c, s, n, t, ctl);
+    Ctl g;
+    d2h(c, &g, ctl, sizeof(Ctl));
+    const double initial = g.before;
+    if (initial == 0.0) return 0.0;
+    double after = initial;
+    if (kq > 0) {
+      k::cgs_pass(c, s, n, t, Q, false, false, ctl, nullptr, coef, cap);
+      k::cgs_pass(c, s, n, t, Q, false, true, ctl, nullptr, coef, cap);
+      d2h(c, &g, ctl, sizeof(Ctl));
+      after = g.after;
+    }
+    if (after <= 1e-14 * initial) return 0.0;  // kBreakdownTol (orth.hpp:14)
+    k::scale(c, n, 1.0 / after, t);
+    return after;
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<SliceResult> cheb_si(Ctx& c, const DevCsr& a, const PolyFilter& f, double xi,
+                                     double eta, int est_count, const SolverCfg& cfg) {
+  if (!(eta > xi)) fail(SE_EINVAL, "cheb_si: degenerate interval");
+  if (est_count < 0) fail(SE_EINVAL, "cheb_si: negative est_count");
+  if (f.k < 1 || (int)f.mu.size() != f.k + 1) fail(SE_EINVAL, "cheb_si: malformed filter");
+  HiPrio hp(c);
+  const auto t0 = std::chrono::steady_clock::now();
+  const int n = a.n;
+  const int q = std::min(n, (int)std::ceil(1.3 * est_count) + 8);
+  const double bar_eff = f.bar * (1.0 - 1e-4);
+  StepOp op;
+  op.plain = false;
+  op.k = f.k;
+  op.mu = f.mu;
+  op.c = f.c;
+  op.invd = 1.0 / f.d;
+  Rng rng(cfg.seed);
+  auto res = std::make_unique<SliceResult>();
+  res->n = n;
+  se_counters& cnt = res->counters;
+  DevMat Y, T, AY;
+  devmat_reserve(c, Y, n, q, false);
+  devmat_reserve(c, T, n, q, false);
+  devmat_reserve(c, AY, n, q, false);
+  Orth orth(c, n, q);
+  DevEig eig(c);
+  CandBuf cand(c);
+  auto cleanup = [&] {
+    ctx_sync(c);
+    devmat_free(Y);
+    devmat_free(T);
+    devmat_free(AY);
+  };
+  auto secs = [](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+  };
+  auto fresh = [&](double* dst) {  // rng.normal_vec(n) -> device column
+    std::vector<double> h((size_t)n);
+    rng.normal_fill(h.data(), n);
+    h2d(c, dst, h.data(), sizeof(double) * n);
+  };
+  try {
+    // random orthonormal start block (eigensolvers.hpp:818-823)
+    for (int cols = 0; cols < q;) {
+      fresh(Y.col(cols));
+      if (orth.run(Y.col(cols), Y.p, cols) > 0.0) ++cols;
+    }
+    const double slo = 10.0 * cfg.res_tol * std::max(1.0, std::abs(xi));
+    const double shi = 10.0 * cfg.res_tol * std::max(1.0, std::abs(eta));
+    int saturated = 0, idle = 0;
+    long cycle = 0;
+    Vec lam, stats;
+    std::vector<double> G((size_t)q * q);
+    while (true) {
+      ++cycle;
+      // filter sweep (k A-products per column), then CGS2 re-orthonormalisation in column order
+      auto tm = std::chrono::steady_clock::now();
+      apply_filter_block(c, a, op, q, Y.p, T.p);
+      cnt.n_A_matvec += (long)f.k * q;
+      cnt.t_mv += secs(tm);
+      auto to = std::chrono::steady_clock::now();
+      for (int j = 0; j < q; ++j)
+        while (orth.run(T.col(j), T.p, j) == 0.0) fresh(T.col(j));  // collapsed: fresh direction
+      ctx_sync(c);
+      cnt.t_orth += secs(to);
+      // Rayleigh-Ritz: AY = A T, gram(i, j) = <AY_j, T_i> (i <= j, mirrored), eig, Y = T V
+      tm = std::chrono::steady_clock::now();
+      for (int j0 = 0; j0 < q; j0 += 65535) {
+        k::ChebArgs pa;
+        pa.x = T.col(j0);
+        pa.y = AY.col(j0);
+        pa.ncols = std::min(65535, q - j0);
+        k::spmv_cheb(c, a, k::kPlain, pa);
+      }
+      cnt.n_A_matvec += q;
+      const double one = 1.0, zero = 0.0;
+      double* dG = dev_alloc<double>((size_t)q * q);
+      if (cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, q, q, n, &one, T.p, n, AY.p, n, &zero, dG, q) !=
+          CUBLAS_STATUS_SUCCESS) {
+        dev_free(dG);
+        fail(SE_ECUDA, "cublasDgemm (Rayleigh-Ritz gram) failed");
+      }
+      ++c.launches;
+      d2h(c, G.data(), dG, sizeof(double) * (size_t)q * q);
+      dev_free(dG);
+      for (int j = 0; j < q; ++j)
+        for (int i = j + 1; i < q; ++i) G[(size_t)j * q + i] = G[(size_t)i * q + j];  // lower := upper
+      const double* V = eig.solve(q, G, lam);
+      if (cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, q, q, &one, T.p, n, V, q, &zero, Y.p, n) !=
+          CUBLAS_STATUS_SUCCESS)
+        fail(SE_ECUDA, "cublasDgemm (Ritz block) failed");
+      ++c.launches;
+      cnt.t_mv += secs(tm);
+      // candidate pass (eigensolvers.hpp:857-896): Ritz values inside the slack-widened slice
+      std::vector<int> sel;
+      for (int j = 0; j < q; ++j)
+        if (!(lam[j] < xi - slo || lam[j] > eta + shi)) sel.push_back(j);
+      struct Pair {
+        double lambda, residual, scale;
+        int col;
+      };
+      std::vector<Pair> inside;
+      bool all_good = true;
+      if (!sel.empty()) {
+        std::vector<double> Vs((size_t)q * sel.size());
+        std::vector<double> Vh((size_t)q * q);
+        d2h(c, Vh.data(), V, sizeof(double) * (size_t)q * q);
+        for (size_t s2 = 0; s2 < sel.size(); ++s2)
+          std::copy(Vh.begin() + (size_t)sel[s2] * q, Vh.begin() + (size_t)(sel[s2] + 1) * q,
+                    Vs.begin() + s2 * q);
+        double* dV = dev_alloc<double>(Vs.size());
+        h2d(c, dV, Vs.data(), sizeof(double) * Vs.size());
+        cand.eval(a, T.p, q, dV, q, (int)sel.size(), stats);
+        dev_free(dV);
+        cnt.n_A_matvec += (long)sel.size();
+        for (size_t s2 = 0; s2 < sel.size(); ++s2) {
+          const double l = stats[3 * s2], r = stats[3 * s2 + 1], uu = stats[3 * s2 + 2];
+          if (!(uu > 0.0)) continue;
+          if (r > cfg.res_tol * std::max(1.0, std::abs(l))) all_good = false;
+          inside.push_back({l, r, 1.0 / std::sqrt(uu), (int)s2});
+        }
+      }
+      // a block whose every Ritz value maps above the bar cannot bracket the slice
+      int above = 0;
+      for (int j = 0; j < q; ++j) {
+        const double t = std::clamp((lam[j] - f.c) / f.d, -1.0, 1.0);
+        if (eval_pol(f.mu.data(), f.k, t) >= bar_eff) ++above;
+      }
+      saturated = above == q ? saturated + 1 : 0;
+      if (saturated >= 3)
+        fail(SE_ENUMERIC, "cheb_si: subspace saturated above the filter bar; raise est_count");
+      idle = inside.empty() ? idle + 1 : 0;
+      const bool done = (!inside.empty() && all_good) || idle >= 6;
+      const bool budget = cycle >= cfg.max_its;
+      if (done || budget) {
+        std::sort(inside.begin(), inside.end(), [](const Pair& x, const Pair& y) { return x.lambda < y.lambda; });
+        const int nev = (int)inside.size();
+        devmat_reserve(c, res->vectors, n, std::max(nev, 1), false);
+        for (int i = 0; i < nev; ++i) {
+          k::scale_copy(c, n, inside[i].scale, cand.U.col(inside[i].col), res->vectors.col(i));
+          res->eigenvalues.push_back(inside[i].lambda);
+          res->residuals.push_back(inside[i].residual);
+        }
+        ctx_sync(c);
+        res->niter = cycle;
+        res->hit_max_its = budget && !done;
+        cnt.t_total += secs(t0);
+        cleanup();
+        return res;
+      }
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+}
+
 }  // namespace se
 
 namespace se {

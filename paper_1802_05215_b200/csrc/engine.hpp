@@ -43,6 +43,10 @@ struct SliceResult {
 void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const double* v,
                       double* out);
 
+// The same on the multi-vector kernel (8 columns per launch; bitwise the per-column result).
+void apply_filter_block(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const double* v,
+                        double* out);
+
 // Lanczos-family drivers.
 struct LanczosRun {
   Vec alpha, beta;
@@ -62,6 +66,11 @@ std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter&
                                       double eta, const SolverCfg& cfg, bool thick_restart,
                                       int ndefl, const double* defl_u, const double* defl_vals,
                                       const char* who);
+
+// Filtered subspace iteration (cheb_si, eigensolvers.hpp:760-940) on a block of
+// ceil(1.3 est_count) + 8 vectors; standard problems.
+std::unique_ptr<SliceResult> cheb_si(Ctx& c, const DevCsr& a, const PolyFilter& f, double xi,
+                                     double eta, int est_count, const SolverCfg& cfg);
 
 }  // namespace se
 

@@ -190,7 +190,7 @@ def cli():
     reference's cmd_solve semantics (tools/sliceeig_main.cpp:464-619) via the harness."""
     rp, ci, v = reflib.laplacian([30, 30])
     out = {}
-    for solver in ("nr", "tr"):
+    for solver in ("nr", "tr", "si"):
         r = reflib.solve(rp, ci, v, 0.4, 0.6, 4, solver=solver, jobs=4)
         out[f"{solver}_bp"] = r["breakpoints"]
         out[f"{solver}_est"] = r["est_counts"]
@@ -199,6 +199,15 @@ def cli():
             assert s["error"] is None
             out[f"{solver}_slice{i}_vals"] = s["eigenvalues"]
             out[f"{solver}_slice{i}_meta"] = [s["niter"], s["n_A_matvec"], s["degree"], int(s["hit_max_its"])]
+    # cheb_si directly (eigensolvers.hpp:760-940) on a 60x60 window with the bounds fixed
+    rp6, ci6, v6 = reflib.laplacian([60, 60])
+    b6 = reflib.lan_tr_bounds(rp6, ci6, v6, 1e-4, 60, 40, 1234)
+    for q, (lo, hi, est) in enumerate([(0.5, 0.6, 20), (1.0, 1.1, 25)]):
+        r = reflib.cheb_lan(rp6, ci6, v6, "si", lo, hi, b6[0], b6[1], est_count=est, seed=1234)
+        out[f"si60_{q}_vals"] = r["eigenvalues"]
+        out[f"si60_{q}_res"] = r["residuals"]
+        out[f"si60_{q}_meta"] = [r["niter"], r["n_A_matvec"], r["degree"], int(r["hit_max_its"]), lo, hi, est,
+                                 b6[0], b6[1]]
     save("cli", **out)
 
 

@@ -52,6 +52,21 @@ def test_apply_pol_bitwise(gpu_ctx, dims, slice_, damping):
     assert np.array_equal(out, ref), np.max(np.abs(out - ref))
 
 
+def test_apply_pol_block_bitwise(gpu_ctx):
+    """Block application (multi-vector fused kernel, 8 columns per launch; used by cheb_si):
+    every column bitwise the reference's apply_pol (9 columns: a full group of 8 plus a tail)."""
+    api = _api()
+    a = api.gen_laplacian([40, 40])
+    f = api.find_pol(0.5, 0.6, api.SpectralBounds(0.0, 8.0))
+    X = clib.rng_vectors(5, "normal", a.n, 9)
+    cnt = api.Counters()
+    out = api.apply_pol(f, a, X, cnt)
+    assert cnt.n_A_matvec == 9 * f.k
+    for j in range(9):
+        ref = clib.apply_pol(a.row_ptr, a.col_idx, a.vals, f.mu, f.c, f.d, X[j])
+        assert np.array_equal(out[j], ref), (j, np.max(np.abs(out[j] - ref)))
+
+
 def test_kpm_moments_match_oracle(gpu_ctx):
     api = _api()
     a = api.gen_laplacian([100, 100])

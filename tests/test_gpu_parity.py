@@ -332,3 +332,39 @@ def test_fused_cgs2_opt_in_matches_reference(gpu_ctx):
     out = subprocess.run([sys.executable, os.path.join(here, "_fused_cgs_case.py")], env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "fused-ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_cheb_si_matches_reference(gpu_ctx, golden, case):
+    """cheb_si (eigensolvers.hpp:760-940) on 60x60 windows against the reference's own run:
+    identical count, eigenvalues within 1e-10 relative, residuals under tol, converged."""
+    api = _api()
+    g = golden("cli")
+    meta = g[f"si60_{case}_meta"]
+    lo, hi, est, lmin, lmax = meta[4], meta[5], int(meta[6]), meta[7], meta[8]
+    a = api.gen_laplacian([60, 60])
+    f = api.find_pol(lo, hi, api.SpectralBounds(lmin, lmax))
+    assert f.k == int(meta[2])
+    r = api.cheb_si(a, None, f, lo, hi, est, api.SolverConfig(seed=1234))
+    ref = g[f"si60_{case}_vals"]
+    assert not r.hit_max_its
+    assert r.eigenvalues.size == ref.size
+    assert np.all(np.abs(r.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+    assert np.all(r.residuals <= 1e-8 * np.maximum(1.0, np.abs(r.eigenvalues)))
+    ev = api.laplacian_analytic_eigs([60, 60])
+    assert np.all(np.min(np.abs(r.eigenvalues[:, None] - ev[None, :]), axis=1) <= 1e-9)
+    for j in range(r.eigenvalues.size):  # returned vectors: unit norm, residual as reported
+        lam, res = api.rayleigh_and_residual(a, None, r.vectors[:, j])
+        assert abs(lam - r.eigenvalues[j]) <= 1e-10 * max(1.0, abs(lam))
+        assert abs(np.linalg.norm(r.vectors[:, j]) - 1.0) <= 1e-10
+
+
+def test_cheb_si_saturation_raises(gpu_ctx):
+    """A block far too small for the slice saturates above the bar: runtime_error
+    (eigensolvers.hpp:903-909)."""
+    api = _api()
+    a = api.gen_laplacian([40, 40])
+    b = api.lan_tr_bounds(a, 1e-4, 60, 40, 1234)
+    f = api.find_pol(0.5, 1.5, b)
+    with pytest.raises(RuntimeError):
+        api.cheb_si(a, None, f, 0.5, 1.5, 1, api.SolverConfig(est_count=1, seed=1))

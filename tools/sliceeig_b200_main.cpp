@@ -6,9 +6,9 @@
 // (dos_curve.csv, slices.json, filter_curve.csv, slice_<i>.json, report.json, vectors_<i>.bin).
 // Exit status is 0 only when every requested slice converged.
 //
-// In scope: polynomial filters with the nr / tr drivers, KPM or Lanczos densities, standard
-// problems.  Rational filters, subspace iteration and B-pencils are reported as errors (nonzero
-// exit), as the reference does for invalid combinations.  B200 extension: --gpus N spreads the
+// In scope: polynomial filters with the nr / tr / si drivers, KPM or Lanczos densities, standard
+// problems.  Rational filters and B-pencils are reported as errors (nonzero exit), as the
+// reference does for invalid combinations.  B200 extension: --gpus N spreads the
 // slice pool over N GPUs of the node (slice i on GPU i mod N).
 #include <algorithm>
 #include <atomic>
@@ -402,7 +402,7 @@ EigenResults run_slice(const CsrMatrix& a, const SpectralBounds& bounds, const T
   const PolynomialFilter f = find_pol(t.lo, t.hi, bounds, po);
   if (m.solver == "nr") return cheb_lan_nr(a, nullptr, f, t.lo, t.hi, cfg);
   if (m.solver == "tr") return cheb_lan_tr(a, nullptr, f, t.lo, t.hi, cfg);
-  throw std::invalid_argument("filtered subspace iteration (--solver si) is outside the B200 build");
+  return cheb_si(a, nullptr, f, t.lo, t.hi, cfg.est_count, cfg);
 }
 
 // an eigenvalue within delta above an interior breakpoint belongs to the slice below
@@ -459,8 +459,6 @@ int cmd_solve(const Manifest& m) {
   const auto t0 = std::chrono::steady_clock::now();
   m.require_interval();
   require_poly(m);
-  if (m.solver == "si")
-    throw std::invalid_argument("filtered subspace iteration (--solver si) is outside the B200 build");
   const double xi = m.interval[0], eta = m.interval[1];
   const CsrMatrix a = load_problem(m);
   const double t_load = since(t0);
@@ -619,7 +617,7 @@ void usage(std::ostream& os) {
         "  input:  --dims d1[,d2[,d3]] | --matrix FILE.mtx\n"
         "  dos:    --method kpm|lanczos --deg M --vecs N --npts P\n"
         "  output: --out DIR --format json|csv\n"
-        "  solve:  --interval LO,HI --slices S --damping sigma|jackson|none --solver nr|tr\n"
+        "  solve:  --interval LO,HI --slices S --damping sigma|jackson|none --solver nr|tr|si\n"
         "          --tol T --seed S --jobs J --gpus G --vectors\n";
 }
 
