@@ -49,6 +49,7 @@ int guard(F&& f) {
 Ctx& C(se_ctx* c) {
   if (!c || !c->c) fail(SE_EINVAL, "null se_ctx");
   SE_CUDA(cudaSetDevice(c->c->device));
+  set_current_ctx(c->c);  // the thread's stream-ordered allocations go to this context
   return *c->c;
 }
 const DevCsr& M(const se_csr* a) {
@@ -297,9 +298,9 @@ int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, co
     a.device = c.device;
     a.n = n;
     a.nnz = row_ptr[n];
-    a.rp = dev_alloc<int>(n + 1);
-    a.ci = dev_alloc<int>(a.nnz);
-    a.v = dev_alloc<double>(a.nnz);
+    a.rp = dev_alloc_shared<int>(n + 1);
+    a.ci = dev_alloc_shared<int>(a.nnz);
+    a.v = dev_alloc_shared<double>(a.nnz);
     int mx = 0;
     for (int i = 0; i < n; ++i) mx = std::max(mx, row_ptr[i + 1] - row_ptr[i]);
     a.max_row_nnz = mx;
@@ -371,10 +372,10 @@ int se_csr_free(se_csr* a) {
   return guard([&] {
     if (!a) return;
     cudaSetDevice(a->a.device);
-    dev_free(a->a.rp);
-    dev_free(a->a.part);
-    dev_free(a->a.ci);
-    dev_free(a->a.v);
+    dev_free_shared(a->a.rp);
+    dev_free_shared(a->a.part);
+    dev_free_shared(a->a.ci);
+    dev_free_shared(a->a.v);
     delete a;
   });
 }
@@ -944,7 +945,7 @@ int se_results_free(se_results* r) {
   return guard([&] {
     if (!r) return;
     cudaSetDevice(r->device);
-    devmat_free(r->r->vectors);
+    devmat_free(r->r->vectors);  // stream-ordered if this thread's context is on the device
     delete r;
   });
 }

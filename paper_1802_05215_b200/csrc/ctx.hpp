@@ -30,6 +30,7 @@ struct Ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evsync = nullptr;
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // profiling of host-driven phases
+  cudaEvent_t evx = nullptr;                    // cross-stream ordering of allocations
   double prof_kernel_ms = 0.0;
   void* pinned = nullptr;  // staging for host<->device copies (pageable copies serialise
   size_t pinned_bytes = 0; // across the slice threads sharing a GPU)  // blocking-sync event: host waits sleep instead of spinning
@@ -56,21 +57,28 @@ void d2h(Ctx& c, void* dst, const void* src, size_t bytes);
 Ctx* ctx_create(int device);
 void ctx_destroy(Ctx* c);
 
-// RAII device allocation on a context's device.
+// ---- device memory -------------------------------------------------------------------------
+// dev_alloc / dev_free are stream-ordered (cudaMallocAsync / cudaFreeAsync from the device's
+// memory pool, kept resident) on the calling thread's current context, ordered against both of
+// its streams with events: no device-wide synchronisation, so one slice thread's allocations do
+// not stall the other slices sharing the GPU (cudaFree waits for the whole device).  Without a
+// current context (or inside a stream capture) they fall back to cudaMalloc / cudaFree.
+// Memory several contexts read (a CSR matrix) comes from dev_alloc_shared / dev_free_shared.
+void set_current_ctx(Ctx* c);
+Ctx* current_ctx();
+void* dev_alloc_bytes(size_t bytes);
+void dev_free(void* p);
+void* dev_alloc_shared_bytes(size_t bytes);
+void dev_free_shared(void* p);
+std::atomic<long>& dev_frees();  // synchronising frees (SE_PROFILE)
+
 template <class T>
 T* dev_alloc(size_t count) {
-  T* p = nullptr;
-  if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    fail(SE_ENOMEM, std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
-                        " bytes failed: " + cudaGetErrorString(e));
-  }
-  return p;
+  return static_cast<T*>(dev_alloc_bytes((count ? count : 1) * sizeof(T)));
 }
-inline void dev_free(void* p) {
-  if (p) cudaFree(p);
+template <class T>
+T* dev_alloc_shared(size_t count) {
+  return static_cast<T*>(dev_alloc_shared_bytes((count ? count : 1) * sizeof(T)));
 }
 
 }  // namespace se

@@ -364,8 +364,10 @@ struct CandBuf {
             Vec& out3) {
     HiPrio hp(c);
     const int n = A.n;
-    devmat_reserve(c, U, n, nc, false);
-    devmat_reserve(c, AU, n, nc, false);
+    // geometric growth: every reallocation is a cudaFree, which waits for the whole device
+    // (the other slices' queued work included)
+    if (nc > U.cap || U.n != n) devmat_reserve(c, U, n, grow(nc), false);
+    if (nc > AU.cap || AU.n != n) devmat_reserve(c, AU, n, grow(nc), false);
     if (nc > stats_cap) {
       dev_free(stats);
       stats_cap = grow(nc);
@@ -536,9 +538,9 @@ struct Slice {
     if (std::getenv("SE_PROFILE"))
       std::fprintf(stderr,
                    "[se] n=%d its=%ld total %.3f mv %.3f orth %.3f check %.3f eig %.3f cand %.3f "
-                   "passes %lld check_kernel_ms %.1f wcap %d fused %d\n",
+                   "passes %lld check_kernel_ms %.1f wcap %d fused %d frees %ld\n",
                    A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
-                   kr.get().passes_total, c.prof_kernel_ms, kr.W.cap, (int)kr.fused());
+                   kr.get().passes_total, c.prof_kernel_ms, kr.W.cap, (int)kr.fused(), dev_frees().load());
     r->niter = its;
     r->hit_max_its = warn;
     r->counters = cnt;

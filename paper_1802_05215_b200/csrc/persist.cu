@@ -167,7 +167,7 @@ void build_partition(Ctx& c, DevCsr& a, const int* rp_host) {
   int t32 = 0;
   for (long r0 = 0; r0 < a.n; r0 += 32) t32 = std::max(t32, rp_host[std::min<long>(r0 + 32, a.n)] - rp_host[r0]);
   a.tile32_nnz_max = t32;
-  a.part = dev_alloc<int>(P + 1);
+  a.part = dev_alloc_shared<int>(P + 1);
   h2d(c, a.part, part.data(), sizeof(int) * (P + 1));
   a.nparts = P;
   a.part_nnz_max = mx_nz;

@@ -953,7 +953,7 @@ void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
   const long nl = (long)g.nx * g.ny * g.nz;
   const int n = (int)nl;
   a.n = n;
-  a.rp = dev_alloc<int>(n + 1);
+  a.rp = dev_alloc_shared<int>(n + 1);
   const int tb = 256;
   k_lap_count<<<(n + 1 + tb - 1) / tb, tb, 0, c.stream>>>(g, n, a.rp);
   ++c.launches;
@@ -967,8 +967,8 @@ void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
   SE_CUDA(cudaMemcpyAsync(&nnz, a.rp + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   ctx_sync(c);
   a.nnz = nnz;
-  a.ci = dev_alloc<int>(nnz);
-  a.v = dev_alloc<double>(nnz);
+  a.ci = dev_alloc_shared<int>(nnz);
+  a.v = dev_alloc_shared<double>(nnz);
   k_lap_fill<<<(n + tb - 1) / tb, tb, 0, c.stream>>>(g, n, a.rp, a.ci, a.v);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
