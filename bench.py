@@ -192,22 +192,31 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
     A.free()
     ctx.close()
     g, per, by = out["cgs"]
+    traffic = {}
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_traffic.json")
+    if os.path.exists(tpath):  # dram bytes per launch from the committed ncu --set full captures
+        with open(tpath) as fh:
+            traffic = json.load(fh)
+    def _t(key):
+        return traffic.get(key, {}).get("traffic_bytes")
     roof = {"bound": "hbm", "kernel": "reorthogonalisation pass k_gemvt + k_gemvn (CGS, orth.hpp:19-32)",
             "achieved": round(g, 1), "peak": peak, "unit": "GB/s", "frac": round(g / peak, 4),
-            "peak_kind": peak_kind, "traffic": None,
+            "peak_kind": peak_kind, "traffic": _t("cgs_pass_n262144_k1440"),
             "shape": f"n={n}, k={cfg2_mean_cols} basis columns (mean over the cfg2 run)",
             "us_per_pass": round(per * 1e6, 2), "bytes_per_pass": by,
             "filter_spmv": {"kernel": "k_spmv_cheb<kNext> (fused filter degree)",
                             "hbm_160^3": {"achieved": round(out["hbm"][0], 1),
                                           "frac": round(out["hbm"][0] / peak, 4),
-                                          "us_per_launch": round(out["hbm"][1] * 1e6, 2)},
+                                          "us_per_launch": round(out["hbm"][1] * 1e6, 2),
+                                          "traffic": _t("spmv_cheb_160cubed")},
                             "workload_64^3_L2_resident": {"achieved": round(out["workload"][0], 1),
                                                           "us_per_launch": round(out["workload"][1] * 1e6, 2)}},
             "kpm_block_step": {"kernel": "k_kpm_stream (16-probe block, doubling; dos.hpp:96-110)",
                                "shape": "160^3 (BASELINE cfg3 matrix), b=16",
                                "achieved": round(out["kpm"][0], 1), "frac": round(out["kpm"][0] / peak, 4),
                                "us_per_step": round(out["kpm"][1] * 1e6, 2),
-                               "bytes_per_step": round(out["kpm"][2])}}
+                               "bytes_per_step": round(out["kpm"][2]),
+                               "traffic": _t("kpm_stream_160cubed_b16")}}
     return roof
 
 
