@@ -53,27 +53,55 @@ struct KArgs {
 // Latency structure (the kernel is latency-bound when A is L2-resident): one round trip for the
 // row pointers and every row-local operand (x[r], prev[r], out[r]), one for the staged tile,
 // one for the x gathers (8 in flight per thread).
+// Programmatic dependent launch: everything that does not depend on the previous kernel (row
+// pointers, the tile's A entries) is fetched BEFORE griddepcontrol.wait, so in a chain of filter
+// degrees the next launch's A staging overlaps the previous degree's tail; x, prev, out, and the
+// Ctl words are read after it.  Without the launch attribute the wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 template <int MODE>
 __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restrict__ rp,
                                                       const int* __restrict__ ci,
                                                       const double* __restrict__ v, KArgs a) {
-  if (a.halt && a.halt->halted) return;
   __shared__ __align__(16) double s_v[kChunk + 8];
   __shared__ __align__(16) int s_c[kChunk + 8];
   const size_t coff = (size_t)blockIdx.y * n;  // column of a column-major batch (kPlain)
-  const size_t ioff = a.src_ctl ? (size_t)a.src_ctl->i * a.src_ld : 0;
-  const double* __restrict__ x = a.x + coff + (a.x_indirect ? ioff : 0);
   const int r0 = blockIdx.x * kRows;
   const int r = r0 + threadIdx.x;
   const bool live = r < n;
   const int rend = min(r0 + kRows, n);
-  // round trip 1: tile bounds, own row bounds, row-local operands
+  // independent of the previous kernel: tile bounds, own row bounds, first chunk of A
   const int base = __ldg(rp + r0), end = __ldg(rp + rend);
   int rs = end, re = end;
-  double xr = 0.0, pv = 0.0, ov = 0.0;
   if (live) {
     rs = __ldg(rp + r);
     re = __ldg(rp + r + 1);
+  }
+  auto stage = [&](int c0) {  // cp.async (LDGSTS, 16-byte, zero-filled tails)
+    const int cend = c0 + min(kChunk, end - c0);
+    const int va = c0 & ~1, ca = c0 & ~3;
+    const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
+    for (int q = threadIdx.x; q < nv16; q += kRows) {
+      const int valid = min(2, cend - (va + 2 * q));
+      cp_async16(&s_v[2 * q], v + va + 2 * q, 8 * valid);
+    }
+    for (int q = threadIdx.x; q < nc16; q += kRows) {
+      const int valid = min(4, cend - (ca + 4 * q));
+      cp_async16(&s_c[4 * q], ci + ca + 4 * q, 4 * valid);
+    }
+  };
+  if (base < end) stage(base);
+  pdl_wait();
+  pdl_trigger();
+  if (a.halt && a.halt->halted) {
+    cp_async_wait_all();
+    return;
+  }
+  const size_t ioff = a.src_ctl ? (size_t)a.src_ctl->i * a.src_ld : 0;
+  const double* __restrict__ x = a.x + coff + (a.x_indirect ? ioff : 0);
+  double xr = 0.0, pv = 0.0, ov = 0.0;
+  if (live) {
     if (MODE != kPlain) xr = __ldg(x + r);
     if (MODE == kNext) {
       const double* __restrict__ prev = a.prev + (a.prev_indirect ? ioff : 0);
@@ -84,22 +112,12 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
   double acc = 0.0;
   for (int c0 = base; c0 < end; c0 += kChunk) {
     const int cn = min(kChunk, end - c0);
-    // round trip 2: stage the chunk with cp.async (LDGSTS, 16-byte, zero-filled tails): every
-    // load of the tile is in flight at once and none occupies a register.
     const int va = c0 & ~1, ca = c0 & ~3;
     const int cend = c0 + cn;
-    const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
-    for (int q = threadIdx.x; q < nv16; q += kRows) {
-      const int valid = min(2, cend - (va + 2 * q));
-      cp_async16(&s_v[2 * q], v + va + 2 * q, 8 * valid);
-    }
-    for (int q = threadIdx.x; q < nc16; q += kRows) {
-      const int valid = min(4, cend - (ca + 4 * q));
-      cp_async16(&s_c[4 * q], ci + ca + 4 * q, 4 * valid);
-    }
+    if (c0 != base) stage(c0);
     cp_async_wait_all();
     __syncthreads();
-    // round trip 3: gathers, 8 in flight; sums stay in storage order
+    // gathers, 8 in flight; sums stay in storage order
     const int p0 = max(rs, c0), pend = min(re, cend);
     const int dv = va, dc = ca;  // smem index = global index - chunk origin (per array)
     for (int p = p0; p < pend; p += 8) {
@@ -824,18 +842,31 @@ void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
     k.prev_indirect = (mode == kNext);
   }
   dim3 grid((a.n + kRows - 1) / kRows, mode == kPlain ? args.ncols : 1);
+  static const bool pdl = std::getenv("SE_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kRows);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
   switch (mode) {
     case kPlain:
-      k_spmv_cheb<kPlain><<<grid, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, k);
+      SE_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_cheb<kPlain>, a.n, (const int*)a.rp, (const int*)a.ci,
+                                 (const double*)a.v, k));
       break;
     case kFirst:
-      k_spmv_cheb<kFirst><<<grid, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, k);
+      SE_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_cheb<kFirst>, a.n, (const int*)a.rp, (const int*)a.ci,
+                                 (const double*)a.v, k));
       break;
     default:
-      k_spmv_cheb<kNext><<<grid, kRows, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, k);
+      SE_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_cheb<kNext>, a.n, (const int*)a.rp, (const int*)a.ci,
+                                 (const double*)a.v, k));
   }
   ++c.launches;
-  SE_CUDA(cudaGetLastError());
 }
 
 constexpr size_t kKpmSmem = sizeof(double) * (kKSlots * kB + kKSlots + 8) + sizeof(int) * (kKSlots + 8);
