@@ -25,6 +25,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# before anything initialises CUDA (see paper_1802_05215_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import subprocess
 import sys
 import threading

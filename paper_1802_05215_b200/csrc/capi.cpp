@@ -299,8 +299,7 @@ int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, co
     a.n = n;
     a.nnz = row_ptr[n];
     a.rp = dev_alloc_shared<int>(n + 1);
-    a.ci = dev_alloc_shared<int>(a.nnz);
-    a.v = dev_alloc_shared<double>(a.nnz);
+    a.alloc_entries(a.nnz);
     int mx = 0;
     for (int i = 0; i < n; ++i) mx = std::max(mx, row_ptr[i + 1] - row_ptr[i]);
     a.max_row_nnz = mx;
@@ -374,8 +373,7 @@ int se_csr_free(se_csr* a) {
     cudaSetDevice(a->a.device);
     dev_free_shared(a->a.rp);
     dev_free_shared(a->a.part);
-    dev_free_shared(a->a.ci);
-    dev_free_shared(a->a.v);
+    a->a.free_entries();
     delete a;
   });
 }

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -37,6 +38,11 @@ struct DevCsr {
   double* v = nullptr;
   int max_row_nnz = 0;
   int tile32_nnz_max = 0;  // max nnz over aligned 32-row tiles (pipelined KPM kernel precondition)
+  // vals and col_idx live in ONE allocation (vals first, col_idx right after) so a single L2
+  // access-policy window covers the whole matrix stream of the filter SpMV
+  void alloc_entries(long count);
+  size_t entries_bytes() const { return (((size_t)std::max(nnz, 1L) + 1) & ~(size_t)1) * 12; }
+  void free_entries();
   // nnz-balanced row partition (one part per SM) for the persistent filter kernel
   int* part = nullptr;
   int nparts = 0;
@@ -51,6 +57,19 @@ struct DevMat {
   double* p = nullptr;
   double* col(int j) const { return p + (size_t)j * n; }
 };
+
+void* dev_alloc_shared_bytes(size_t bytes);
+void dev_free_shared(void* p);
+inline void DevCsr::alloc_entries(long count) {
+  const size_t c = ((size_t)std::max(count, 1L) + 1) & ~(size_t)1;  // even: col_idx 16-byte aligned
+  v = static_cast<double*>(dev_alloc_shared_bytes(c * (sizeof(double) + sizeof(int)) + 16));
+  ci = reinterpret_cast<int*>(v + c);
+}
+inline void DevCsr::free_entries() {
+  dev_free_shared(v);
+  v = nullptr;
+  ci = nullptr;
+}
 
 struct Ctx;
 void devmat_reserve(Ctx& c, DevMat& m, int n, int cols, bool keep);

@@ -15,6 +15,9 @@ namespace se {
 struct Ctx {
   int device = 0;
   int num_sms = 148;
+  int prio_hi = 0, prio_lo = 0;  // stream/kernel priority range of the device
+  size_t l2_persist = 0;         // persisting-L2 set-aside granted (bytes; 0: disabled)
+  size_t l2_window_max = 0;      // largest access-policy window
   cudaStream_t stream = nullptr;   // current launch stream (bulk Lanczos work: low priority)
   cudaStream_t bulk = nullptr;     // the low-priority stream
   cudaStream_t hstream = nullptr;  // high priority: latency-bound host-driven phases
@@ -32,6 +35,7 @@ struct Ctx {
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // profiling of host-driven phases
   cudaEvent_t evx = nullptr;                    // cross-stream ordering of allocations
   double prof_kernel_ms = 0.0;
+  double prof_chk[3] = {0, 0, 0};  // stagnation check: h2d, kernel + count, d2h (host seconds)
   void* pinned = nullptr;  // staging for host<->device copies (pageable copies serialise
   size_t pinned_bytes = 0; // across the slice threads sharing a GPU)  // blocking-sync event: host waits sleep instead of spinning
 };

@@ -258,7 +258,7 @@ struct Krylov {
       }
       cudaGraph_t g;
       SE_CUDA(cudaStreamEndCapture(c.stream, &g));
-      SE_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+      SE_CUDA(cudaGraphInstantiate(&gexec, g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
       gnodes = (int)(c.launches - before);
       c.launches = before;
@@ -538,9 +538,10 @@ struct Slice {
     if (std::getenv("SE_PROFILE"))
       std::fprintf(stderr,
                    "[se] n=%d its=%ld total %.3f mv %.3f orth %.3f check %.3f eig %.3f cand %.3f "
-                   "passes %lld check_kernel_ms %.1f wcap %d fused %d frees %ld\n",
+                   "passes %lld check_kernel_ms %.1f wcap %d fused %d frees %ld chk %.2f/%.2f/%.2f\n",
                    A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
-                   kr.get().passes_total, c.prof_kernel_ms, kr.W.cap, (int)kr.fused(), dev_frees().load());
+                   kr.get().passes_total, c.prof_kernel_ms, kr.W.cap, (int)kr.fused(), dev_frees().load(),
+                   c.prof_chk[0], c.prof_chk[1], c.prof_chk[2]);
     r->niter = its;
     r->hit_max_its = warn;
     r->counters = cnt;
@@ -1288,7 +1289,7 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
-    SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
     const long per = persist ? op.k : c.launches - before;
     SE_CUDA(cudaGraphLaunch(ge, c.stream));  // warm
@@ -1371,7 +1372,7 @@ void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
     }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
-    SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
     const long per = c.launches - before;
     SE_CUDA(cudaGraphLaunch(ge, c.stream));
@@ -1431,7 +1432,7 @@ void multi_filter_bench(Ctx& c, const DevCsr& a, int nv, int kdeg, int reps, dou
     }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
-    SE_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
     SE_CUDA(cudaGraphLaunch(ge, c.stream));
     SE_CUDA(cudaEventRecord(c.ev0, c.stream));

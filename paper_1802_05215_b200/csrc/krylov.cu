@@ -8,6 +8,8 @@
 // whole Lanczos step is replayable as one CUDA graph.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace se {
@@ -385,7 +387,14 @@ __global__ void k_stamp(Ctl* ctl, int which) {
   }
 }
 
-int rch_for(int n) { return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512); }
+int rch_for(int n) {
+  static const int force = [] {
+    const char* e = std::getenv("SE_RCH");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force > 0) return std::min(force, kMaxRch);
+  return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512);
+}
 
 }  // namespace
 

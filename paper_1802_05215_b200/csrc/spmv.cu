@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
   }
 }
 
+
 // ---- multi-vector filter degree (one A tile staging for up to kMV independent recurrences) ------
 // Used to batch the filter degree j of several slices solved on the same GPU: the tile of A is
 // staged once and every live vector's row sum is formed from it (storage order, rounded exactly
@@ -843,16 +844,41 @@ void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
   }
   dim3 grid((a.n + kRows - 1) / kRows, mode == kPlain ? args.ncols : 1);
   static const bool pdl = std::getenv("SE_NO_PDL") == nullptr;
+  // The filter chain is latency-bound (k dependent launches per Lanczos step) while the slices'
+  // reorthogonalisation passes sharing the GPU are bandwidth-bound: filter launches (and their
+  // graph nodes) get the device's highest priority so their CTAs are scheduled ahead of queued
+  // GEMV CTAs of other slices.
+  static const bool prio = std::getenv("SE_NO_FILTER_PRIO") == nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kRows);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = c.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[3];
+  int na = 0;
+  const size_t eb = a.entries_bytes();
+  if (c.l2_persist > 0 && eb <= c.l2_persist && eb <= c.l2_window_max) {
+    // the CSR entries (vals + col_idx, one allocation) persist in the L2 set-aside
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow.base_ptr = a.v;
+    attr[na].val.accessPolicyWindow.num_bytes = eb;
+    attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (prio) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = c.prio_hi;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   switch (mode) {
     case kPlain:
       SE_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_cheb<kPlain>, a.n, (const int*)a.rp, (const int*)a.ci,
@@ -998,8 +1024,7 @@ void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
   SE_CUDA(cudaMemcpyAsync(&nnz, a.rp + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   ctx_sync(c);
   a.nnz = nnz;
-  a.ci = dev_alloc_shared<int>(nnz);
-  a.v = dev_alloc_shared<double>(nnz);
+  a.alloc_entries(nnz);
   k_lap_fill<<<(n + tb - 1) / tb, tb, 0, c.stream>>>(g, n, a.rp, a.ci, a.v);
   ++c.launches;
   SE_CUDA(cudaGetLastError());

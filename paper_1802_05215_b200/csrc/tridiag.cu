@@ -5,6 +5,8 @@
 // once per cycle) is bisected on the device with Sturm counts, one thread per wanted eigenvalue.
 #include <cfloat>
 
+#include <chrono>
+
 #include "kernels.hpp"
 
 namespace se {
@@ -83,9 +85,11 @@ void tridiag_eigs_above(Ctx& c, int m, const double* d_host, const double* e_hos
   double* e = work + m;
   double* vals = work + 3 * m;
   int* cnt = reinterpret_cast<int*>(work + 4 * m);
+  const auto t0 = std::chrono::steady_clock::now();
   h2d(c, d, d_host, sizeof(double) * m);
   if (m > 1)
     h2d(c, e, e_host, sizeof(double) * (m - 1));
+  const auto t1 = std::chrono::steady_clock::now();
   const int tb = 128;  // 4 eigenvalues (warps) per CTA
   SE_CUDA(cudaEventRecord(c.evk0, c.stream));
   k_tridiag_above<<<(m + 3) / 4, tb, 0, c.stream>>>(m, d, e, bar, vals, cnt);
@@ -95,6 +99,7 @@ void tridiag_eigs_above(Ctx& c, int m, const double* d_host, const double* e_hos
   int h = 0;
   d2h(c, &h, cnt, sizeof(int));
   ctx_sync(c);
+  const auto t2 = std::chrono::steady_clock::now();
   float kms = 0.f;
   SE_CUDA(cudaEventElapsedTime(&kms, c.evk0, c.evk1));
   c.prof_kernel_ms += kms;
@@ -102,6 +107,11 @@ void tridiag_eigs_above(Ctx& c, int m, const double* d_host, const double* e_hos
   if (h)
     d2h(c, out.data(), vals, sizeof(double) * h);
   ctx_sync(c);
+  const auto t3 = std::chrono::steady_clock::now();
+  auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+  c.prof_chk[0] += sec(t0, t1);
+  c.prof_chk[1] += sec(t1, t2);
+  c.prof_chk[2] += sec(t2, t3);
 }
 
 }  // namespace k

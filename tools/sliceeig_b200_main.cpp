@@ -624,6 +624,8 @@ void usage(std::ostream& os) {
 }  // namespace
 
 int main(int argc, char** argv) {
+  // 32 hardware work queues for the slice contexts' streams (before CUDA initialises)
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
   if (argc < 2) {
     usage(std::cerr);
     return 2;
