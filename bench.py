@@ -223,6 +223,14 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
     return roof
 
 
+def arm_config(cfg, n, world):
+    """The workload both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": f"cfg2: {cfg['dims'][0]}^3 7-pt Laplacian, KPM 100x40 Gaussian, "
+                        f"[0.6,1.2] in 8 slices, ChebLanTr tol 1e-8",
+            "n": n, "slices": cfg["ns"], "parallelism": f"slices{world}",
+            "l2": "working set (Krylov bases ~1-6 GB per slice) >> 126 MB L2; no flush"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the unmodified reference pipeline (oracle/_ref) on this host's cores."""
     if rank != 0:
@@ -253,9 +261,8 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg2 recipe on {cfg['dims'][0]}^3 proxy (CPU-bounded sample)",
-                       "matrix": "3-D 7-pt Laplacian", "interval": [cfg["xi"], cfg["eta"]],
-                       "slices": cfg["ns"], "solver": "ChebLanTr", "tol": cfg["tol"]},
+            "config": dict(arm_config(CFG2, int(np.prod(CFG2["dims"])), args.gpus),
+                           sample=f"bounded sample: the same recipe on the {cfg['dims'][0]}^3 proxy"),
             "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": min(cores, cfg["ns"]),
                              "kind": "reference", "sample": sample},
             "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -372,10 +379,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (generated Laplacian, seeded Gaussian/normal probes)",
-                "config": {"workload": f"cfg2: {cfg['dims'][0]}^3 7-pt Laplacian, KPM 100x40 Gaussian, "
-                                       f"[0.6,1.2] in 8 slices, ChebLanTr tol 1e-8",
-                           "n": backend.n, "slices": cfg["ns"], "parallelism": f"slices{world}",
-                           "l2": "working set (Krylov bases ~1-6 GB per slice) >> 126 MB L2; no flush"},
+                "config": arm_config(cfg, backend.n, world),
                 "eigenpairs_per_step": int(found_all / args.steps),
                 "per_slice": per_slice, "t_bounds": round(res.t_bounds, 3),
                 "t_dos": round(res.t_dos, 3), "t_solve": round(res.t_solve, 3),
