@@ -304,7 +304,6 @@ int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, co
     for (int i = 0; i < n; ++i) mx = std::max(mx, row_ptr[i + 1] - row_ptr[i]);
     a.max_row_nnz = mx;
     SE_CUDA(cudaMemcpyAsync(a.rp, row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, c.stream));
-    if (n > 0) k::build_partition(c, a, row_ptr);
     if (a.nnz) {
       SE_CUDA(cudaMemcpyAsync(a.ci, col_idx, sizeof(int) * a.nnz, cudaMemcpyHostToDevice, c.stream));
       SE_CUDA(cudaMemcpyAsync(a.v, vals, sizeof(double) * a.nnz, cudaMemcpyHostToDevice, c.stream));
@@ -328,9 +327,6 @@ int se_csr_gen_laplacian(se_ctx* ctx, int ndims, const int* dims, se_csr** out) 
     h->a.device = c.device;
     k::gen_laplacian(c, ndims, dims, h->a);
     ctx_sync(c);
-    std::vector<int> rp(h->a.n + 1);
-    d2h(c, rp.data(), h->a.rp, sizeof(int) * (h->a.n + 1));
-    k::build_partition(c, h->a, rp.data());
     *out = h.release();
   });
 }
@@ -372,7 +368,6 @@ int se_csr_free(se_csr* a) {
     if (!a) return;
     cudaSetDevice(a->a.device);
     dev_free_shared(a->a.rp);
-    dev_free_shared(a->a.part);
     a->a.free_entries();
     delete a;
   });

@@ -37,16 +37,11 @@ struct DevCsr {
   int* ci = nullptr;
   double* v = nullptr;
   int max_row_nnz = 0;
-  int tile32_nnz_max = 0;  // max nnz over aligned 32-row tiles (pipelined KPM kernel precondition)
   // vals and col_idx live in ONE allocation (vals first, col_idx right after) so a single L2
   // access-policy window covers the whole matrix stream of the filter SpMV
   void alloc_entries(long count);
   size_t entries_bytes() const { return (((size_t)std::max(nnz, 1L) + 1) & ~(size_t)1) * 12; }
   void free_entries();
-  // nnz-balanced row partition (one part per SM) for the persistent filter kernel
-  int* part = nullptr;
-  int nparts = 0;
-  int part_nnz_max = 0, part_rows_max = 0;
   double abytes() const { return 12.0 * (double)nnz + 4.0 * (double)(n + 1); }
 };
 

@@ -40,7 +40,6 @@ struct Krylov {
   int nlock = 0;
 
   double* mu_dev = nullptr;
-  bool persist = false;
   // fused CGS2 middle (cgs_mid.cu): second coefficient vector + its own scratch and counter
   double* coef2 = nullptr;
   double* mid_scratch = nullptr;
@@ -53,7 +52,6 @@ struct Krylov {
       for (double*& b : fb) b = dev_alloc<double>(n);
       mu_dev = dev_alloc<double>(op.k + 1);
       h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
-      persist = k::persist_eligible(c, a) && std::getenv("SE_PERSIST") != nullptr;
     }
     ctl = dev_alloc<Ctl>(1);
     dscal = dev_alloc<double>(4);
@@ -185,10 +183,6 @@ struct Krylov {
       a.x = W.p;
       a.y = t;
       k::spmv_cheb(c, A, k::kPlain, a);
-      return;
-    }
-    if (persist) {
-      k::filter_persist(c, A, W.p, ctl, n, ctl, t, fb, mu_dev, op.k, op.c, op.invd);
       return;
     }
     a.c = op.c;
@@ -820,20 +814,7 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
   if (op.k < 1) fail(SE_EINVAL, "apply_pol: filter degree must be >= 1");
   double* fb[3];
   for (double*& b : fb) b = dev_alloc<double>(n);
-  double* mu_dev = nullptr;
-  const bool persist = k::persist_eligible(c, a) && std::getenv("SE_PERSIST") != nullptr;
   try {
-    if (persist) {
-      mu_dev = dev_alloc<double>(op.k + 1);
-      h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
-      for (int col = 0; col < nvec; ++col)
-        k::filter_persist(c, a, v + (size_t)col * n, nullptr, 0, nullptr, out + (size_t)col * n, fb,
-                          mu_dev, op.k, op.c, op.invd);
-      ctx_sync(c);
-      dev_free(mu_dev);
-      for (double* b : fb) dev_free(b);
-      return;
-    }
     for (int col = 0; col < nvec; ++col) {
       const double* x = v + (size_t)col * n;
       double* o = out + (size_t)col * n;
@@ -862,7 +843,6 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
     }
     ctx_sync(c);
   } catch (...) {
-    dev_free(mu_dev);
     for (double* b : fb) dev_free(b);
     throw;
   }
@@ -1259,11 +1239,7 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     const long before = c.launches;
     double* mu_dev = dev_alloc<double>(op.k + 1);
     h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
-    const bool persist = k::persist_eligible(c, a) && std::getenv("SE_PERSIST") != nullptr;
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
-    if (persist) {
-      k::filter_persist(c, a, v, nullptr, 0, nullptr, out, fb, mu_dev, op.k, op.c, op.invd);
-    } else {
     k::ChebArgs a1;
     a1.c = op.c;
     a1.invd = op.invd;
@@ -1286,12 +1262,11 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
       cur = nxt;
       nxt = old;
     }
-    }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
     SE_CUDA(cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
-    const long per = persist ? op.k : c.launches - before;
+    const long per = c.launches - before;
     SE_CUDA(cudaGraphLaunch(ge, c.stream));  // warm
     SE_CUDA(cudaEventRecord(c.ev0, c.stream));
     for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));

@@ -63,13 +63,7 @@ struct MultiArgs {
 };
 void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args);
 
-// Persistent cooperative filter (all k degrees in one launch, A resident in shared memory) for
-// matrices whose CSR fits the GPU's aggregate shared memory (persist.cu).
-bool persist_eligible(const Ctx& c, const DevCsr& a);
-void build_partition(Ctx& c, DevCsr& a, const int* rp_host);
-void filter_persist(Ctx& c, const DevCsr& a, const double* v, const Ctl* src_ctl, long src_ld,
-                    const Ctl* halt, double* out, double* const* bufs, const double* mu_dev,
-                    int kdeg, double cc, double invd);
+
 
 // Block KPM step over b <= 16 row-major probe columns (dos.hpp:98-108):
 //   first: w1 = (A w0 - c w0)/d ; zeta[0], zeta[1] partials

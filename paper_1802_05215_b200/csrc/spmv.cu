@@ -398,237 +398,9 @@ __global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_step(
   kpm_finish(acc0, acc1, b, first, dbl, partial, counter, zeta, kmom);
 }
 
-// Software-pipelined variant for matrices whose aligned 32-row tiles hold <= kPS entries (the
-// stencils of cfgs 1/2/3/5): while tile k is reduced, the probe-row gathers of tile k+1, the A
-// entries of tile k+2 and the row pointers of tile k+3 are in flight (cp.async groups), so the
-// three dependent fetches of a tile (row_ptr -> (col_idx, vals) -> probe rows) overlap other
-// tiles' arithmetic instead of serialising.  Same per-row storage-order sums as k_kpm_step.
-constexpr int kPR = 32;   // rows per tile: 16 half-warps x 2 rows
-constexpr int kPS = 224;  // A entries (and gathered probe rows) per tile (7-point stencil: 32 x 7)
-constexpr size_t kPipeSmem = sizeof(double) * (2 * kPS * kB + 3 * (kPS + 8)) + sizeof(int) * (3 * (kPS + 8) + 4 * 40);
-
-__global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_pipe(
-    int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
-    int b, int mode, const double* __restrict__ v, const double* __restrict__ w0,
-    const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
-    double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
-  const bool first = mode == kKpmFirst;
-  const bool dbl = mode == kKpmDoubling;
-  extern __shared__ __align__(16) unsigned char kpm_smem[];
-  double(*s_x)[kPS][kB] = reinterpret_cast<double(*)[kPS][kB]>(kpm_smem);      // [2]
-  double* s_vb = reinterpret_cast<double*>(kpm_smem + sizeof(double) * 2 * kPS * kB);  // [3][kPS+8]
-  int* s_cb = reinterpret_cast<int*>(kpm_smem + sizeof(double) * (2 * kPS * kB + 3 * (kPS + 8)));
-  int* s_rb = s_cb + 3 * (kPS + 8);  // [4][40]
-  const int lane = threadIdx.x & (kB - 1);
-  const int hw = threadIdx.x / kB;
-  const bool live = lane < b;
-  const double* __restrict__ src = first ? w0 : w1;
-  const int ntiles = (n + kPR - 1) / kPR;
-  const int parts = (b * 8 + 15) / 16;
-  auto tile_of = [&](int k) { return (int)blockIdx.x + k * (int)gridDim.x; };
-  auto issue_rp = [&](int k) {  // rp[r0 .. r0+32] -> s_rb[k % 4]
-    const int tl = tile_of(k);
-    if (tl >= ntiles || threadIdx.x >= 9) return;
-    const int r0 = tl * kPR, q = threadIdx.x;
-    const int valid = max(0, min(4, n + 1 - (r0 + 4 * q)));
-    cp_async16(s_rb + (k & 3) * 40 + 4 * q, rp + r0 + 4 * q, 4 * valid);
-  };
-  auto issue_a = [&](int k) {  // entries of tile k -> s_vb/s_cb[k % 3] (row pointers landed)
-    const int tl = tile_of(k);
-    if (tl >= ntiles) return;
-    const int* rr = s_rb + (k & 3) * 40;
-    const int base = rr[0], end = rr[min(kPR, n - tl * kPR)];
-    const int va = base & ~1, ca = base & ~3;
-    const int nv16 = (end - va + 1) >> 1, nc16 = (end - ca + 3) >> 2;
-    double* sv = s_vb + (k % 3) * (kPS + 8);
-    int* sc = s_cb + (k % 3) * (kPS + 8);
-    for (int q = threadIdx.x; q < nv16; q += kKpmThreads)
-      cp_async16(&sv[2 * q], vals + va + 2 * q, 8 * min(2, end - (va + 2 * q)));
-    for (int q = threadIdx.x; q < nc16; q += kKpmThreads)
-      cp_async16(&sc[4 * q], ci + ca + 4 * q, 4 * min(4, end - (ca + 4 * q)));
-  };
-  auto issue_gather = [&](int k) {  // probe rows of tile k -> s_x[k & 1] (entries landed)
-    const int tl = tile_of(k);
-    if (tl >= ntiles) return;
-    const int* rr = s_rb + (k & 3) * 40;
-    const int base = rr[0], end = rr[min(kPR, n - tl * kPR)], cn = end - base;
-    const int* sc = s_cb + (k % 3) * (kPS + 8) + (base - (base & ~3));
-    double(*sx)[kB] = s_x[k & 1];
-    if (b == kB) {
-      for (int q = threadIdx.x; q < cn * 8; q += kKpmThreads) {
-        const int p = q >> 3, part = q & 7;
-        cp_async16(&sx[p][2 * part], src + (size_t)sc[p] * kB + 2 * part, 16);
-      }
-    } else {
-      for (int q = threadIdx.x; q < cn * parts; q += kKpmThreads) {
-        const int p = q / parts, part = q - p * parts;
-        cp_async16(&sx[p][2 * part], src + (size_t)sc[p] * b + 2 * part, min(16, b * 8 - part * 16));
-      }
-    }
-  };
-  // prologue: rp(0), rp(1) -> A(0), rp(2) -> gathers(0), A(1)
-  issue_rp(0);
-  issue_rp(1);
-  cp_async_wait_all();
-  __syncthreads();
-  issue_a(0);
-  issue_rp(2);
-  cp_async_wait_all();
-  __syncthreads();
-  issue_gather(0);
-  issue_a(1);
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  double acc0 = 0.0, acc1 = 0.0;
-  for (int k = 0; tile_of(k) < ntiles; ++k) {
-    const int r0 = tile_of(k) * kPR;
-    double xr[2], pr[2], vr[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {  // this tile's own probe rows (in flight during the wait)
-      const int r = r0 + hw + 16 * q;
-      xr[q] = pr[q] = vr[q] = 0.0;
-      if (r < n && live) {
-        const size_t o = (size_t)r * b + lane;
-        xr[q] = __ldg(src + o);
-        if (!dbl) vr[q] = __ldg(v + o);
-        if (!first) pr[q] = __ldg(w0 + o);
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();  // gathers(k), A(k+1), rp(k+2) landed; tile k-1 fully consumed
-    issue_gather(k + 1);
-    issue_a(k + 2);
-    issue_rp(k + 3);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const int* rr = s_rb + (k & 3) * 40;
-    const int base = rr[0];
-    const double* sv = s_vb + (k % 3) * (kPS + 8) + (base - (base & ~1));
-    const double(*sx)[kB] = s_x[k & 1];
-    if (live) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int rl = hw + 16 * q, r = r0 + rl;
-        if (r >= n) continue;
-        double acc = 0.0;
-        for (int p = rr[rl] - base, pe = rr[rl + 1] - base; p < pe; ++p) acc = add(acc, mul(sv[p], sx[p][lane]));
-        const size_t o = (size_t)r * b + lane;
-        const double m = __ddiv_rn(sub(acc, mul(cc, xr[q])), d);  // dos.hpp:99
-        if (first) {
-          t[o] = m;
-          acc0 = add(acc0, mul(vr[q], xr[q]));
-          acc1 = add(acc1, mul(vr[q], m));
-        } else {
-          const double tk = sub(mul(2.0, m), pr[q]);
-          t[o] = tk;
-          if (dbl) {
-            acc0 = add(acc0, mul(xr[q], xr[q]));
-            acc1 = add(acc1, mul(xr[q], tk));
-          } else {
-            acc0 = add(acc0, mul(vr[q], tk));
-          }
-        }
-      }
-    }
-  }
-  cp_async_wait_all();
-  kpm_finish(acc0, acc1, b, first, dbl, partial, counter, zeta, kmom);
-}
-
-// Direct-gather variant for even probe counts: no shared-memory staging.  A warp sweeps 4 rows
-// at a time, 8 lanes per row, each lane owning a probe pair (16-byte loads and stores); the
-// entries of a row are taken U at a time: U (col, val) loads, then U independent probe-row
-// loads, then the storage-order sums.  Few instructions per entry and many independent loads in
-// flight; probe rows re-read by neighbouring rows hit L1/L2.  Same per-row storage-order sums.
-template <int U>
-__global__ void __launch_bounds__(kKpmThreads, 4) k_kpm_direct(
-    int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
-    int b, int mode, const double* __restrict__ v, const double* __restrict__ w0,
-    const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
-    double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
-  const bool first = mode == kKpmFirst;
-  const bool dbl = mode == kKpmDoubling;
-  const int lane = threadIdx.x & 31, g = lane >> 3, l8 = lane & 7;
-  const bool live = 2 * l8 < b;  // b even
-  const double* __restrict__ src = first ? w0 : w1;
-  const int warps = (int)(gridDim.x * (kKpmThreads / 32));
-  const int gw = (int)(blockIdx.x * (kKpmThreads / 32) + (threadIdx.x >> 5));
-  const int nb = (n + 3) / 4;
-  double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-  for (int rb = gw; rb < nb; rb += warps) {
-    const int r = 4 * rb + g;
-    if (r < n && live) {
-      const int rs = __ldg(rp + r), re = __ldg(rp + r + 1);
-      const size_t o = (size_t)r * b + 2 * l8;
-      const double2 xr = __ldg(reinterpret_cast<const double2*>(src + o));
-      double2 vr = make_double2(0.0, 0.0), pr = make_double2(0.0, 0.0);
-      if (!dbl) vr = __ldg(reinterpret_cast<const double2*>(v + o));
-      if (!first) pr = __ldg(reinterpret_cast<const double2*>(w0 + o));
-      double2 acc = make_double2(0.0, 0.0);
-      for (int p0 = rs; p0 < re; p0 += U) {
-        int c[U];
-        double a[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool ok = p0 + u < re;
-          c[u] = ok ? __ldg(ci + p0 + u) : 0;
-          a[u] = ok ? __ldg(vals + p0 + u) : 0.0;
-        }
-        double2 x[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          x[u] = p0 + u < re ? __ldg(reinterpret_cast<const double2*>(src + (size_t)c[u] * b + 2 * l8))
-                             : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (p0 + u < re) {
-            acc.x = add(acc.x, mul(a[u], x[u].x));
-            acc.y = add(acc.y, mul(a[u], x[u].y));
-          }
-      }
-      // (A w - c w) / d   (dos.hpp:99)
-      const double2 m = make_double2(__ddiv_rn(sub(acc.x, mul(cc, xr.x)), d),
-                                     __ddiv_rn(sub(acc.y, mul(cc, xr.y)), d));
-      double2* to = reinterpret_cast<double2*>(t + o);
-      if (first) {
-        *to = m;
-        a0.x = add(a0.x, mul(vr.x, xr.x));
-        a0.y = add(a0.y, mul(vr.y, xr.y));
-        a1.x = add(a1.x, mul(vr.x, m.x));
-        a1.y = add(a1.y, mul(vr.y, m.y));
-      } else {
-        const double2 tk = make_double2(sub(mul(2.0, m.x), pr.x), sub(mul(2.0, m.y), pr.y));
-        *to = tk;
-        if (dbl) {
-          a0.x = add(a0.x, mul(xr.x, xr.x));
-          a0.y = add(a0.y, mul(xr.y, xr.y));
-          a1.x = add(a1.x, mul(xr.x, tk.x));
-          a1.y = add(a1.y, mul(xr.y, tk.y));
-        } else {
-          a0.x = add(a0.x, mul(vr.x, tk.x));
-          a0.y = add(a0.y, mul(vr.y, tk.y));
-        }
-      }
-    }
-  }
-  // regroup to kpm_finish's layout (thread h*16 + j holds probe j's partial of group h): the
-  // 256 threads hold (warp, row-group g, pair l8) -> probe 2 l8 + {0,1}; 32 groups of 8 lanes
-  __shared__ double s_a0[kKpmThreads / 8][kB], s_a1[kKpmThreads / 8][kB];
-  const int grp = threadIdx.x >> 3;  // warp * 4 + g
-  s_a0[grp][2 * l8] = a0.x;
-  s_a0[grp][2 * l8 + 1] = a0.y;
-  s_a1[grp][2 * l8] = a1.x;
-  s_a1[grp][2 * l8 + 1] = a1.y;
-  __syncthreads();
-  // 16 "half-warp" slots of kpm_finish: slot h sums groups 2h, 2h+1 in order
-  const int h = threadIdx.x / kB, j = threadIdx.x % kB;
-  const double f0 = add(s_a0[2 * h][j], s_a0[2 * h + 1][j]);
-  const double f1 = add(s_a1[2 * h][j], s_a1[2 * h + 1][j]);
-  __syncthreads();
-  kpm_finish(f0, f1, b, first, dbl, partial, counter, zeta, kmom);
-}
-
-// Pipelined direct-gather variant (default for even probe counts).  Layout as k_kpm_direct (a
-// warp sweeps 4 rows, 8 lanes x probe pairs per row), but the three dependent fetches of a row
-// batch are software-pipelined across batches: the row pointers of batch k+2 and the
+// Pipelined direct-gather block step (default for even probe counts): no shared-memory staging;
+// a warp sweeps 4 rows at a time, 8 lanes per row, each lane owning a probe pair (16-byte loads
+// and stores).  The three dependent fetches of a row batch are software-pipelined across batches: the row pointers of batch k+2 and the
 // (col, val) entries of batch k+1 -- loaded cooperatively, one coalesced load per warp, since
 // the 4 rows' entries are contiguous -- are in flight while batch k's probe rows are gathered
 // and reduced.  Entries reach their row's lanes by warp shuffles.  Batches whose rows exceed U
@@ -919,24 +691,8 @@ int kpm_blocks(const Ctx& c, int n) {
   }();
   return std::max(1, std::min(c.num_sms * per_sm, (n + kKRows - 1) / kKRows));
 }
-template <int U>
-int direct_per_sm() {
-  int v = 0;
-  SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_direct<U>, kKpmThreads, 0));
-  return std::max(1, v);
-}
-
-int kpm_pipe_blocks(const Ctx& c, int n) {
-  static const int per_sm = [] {
-    SE_CUDA(cudaFuncSetAttribute(k_kpm_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem));
-    int v = 0;
-    SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_pipe, kKpmThreads, kPipeSmem));
-    return std::max(1, v);
-  }();
-  return std::max(1, std::min(c.num_sms * per_sm, (n + kPR - 1) / kPR));
-}
 size_t kpm_scratch_doubles(const Ctx& c, int n) {
-  return (size_t)2 * kB * std::max(kpm_blocks(c, n), std::max(kpm_pipe_blocks(c, n), c.num_sms * 8));
+  return (size_t)2 * kB * std::max(kpm_blocks(c, n), c.num_sms * 8);
 }
 
 void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args) {
@@ -960,12 +716,13 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
               const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
               int kmom) {
   if (kpm_scratch_doubles(c, a.n) > s.cap || s.ncnt < 1) fail(SE_EINVAL, "internal: kpm scratch");
-  static const int variant = [] {
-    const char* e = std::getenv("SE_KPM_KERNEL");  // stream (default) | direct4 | direct8 | pipe | tile
-    const std::string v = e ? e : "stream";
-    return v == "direct4" ? 0 : v == "direct8" ? 1 : v == "pipe" ? 2 : v == "tile" ? 3 : 4;
+  // default: the pipelined direct-gather kernel (even probe counts); odd counts take the
+  // shared-memory tile kernel.  SE_KPM_KERNEL=tile forces the latter (A/B comparisons).
+  static const bool force_tile = [] {
+    const char* e = std::getenv("SE_KPM_KERNEL");
+    return e && std::string(e) == "tile";
   }();
-  if (variant == 4 && b % 2 == 0) {
+  if (!force_tile && b % 2 == 0) {
     static const int per_sm = [] {
       int v = 0;
       SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_stream<8, 0>, kKpmThreads, 0));
@@ -983,27 +740,6 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
                                           : pick(std::integral_constant<int, 8>{});
     kern<<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc, d, s.buf,
                                              s.cnt, zeta_dev, kmom);
-    ++c.launches;
-    SE_CUDA(cudaGetLastError());
-    return;
-  }
-  if (variant <= 1 && b % 2 == 0) {
-    static const int per_sm[2] = {direct_per_sm<4>(), direct_per_sm<8>()};
-    const int grid = std::max(1, std::min(c.num_sms * per_sm[variant], (a.n + 31) / 32));
-    if (variant == 0)
-      k_kpm_direct<4><<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc,
-                                                          d, s.buf, s.cnt, zeta_dev, kmom);
-    else
-      k_kpm_direct<8><<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc,
-                                                          d, s.buf, s.cnt, zeta_dev, kmom);
-    ++c.launches;
-    SE_CUDA(cudaGetLastError());
-    return;
-  }
-  const bool no_pipe = variant == 3;
-  if (a.tile32_nnz_max <= kPS && !no_pipe) {
-    k_kpm_pipe<<<kpm_pipe_blocks(c, a.n), kKpmThreads, kPipeSmem, c.stream>>>(
-        a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc, d, s.buf, s.cnt, zeta_dev, kmom);
     ++c.launches;
     SE_CUDA(cudaGetLastError());
     return;
