@@ -308,6 +308,7 @@ int se_csr_upload(se_ctx* ctx, int n, const int* row_ptr, const int* col_idx, co
       SE_CUDA(cudaMemcpyAsync(a.ci, col_idx, sizeof(int) * a.nnz, cudaMemcpyHostToDevice, c.stream));
       SE_CUDA(cudaMemcpyAsync(a.v, vals, sizeof(double) * a.nnz, cudaMemcpyHostToDevice, c.stream));
     }
+    k::build_ell(c, a);
     ctx_sync(c);
     *out = h.release();
   });
@@ -369,6 +370,10 @@ int se_csr_free(se_csr* a) {
     cudaSetDevice(a->a.device);
     dev_free_shared(a->a.rp);
     a->a.free_entries();
+    if (a->a.ell_c) {
+      dev_free_shared(a->a.ell_c);
+      dev_free_shared(a->a.ell_a);
+    }
     delete a;
   });
 }
@@ -563,14 +568,18 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
   try {
     for (int b0 = 0, q = 0; b0 < count; b0 += kBlock, ++q) {
       const int b = std::min(kBlock, count - b0);
+      // odd blocks carry one zero probe column (its moments are dropped): every row of the
+      // row-major block is then 16-byte aligned for the kernels' paired loads
+      const int bk = b + (b & 1);
       next.get();
       hbuf = hb[q & 1];
-      SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(double) * (size_t)n * b, cudaMemcpyHostToDevice, c.stream));
-      k::transpose_probes(c, X[2], V, n, b);
+      if (bk != b) std::fill(hbuf + (size_t)n * b, hbuf + (size_t)n * bk, 0.0);
+      SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(double) * (size_t)n * bk, cudaMemcpyHostToDevice, c.stream));
+      k::transpose_probes(c, X[2], V, n, bk);
       ctx_sync(c);  // hbuf consumed; the other buffer is free
       if (b0 + kBlock < count) next = std::async(std::launch::async, fill, b0 + kBlock, hb[(q + 1) & 1]);
       if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
-      k::kpm_step(c, s, a, b, 1, V, V, nullptr, X[0], cc, d, dz, 0);
+      k::kpm_step(c, s, a, bk, 1, V, V, nullptr, X[0], cc, d, dz, 0);
       const double* w0 = V;
       double *w1 = X[0], *tb = X[1], *spare = X[2];
       // doubling (default): step k gives w_{k+1} and the dots w_k.w_k, w_k.w_{k+1}, i.e. moments
@@ -578,7 +587,7 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
       const int last = doubling ? m / 2 : m;
       int launched = 1;
       for (int kk = doubling ? 1 : 2; kk <= last; ++kk, ++launched) {
-        k::kpm_step(c, s, a, b, doubling ? 2 : 0, V, w0, w1, tb, cc, d, dz, kk);
+        k::kpm_step(c, s, a, bk, doubling ? 2 : 0, V, w0, w1, tb, cc, d, dz, kk);
         double* freed = (w0 == V) ? spare : const_cast<double*>(w0);  // w0 <- w1 <- t <- free
         w0 = w1;
         w1 = tb;
@@ -593,25 +602,25 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
         c.filter_launches += launched;
         // block-step bytes: direct Abytes + 32 n b; doubling drops the probe
         // stream (Abytes + 24 n b)
-        c.filter_bytes += (double)launched * (a.abytes() + (doubling ? 24.0 : 32.0) * n * b);
+        c.filter_bytes += (double)launched * (a.abytes() + (doubling ? 24.0 : 32.0) * n * bk);
       }
       const int slots = doubling ? 2 * (last + 1) : m + 1;
-      SE_CUDA(cudaMemcpyAsync(hz.data(), dz, sizeof(double) * (size_t)slots * b,
+      SE_CUDA(cudaMemcpyAsync(hz.data(), dz, sizeof(double) * (size_t)slots * bk,
                               cudaMemcpyDeviceToHost, c.stream));
       ctx_sync(c);
       if (doubling) {  // zeta_2k = 2 w_k.w_k - zeta_0, zeta_2k+1 = 2 w_k.w_k+1 - zeta_1
         for (int j = 0; j < b; ++j) {
-          const double z0 = hz[j], z1 = hz[(size_t)b + j];
+          const double z0 = hz[j], z1 = hz[(size_t)bk + j];
           for (int kk = 2; kk <= m; ++kk) {
-            const double raw = hz[(size_t)kk * b + j];
-            hz[(size_t)kk * b + j] = 2.0 * raw - ((kk & 1) ? z1 : z0);
+            const double raw = hz[(size_t)kk * bk + j];
+            hz[(size_t)kk * bk + j] = 2.0 * raw - ((kk & 1) ? z1 : z0);
           }
         }
       }
       for (int j = 0; j < b; ++j)  // probe order (dos.hpp:100-106)
         for (int kk = 0; kk <= m; ++kk) {
-          zeta[kk] += hz[(size_t)kk * b + j];
-          if (per_probe) (*per_probe)[(size_t)(b0 + j) * (m + 1) + kk] = hz[(size_t)kk * b + j];
+          zeta[kk] += hz[(size_t)kk * bk + j];
+          if (per_probe) (*per_probe)[(size_t)(b0 + j) * (m + 1) + kk] = hz[(size_t)kk * bk + j];
         }
     }
   } catch (...) {

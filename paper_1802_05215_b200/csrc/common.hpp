@@ -29,6 +29,10 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 // ---- device matrices -----------------------------------------------------------------------
 // CSR in HBM: int32 row_ptr[n+1], int32 col_idx[nnz], f64 vals[nnz] (the reference layout,
 // csr.hpp:158-162) plus a per-tile nnz table used by the row-tile SpMV.
+// Rows of at most kEllW entries also get a padded copy (ell_c/ell_a, n x kEllW row-major; pad
+// col = row, val = 0) that the block KPM kernel reads instead of the CSR arrays.
+constexpr int kEllW = 8;
+
 struct DevCsr {
   int device = 0;
   int n = 0;
@@ -37,6 +41,8 @@ struct DevCsr {
   int* ci = nullptr;
   double* v = nullptr;
   int max_row_nnz = 0;
+  int* ell_c = nullptr;     // padded copy (max_row_nnz <= kEllW), else null
+  double* ell_a = nullptr;
   // vals and col_idx live in ONE allocation (vals first, col_idx right after) so a single L2
   // access-policy window covers the whole matrix stream of the filter SpMV
   void alloc_entries(long count);

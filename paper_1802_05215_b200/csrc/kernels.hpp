@@ -82,6 +82,8 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
 // Device Laplacian generator (laplacian.hpp:19-48 in closed form).
 void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a);
 void csr_scale_sym(Ctx& c, DevCsr& a, const double* d_dev);
+// (Re)build the padded-row copy the block KPM kernel reads (no-op when rows exceed kEllW).
+void build_ell(Ctx& c, DevCsr& a);
 int csr_max_row_nnz(Ctx& c, const DevCsr& a);
 
 // ---- Krylov kernels (orth.hpp, lanczos.hpp, eigensolvers.hpp) -----------------------------

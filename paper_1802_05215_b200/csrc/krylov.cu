@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads) k_gemvt(int n, int rch, const double
   const int g = blockIdx.x / nrb, rb = blockIdx.x - g * nrb;
   if (ncols <= 0 || g * kCW >= ncols) return;
   const int hcol = (hdiag && ctl) ? ctl->i : -1;
-  __shared__ double s_t[kMaxRch];
+  extern __shared__ double s_t[];  // rch doubles (dynamic: small items leave room for other CTAs)
   __shared__ bool s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = rb * rch, rn = min(rch, n - r0);
@@ -223,15 +223,15 @@ __global__ void __launch_bounds__(kThreads) k_gemvn(int n, const double* __restr
                                                     int pass2, int fixed,
                                                     const double* __restrict__ coef,
                                                     double* __restrict__ P, unsigned* rb_cnt,
-                                                    double* npart, unsigned* gcnt) {
+                                                    double* npart, unsigned* gcnt, int nw) {
   if (ctl && pass_skip(ctl, pass2)) return;
   const int ncols = pass_ncols(ctl, mode, fixed);
-  const int nchunks = (ncols + kNW - 1) / kNW;
+  const int nchunks = (ncols + nw - 1) / nw;
   const int rb = blockIdx.x, cc = blockIdx.y;
   if (ncols <= 0 || cc >= nchunks) return;
   __shared__ double s_c[kNW];
   __shared__ bool s_last;
-  const int j0 = cc * kNW, jn = min(kNW, ncols - j0);
+  const int j0 = cc * nw, jn = min(nw, ncols - j0);
   for (int q = threadIdx.x; q < jn; q += kThreads) s_c[q] = coef[j0 + q];
   __syncthreads();
   const int r = rb * kThreads + threadIdx.x;
@@ -396,6 +396,16 @@ int rch_for(int n) {
   return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512);
 }
 
+// columns per GEMV-N chunk (<= kNW)
+int nw_for() {
+  static const int nw = [] {
+    const char* e = std::getenv("SE_NW");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? std::min(v, kNW) : kNW;
+  }();
+  return nw;
+}
+
 }  // namespace
 
 // Scratch layout of a CGS pass: [GEMV-T partials nrb x cap][GEMV-N chunk partials nchunks x n]
@@ -404,7 +414,7 @@ size_t cgs_scratch_doubles(const Ctx& c, int n, int cap_cols) {
   const int rch = rch_for(n);
   const size_t nrb = (size_t)(n + rch - 1) / rch;
   const size_t gn = (size_t)(n + kThreads - 1) / kThreads;
-  const size_t ncc = (size_t)(std::max(cap_cols, 1) + kNW - 1) / kNW;
+  const size_t ncc = (size_t)(std::max(cap_cols, 1) + nw_for() - 1) / nw_for();
   return nrb * (size_t)std::max(cap_cols, 1) + ncc * (size_t)n + gn + (size_t)c.num_sms * 8 + 64;
 }
 
@@ -451,16 +461,16 @@ static void cgs_impl(Ctx& c, const Scratch& s, int n, double* t, const double* Q
   const int ngrp_max = (ldp + kCW - 1) / kCW;
   const int gn = (n + kThreads - 1) / kThreads;
   need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
-  const int ncc = (ldp + kNW - 1) / kNW;
+  const int ncc = (ldp + nw_for() - 1) / nw_for();
   double* part = s.buf;
   double* P = part + (size_t)nrb * ldp;
   double* npart = P + (size_t)ncc * n;
-  k_gemvt<<<nrb * ngrp_max, kThreads, 0, c.stream>>>(n, rch, Q, t, ctl, mode, pass2 ? 1 : 0, fixed,
+  k_gemvt<<<nrb * ngrp_max, kThreads, rch * sizeof(double), c.stream>>>(n, rch, Q, t, ctl, mode, pass2 ? 1 : 0, fixed,
                                                      part, ldp, s.cnt + kSlotGroups, coef, hdiag);
   ++c.launches;
   k_gemvn<<<dim3(gn, ncc), kThreads, 0, c.stream>>>(n, Q, t, ctl, mode, pass2 ? 1 : 0, fixed, coef, P,
                                                     s.cnt + kSlotGroups + ngrp_max, npart,
-                                                    s.cnt + kSlotMisc);
+                                                    s.cnt + kSlotMisc, nw_for());
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -473,7 +483,7 @@ void gemvt_only(Ctx& c, const Scratch& s, int n, const double* t, const double* 
   const int nrb = (n + rch - 1) / rch;
   const int ngrp_max = (ldp + kCW - 1) / kCW;
   need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
-  k_gemvt<<<nrb * ngrp_max, kThreads, 0, c.stream>>>(n, rch, Q, t, ctl, 0, pass2 ? 1 : 0, -1, s.buf,
+  k_gemvt<<<nrb * ngrp_max, kThreads, rch * sizeof(double), c.stream>>>(n, rch, Q, t, ctl, 0, pass2 ? 1 : 0, -1, s.buf,
                                                      ldp, s.cnt + kSlotGroups, coef, hdiag);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
@@ -487,13 +497,13 @@ void gemvn_only(Ctx& c, const Scratch& s, int n, double* t, const double* Q, boo
   const int nrb = (n + rch - 1) / rch;
   const int ngrp_max = (ldp + kCW - 1) / kCW;
   const int gn = (n + kThreads - 1) / kThreads;
-  const int ncc = (ldp + kNW - 1) / kNW;
+  const int ncc = (ldp + nw_for() - 1) / nw_for();
   need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
   double* P = s.buf + (size_t)nrb * ldp;
   double* npart = P + (size_t)ncc * n;
   k_gemvn<<<dim3(gn, ncc), kThreads, 0, c.stream>>>(n, Q, t, ctl, 0, pass2 ? 1 : 0, -1, coef, P,
                                                     s.cnt + kSlotGroups + ngrp_max, npart,
-                                                    s.cnt + kSlotMisc);
+                                                    s.cnt + kSlotMisc, nw_for());
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }

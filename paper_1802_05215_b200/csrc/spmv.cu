@@ -60,14 +60,15 @@ struct KArgs {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// One tile of kRows rows (see k_spmv_cheb).  `wait` = this is the CTA's first tile: the PDL wait
+// and the halt check happen once, after the first tile's A staging has been issued.
 template <int MODE>
-__global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restrict__ rp,
-                                                      const int* __restrict__ ci,
-                                                      const double* __restrict__ v, KArgs a) {
-  __shared__ __align__(16) double s_v[kChunk + 8];
-  __shared__ __align__(16) int s_c[kChunk + 8];
+__device__ __forceinline__ bool spmv_cheb_tile(int n, int tile, bool wait, const int* __restrict__ rp,
+                                               const int* __restrict__ ci,
+                                               const double* __restrict__ v, const KArgs& a,
+                                               double* s_v, int* s_c) {
   const size_t coff = (size_t)blockIdx.y * n;  // column of a column-major batch (kPlain)
-  const int r0 = blockIdx.x * kRows;
+  const int r0 = tile * kRows;
   const int r = r0 + threadIdx.x;
   const bool live = r < n;
   const int rend = min(r0 + kRows, n);
@@ -92,11 +93,13 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
     }
   };
   if (base < end) stage(base);
-  pdl_wait();
-  pdl_trigger();
-  if (a.halt && a.halt->halted) {
-    cp_async_wait_all();
-    return;
+  if (wait) {
+    pdl_wait();
+    pdl_trigger();
+    if (a.halt && a.halt->halted) {
+      cp_async_wait_all();
+      return false;
+    }
   }
   const size_t ioff = a.src_ctl ? (size_t)a.src_ctl->i * a.src_ld : 0;
   const double* __restrict__ x = a.x + coff + (a.x_indirect ? ioff : 0);
@@ -130,11 +133,11 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
     }
     __syncthreads();
   }
-  if (!live) return;
+  if (!live) return true;
   double* __restrict__ y = a.y + coff;
   if (MODE == kPlain) {
     y[r] = acc;
-    return;
+    return true;
   }
   // Ahat x = (A x - c x) * (1/d)   (filter_poly.hpp:265)
   const double t = mul(sub(acc, mul(a.c, xr)), a.invd);
@@ -147,6 +150,24 @@ __global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restric
     const double tj = sub(mul(2.0, t), pv);
     y[r] = tj;
     a.out[r] = add(ov, mul(a.muj, tj));
+  }
+  return true;
+}
+
+// Grid: one CTA per tile by default; a capped grid (SE_FILTER_CTAS) walks the tiles with a
+// stride, so a filter degree occupies fewer SM slots next to other slices' GEMV CTAs.
+template <int MODE>
+__global__ void __launch_bounds__(kRows) k_spmv_cheb(int n, const int* __restrict__ rp,
+                                                      const int* __restrict__ ci,
+                                                      const double* __restrict__ v, KArgs a) {
+  __shared__ __align__(16) double s_v[kChunk + 8];
+  __shared__ __align__(16) int s_c[kChunk + 8];
+  const int ntiles = (n + kRows - 1) / kRows;
+  bool first = true;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (!first) __syncthreads();  // the previous tile's readers of s_v / s_c are done
+    if (!spmv_cheb_tile<MODE>(n, tile, first, rp, ci, v, a, s_v, s_c)) return;
+    first = false;
   }
 }
 
@@ -235,6 +256,7 @@ __global__ void __launch_bounds__(kMRows * kMV) k_spmv_cheb_multi(int n, const i
 constexpr int kB = 16;
 constexpr int kKpmFirst = 1, kKpmDoubling = 2;  // 0: direct recurrence
 constexpr int kKpmThreads = 256;
+constexpr int kEllMinB = 3;  // resident CTAs per SM the ELL kernel is register-capped for
 
 constexpr int kKRows = 64;   // rows per tile: 16 half-warps x 4 rows
 constexpr int kKSlots = 512; // A entries (and gathered probe rows) staged per pass
@@ -543,6 +565,137 @@ __global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_stream(
   kpm_finish(f0, f1, b, first, dbl, partial, counter, zeta, kmom);
 }
 
+// Padded-row (ELL) block step: the default for matrices whose rows hold at most kEllW entries
+// (stencils).  The matrix is kept a second time as ec/ea[n][kEllW] (rows padded with col = row,
+// val = 0: acc + 0 * x leaves the storage-order sum unchanged), so a row's entries are two
+// 16-byte column loads and four 16-byte value loads that the 8 lanes of the row share (L1
+// broadcast): no row pointers, no shuffles, no per-entry predicates.  Column indices are loaded
+// two batches ahead; with the next batch's indices in registers, each lane prefetches one of that
+// batch's probe rows into L2, so a batch's gathers are (mostly) L2 hits.  The mode is a template argument (no runtime branches in the loop).
+// Same lane mapping as k_kpm_stream (8 lanes x 2 probes per row, 4 rows per warp), same sums.
+template <int MODE, int BC, int MINB>
+__global__ void __launch_bounds__(kKpmThreads, MINB) k_kpm_ell(
+    int n, const int* __restrict__ ec, const double* __restrict__ ea, int b_rt,
+    const double* __restrict__ v, const double* __restrict__ w0, const double* __restrict__ w1,
+    double* __restrict__ t, double cc, double d, double* __restrict__ partial, unsigned* counter,
+    double* __restrict__ zeta, int kmom) {
+  constexpr bool first = MODE == kKpmFirst, dbl = MODE == kKpmDoubling;
+  const int b = BC > 0 ? BC : b_rt;
+  const double dinv = 1.0 / d;
+  const int lane = threadIdx.x & 31, g = lane >> 3, l8 = lane & 7;
+  const bool live = 2 * l8 < b;
+  const double* __restrict__ src = first ? w0 : w1;
+  const int warps = (int)(gridDim.x * (kKpmThreads / 32));
+  const int nb = (n + 3) / 4;
+  int rb = (int)(blockIdx.x * (kKpmThreads / 32) + (threadIdx.x >> 5));
+  auto load_cols = [&](int rbq, int4& lo, int4& hi) {
+    const int r = 4 * rbq + g;
+    lo = make_int4(0, 0, 0, 0);
+    hi = lo;
+    if (rbq < nb && r < n) {
+      lo = __ldg(reinterpret_cast<const int4*>(ec + (size_t)r * kEllW));
+      hi = __ldg(reinterpret_cast<const int4*>(ec + (size_t)r * kEllW + 4));
+    }
+  };
+  int4 cl, ch, nl, nh;
+  load_cols(rb, cl, ch);
+  load_cols(rb + warps, nl, nh);
+  double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+  for (; rb < nb; rb += warps) {
+    int4 ml, mh;
+    load_cols(rb + 2 * warps, ml, mh);
+    {  // the next batch's probe rows (and its w0 rows) -> L2: lane (g, l8) takes entry l8 of row g
+      const int rn = 4 * (rb + warps) + g;
+      if (rb + warps < nb && rn < n) {
+        const int4 q = (l8 & 4) ? nh : nl;
+        const int cu = (l8 & 2) ? ((l8 & 1) ? q.w : q.z) : ((l8 & 1) ? q.y : q.x);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)cu * b));
+        if (!first && l8 == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + (size_t)rn * b));
+      }
+    }
+    const int r = 4 * rb + g;
+    if (r < n && live) {
+      const size_t o = (size_t)r * b + 2 * l8;
+      const int cs[kEllW] = {cl.x, cl.y, cl.z, cl.w, ch.x, ch.y, ch.z, ch.w};
+      double2 x[kEllW];
+#pragma unroll
+      for (int u = 0; u < kEllW; ++u)
+        x[u] = __ldg(reinterpret_cast<const double2*>(src + (size_t)cs[u] * b + 2 * l8));
+      const double2 xr = __ldg(reinterpret_cast<const double2*>(src + o));
+      double2 vr = make_double2(0.0, 0.0), pr = vr;
+      if (!dbl) vr = __ldg(reinterpret_cast<const double2*>(v + o));
+      if (!first) pr = __ldg(reinterpret_cast<const double2*>(w0 + o));
+      const double2* ap = reinterpret_cast<const double2*>(ea + (size_t)r * kEllW);
+      double av[kEllW];
+#pragma unroll
+      for (int q = 0; q < kEllW / 2; ++q) {
+        const double2 e = __ldg(ap + q);
+        av[2 * q] = e.x;
+        av[2 * q + 1] = e.y;
+      }
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < kEllW; ++u) {
+        acc.x = add(acc.x, mul(av[u], x[u].x));
+        acc.y = add(acc.y, mul(av[u], x[u].y));
+      }
+      // (A w - c w) / d   (dos.hpp:99)
+      const double2 m = make_double2(div_by(sub(acc.x, mul(cc, xr.x)), d, dinv),
+                                     div_by(sub(acc.y, mul(cc, xr.y)), d, dinv));
+      double2* to = reinterpret_cast<double2*>(t + o);
+      if (first) {
+        *to = m;
+        a0.x = add(a0.x, mul(vr.x, xr.x));
+        a0.y = add(a0.y, mul(vr.y, xr.y));
+        a1.x = add(a1.x, mul(vr.x, m.x));
+        a1.y = add(a1.y, mul(vr.y, m.y));
+      } else {
+        const double2 tk = make_double2(sub(mul(2.0, m.x), pr.x), sub(mul(2.0, m.y), pr.y));
+        *to = tk;
+        if (dbl) {
+          a0.x = add(a0.x, mul(xr.x, xr.x));
+          a0.y = add(a0.y, mul(xr.y, xr.y));
+          a1.x = add(a1.x, mul(xr.x, tk.x));
+          a1.y = add(a1.y, mul(xr.y, tk.y));
+        } else {
+          a0.x = add(a0.x, mul(vr.x, tk.x));
+          a0.y = add(a0.y, mul(vr.y, tk.y));
+        }
+      }
+    }
+    cl = nl;
+    ch = nh;
+    nl = ml;
+    nh = mh;
+  }
+  __shared__ double s_a0[kKpmThreads / 8][kB], s_a1[kKpmThreads / 8][kB];
+  const int grp = threadIdx.x >> 3;
+  s_a0[grp][2 * l8] = a0.x;
+  s_a0[grp][2 * l8 + 1] = a0.y;
+  s_a1[grp][2 * l8] = a1.x;
+  s_a1[grp][2 * l8 + 1] = a1.y;
+  __syncthreads();
+  const int h = threadIdx.x / kB, j = threadIdx.x % kB;
+  const double f0 = add(s_a0[2 * h][j], s_a0[2 * h + 1][j]);
+  const double f1 = add(s_a1[2 * h][j], s_a1[2 * h + 1][j]);
+  __syncthreads();
+  kpm_finish(f0, f1, b, first, dbl, partial, counter, zeta, kmom);
+}
+
+// CSR -> padded rows (kEllW per row; pad col = row, val = 0), one thread per row
+__global__ void k_build_ell(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, int* __restrict__ ec, double* __restrict__ ea) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int p = rp[r], e = rp[r + 1];
+#pragma unroll
+  for (int u = 0; u < kEllW; ++u) {
+    const bool in = p + u < e;
+    ec[(size_t)r * kEllW + u] = in ? ci[p + u] : r;
+    ea[(size_t)r * kEllW + u] = in ? v[p + u] : 0.0;
+  }
+}
+
 // probe-major (b x n) -> row-major (n x b), 32 rows per CTA through shared memory
 __global__ void __launch_bounds__(256) k_transpose_probes(const double* __restrict__ pm,
                                                           double* __restrict__ rm, int n, int b) {
@@ -624,7 +777,12 @@ void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
     k.x_indirect = (mode == kFirst || mode == kPlain);
     k.prev_indirect = (mode == kNext);
   }
-  dim3 grid((a.n + kRows - 1) / kRows, mode == kPlain ? args.ncols : 1);
+  static const int cap = [] {
+    const char* e = std::getenv("SE_FILTER_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int ntiles = (a.n + kRows - 1) / kRows;
+  dim3 grid(cap > 0 ? std::min(cap, ntiles) : ntiles, mode == kPlain ? args.ncols : 1);
   static const bool pdl = std::getenv("SE_NO_PDL") == nullptr;
   // The filter chain is latency-bound (k dependent launches per Lanczos step) while the slices'
   // reorthogonalisation passes sharing the GPU are bandwidth-bound: filter launches (and their
@@ -718,11 +876,42 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
   if (kpm_scratch_doubles(c, a.n) > s.cap || s.ncnt < 1) fail(SE_EINVAL, "internal: kpm scratch");
   // default: the pipelined direct-gather kernel (even probe counts); odd counts take the
   // shared-memory tile kernel.  SE_KPM_KERNEL=tile forces the latter (A/B comparisons).
-  static const bool force_tile = [] {
+  static const int variant = [] {  // 0: ELL (default when built), 1: CSR stream, 2: CSR tile
     const char* e = std::getenv("SE_KPM_KERNEL");
-    return e && std::string(e) == "tile";
+    if (!e) return 0;
+    return std::string(e) == "tile" ? 2 : std::string(e) == "stream" ? 1 : 0;
   }();
-  if (!force_tile && b % 2 == 0) {
+  if (variant == 0 && a.ell_c && b % 2 == 0) {
+    static const int minb = [] {  // SE_KPM_MINB=2: 128-register variant (2 CTAs per SM)
+      const char* e = std::getenv("SE_KPM_MINB");
+      return e && std::atoi(e) == 2 ? 2 : kEllMinB;
+    }();
+    using EFn = decltype(&k_kpm_ell<0, 16, kEllMinB>);
+    auto pick = [&](auto md, auto mb) -> EFn {
+      constexpr int M = decltype(md)::value, B = decltype(mb)::value;
+      return b == 16 ? k_kpm_ell<M, 16, B> : b == 8 ? k_kpm_ell<M, 8, B> : k_kpm_ell<M, 0, B>;
+    };
+    auto pick_mode = [&](auto mb) -> EFn {
+      return mode == kKpmFirst      ? pick(std::integral_constant<int, kKpmFirst>{}, mb)
+             : mode == kKpmDoubling ? pick(std::integral_constant<int, kKpmDoubling>{}, mb)
+                                    : pick(std::integral_constant<int, 0>{}, mb);
+    };
+    const EFn kern = minb == 2 ? pick_mode(std::integral_constant<int, 2>{})
+                               : pick_mode(std::integral_constant<int, kEllMinB>{});
+    static const int per_sm = [&] {
+      int v = 0;
+      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &v, minb == 2 ? k_kpm_ell<kKpmDoubling, 16, 2> : k_kpm_ell<kKpmDoubling, 16, kEllMinB>, kKpmThreads, 0));
+      return std::max(1, v);
+    }();
+    const int grid = std::max(1, std::min(c.num_sms * per_sm, (a.n + 31) / 32));
+    kern<<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.ell_c, a.ell_a, b, v, w0, w1, t, cc, d, s.buf, s.cnt,
+                                             zeta_dev, kmom);
+    ++c.launches;
+    SE_CUDA(cudaGetLastError());
+    return;
+  }
+  if (variant != 2 && b % 2 == 0) {
     static const int per_sm = [] {
       int v = 0;
       SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_stream<8, 0>, kKpmThreads, 0));
@@ -751,6 +940,17 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
   SE_CUDA(cudaGetLastError());
 }
 
+void build_ell(Ctx& c, DevCsr& a) {
+  if (a.n == 0 || a.max_row_nnz > kEllW) return;
+  if (!a.ell_c) {
+    a.ell_c = dev_alloc_shared<int>((size_t)a.n * kEllW);
+    a.ell_a = dev_alloc_shared<double>((size_t)a.n * kEllW);
+  }
+  k_build_ell<<<(a.n + 255) / 256, 256, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, a.ell_c, a.ell_a);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
 void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
   Grid g{dims[0], ndims > 1 ? dims[1] : 1, ndims > 2 ? dims[2] : 1, ndims};
   const long nl = (long)g.nx * g.ny * g.nz;
@@ -775,6 +975,7 @@ void gen_laplacian(Ctx& c, int ndims, const int* dims, DevCsr& a) {
   ++c.launches;
   SE_CUDA(cudaGetLastError());
   a.max_row_nnz = 1 + 2 * ndims;
+  build_ell(c, a);
 }
 
 void csr_scale_sym(Ctx& c, DevCsr& a, const double* d_dev) {
@@ -782,6 +983,7 @@ void csr_scale_sym(Ctx& c, DevCsr& a, const double* d_dev) {
   k_scale_sym<<<(a.n + 255) / 256, 256, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, d_dev);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
+  build_ell(c, a);  // the padded copy follows the scaled values
 }
 
 int csr_max_row_nnz(Ctx& c, const DevCsr& a) {

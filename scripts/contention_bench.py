@@ -30,3 +30,27 @@ for T in (1, 3, 7):
     stop.set()
     for t in th: t.join()
     print(f"with {T} CGS threads: {us:.2f} us/launch")
+
+# Reverse direction: the CGS pass (HBM-bound) while T threads replay filter chains -- if the
+# filters' matrix/vector traffic reaches HBM under load, the pass slows by that bandwidth share.
+def cgs(ctx, reps=40):
+    ms = C.c_double()
+    _lib.call("se_cgs_bench", ctx.handle, 262144, 1440, reps, C.byref(ms))
+    return ms.value / reps * 1e3
+
+print(f"CGS pass alone: {cgs(ctx):.1f} us")
+for T in (1, 3, 7):
+    stop = threading.Event()
+    def fload():
+        c2 = api.Context(0)
+        A2 = api.DeviceCsr.laplacian([64, 64, 64], c2)
+        while not stop.is_set():
+            filt(c2, A2, f, 2)
+        c2.close()
+    th = [threading.Thread(target=fload) for _ in range(T)]
+    for t in th: t.start()
+    time.sleep(4.0)
+    us = cgs(ctx)
+    stop.set()
+    for t in th: t.join()
+    print(f"CGS pass with {T} filter threads: {us:.1f} us")

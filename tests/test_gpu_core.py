@@ -124,3 +124,21 @@ def test_laplacian_60x60_window(gpu_ctx, driver):
         lam, res = api.rayleigh_and_residual(a, None, r.vectors[:, i])
         assert abs(lam - r.eigenvalues[i]) <= 1e-10
         assert abs(res - r.residuals[i]) <= 1e-10
+
+
+@pytest.mark.parametrize("variant", ["ell", "stream", "tile"])
+def test_kpm_kernel_variants(gpu_ctx, variant):
+    """Every block-KPM kernel (padded-row default, CSR stream, CSR tile) against the oracle on
+    stencils and an irregular matrix with 0..8 entries per row (empty rows included), with full
+    (16), ragged (21 = 16 + 5) and narrow (6) probe blocks."""
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SE_KPM_KERNEL=variant,
+               PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")]))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "_kpm_variant_case.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(errs) == 9
+    for k, e in errs.items():
+        assert e <= 1e-12, (variant, k, e)
