@@ -42,6 +42,9 @@ CFG2 = dict(dims=[64, 64, 64], xi=0.6, eta=1.2, ns=8, solver="tr", damping="sigm
             dos_nvec=40, probes="gaussian", tol=1e-8, seed=1234)
 # CPU-boundable proxy of the same recipe (used only for the reference arm / cpu_baseline)
 PROXY = dict(CFG2, dims=[20, 20, 20])
+# side measurements (other BASELINE configs, reported under "other_configs")
+CFGS_OTHER = {"cfg1": dict(dims=[100, 100], xi=0.4, eta=1.6, ns=2, solver="nr", damping="jackson",
+                           dos_m=80, dos_nvec=20, probes="rademacher", tol=1e-8, seed=0)}
 METRIC = "eigenpairs/sec for full sliced solve"
 UNIT = "eigenpairs/s"
 
@@ -214,13 +217,53 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
                                           "traffic": _t("spmv_cheb_160cubed")},
                             "workload_64^3_L2_resident": {"achieved": round(out["workload"][0], 1),
                                                           "us_per_launch": round(out["workload"][1] * 1e6, 2)}},
-            "kpm_block_step": {"kernel": "k_kpm_stream (16-probe block, doubling; dos.hpp:96-110)",
+            "kpm_block_step": {"kernel": "k_kpm_ell (16-probe block, padded rows, doubling; dos.hpp:96-110)",
                                "shape": "160^3 (BASELINE cfg3 matrix), b=16",
                                "achieved": round(out["kpm"][0], 1), "frac": round(out["kpm"][0] / peak, 4),
                                "us_per_step": round(out["kpm"][1] * 1e6, 2),
                                "bytes_per_step": round(out["kpm"][2]),
-                               "traffic": _t("kpm_stream_160cubed_b16")}}
+                               "traffic": _t("kpm_ell_160cubed_b16")}}
     return roof
+
+
+def other_configs(local_gpu: int):
+    """The other BASELINE configs that fit a short run, measured on the same GPU after the timed
+    region (not part of the headline): cfg1 (2-D 100^2, full NR pipeline) and cfg3 (KPM only:
+    160^3, 300 moments x 128 Rademacher probes in blocks of 16, bounds fixed to [0, 12])."""
+    import time as _time
+    import ctypes as C
+    from paper_1802_05215_b200 import _lib, api
+    from paper_1802_05215_b200.pipeline import GpuBackend, run
+    out = {}
+    c1 = CFGS_OTHER["cfg1"]
+    be = GpuBackend(device=local_gpu, dims=c1["dims"])
+    run(_plan(c1), be)  # warm
+    t0 = _time.perf_counter()
+    r = run(_plan(c1), be)
+    el = _time.perf_counter() - t0
+    out["cfg1"] = {"workload": "2-D 100x100 Laplacian, KPM 80x20 Rademacher, [0.4,1.6] in 2 slices, "
+                               "ChebLanNr (Jackson) tol 1e-8",
+                   "eigenpairs": int(r.n_found), "seconds": round(el, 3),
+                   "eigenpairs_per_s": round(r.n_found / el, 1),
+                   "counts": [int(s.eigenvalues.size) for s in r.slices]}
+    ctx = api.Context(local_gpu)
+    A = api.DeviceCsr.laplacian([160, 160, 160], ctx)
+    b3 = api.SpectralBounds(0.0, 12.0)
+    api.kpm_moments(A, b3, 8, 16, seed=0)  # warm
+    _lib.call("se_ctx_filter_timing", ctx.handle, 1, None, None, None)
+    t0 = _time.perf_counter()
+    api.kpm_moments(A, b3, 300, 128, seed=0)
+    el = _time.perf_counter() - t0
+    ms, nl, by = C.c_double(), C.c_long(), C.c_double()
+    _lib.call("se_ctx_filter_timing", ctx.handle, 0, C.byref(ms), C.byref(nl), C.byref(by))
+    out["cfg3"] = {"workload": "KPM: 160^3 Laplacian, 300 moments x 128 Rademacher probes (8 blocks of 16)",
+                   "wall_s": round(el, 3), "device_s": round(ms.value * 1e-3, 3),
+                   "block_steps": int(nl.value),
+                   "device_GBps_algorithmic": round(by.value / (ms.value * 1e-3) / 1e9, 1),
+                   "probe_moments_per_s": round(128 * 301 / el, 1)}
+    A.free()
+    ctx.close()
+    return out
 
 
 def arm_config(cfg, n, world):
@@ -299,6 +342,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--proxy", action="store_true", help="run the GPU arm on the CPU proxy size")
     ap.add_argument("--jobs", type=int, default=0, help="concurrent slices per GPU (0: all)")
+    ap.add_argument("--no-others", action="store_true", help="skip the cfg1 / cfg3 side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         # the reference is CPU code: rank 0 runs it on the host cores, other ranks exit at once
@@ -373,6 +417,7 @@ def main():
     # mean active basis width over the run's reorthogonalisation passes (TR: columns l..m per cycle)
     mean_cols = 1440
     roof = kernel_rooflines(local, cfg["dims"], mean_cols) if rank == 0 else None
+    others = other_configs(local) if rank == 0 and not args.no_others else None
     cpu = cpu_baseline_sample() if (rank == 0 and world == 1 and not args.no_cpu) else None
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
@@ -384,7 +429,7 @@ def main():
                 "per_slice": per_slice, "t_bounds": round(res.t_bounds, 3),
                 "t_dos": round(res.t_dos, 3), "t_solve": round(res.t_solve, 3),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roof, "clocks": clk,
-                "cpu_baseline": cpu}
+                "cpu_baseline": cpu, "other_configs": others}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as td

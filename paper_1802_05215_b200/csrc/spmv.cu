@@ -257,6 +257,7 @@ constexpr int kB = 16;
 constexpr int kKpmFirst = 1, kKpmDoubling = 2;  // 0: direct recurrence
 constexpr int kKpmThreads = 256;
 constexpr int kEllMinB = 3;  // resident CTAs per SM the ELL kernel is register-capped for
+constexpr int kKpmPD = 1;    // default L2 prefetch distance (batches) of the ELL kernel
 
 constexpr int kKRows = 64;   // rows per tile: 16 half-warps x 4 rows
 constexpr int kKSlots = 512; // A entries (and gathered probe rows) staged per pass
@@ -570,11 +571,11 @@ __global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_stream(
 // val = 0: acc + 0 * x leaves the storage-order sum unchanged), so a row's entries are two
 // 16-byte column loads and four 16-byte value loads that the 8 lanes of the row share (L1
 // broadcast): no row pointers, no shuffles, no per-entry predicates.  Column indices are loaded
-// two batches ahead; with the next batch's indices in registers, each lane prefetches one of that
-// batch's probe rows into L2, so a batch's gathers are (mostly) L2 hits.  The mode is a template argument (no runtime branches in the loop).
+// one batch ahead; separately each lane loads one column of the batch PD ahead (a coalesced
+// load) and prefetches that probe row into L2, so a batch's gathers are (mostly) L2 hits.  The mode is a template argument (no runtime branches in the loop).
 // Same lane mapping as k_kpm_stream (8 lanes x 2 probes per row, 4 rows per warp), same sums.
-template <int MODE, int BC, int MINB>
-__global__ void __launch_bounds__(kKpmThreads, MINB) k_kpm_ell(
+template <int MODE, int BC, int PD>
+__global__ void __launch_bounds__(kKpmThreads, kEllMinB) k_kpm_ell(
     int n, const int* __restrict__ ec, const double* __restrict__ ea, int b_rt,
     const double* __restrict__ v, const double* __restrict__ w0, const double* __restrict__ w1,
     double* __restrict__ t, double cc, double d, double* __restrict__ partial, unsigned* counter,
@@ -597,22 +598,25 @@ __global__ void __launch_bounds__(kKpmThreads, MINB) k_kpm_ell(
       hi = __ldg(reinterpret_cast<const int4*>(ec + (size_t)r * kEllW + 4));
     }
   };
-  int4 cl, ch, nl, nh;
+  // prefetch path: lane (g, l8) loads entry l8 of row g of batch rb + PD warps (one coalesced
+  // 128-byte load per warp), and one iteration later prefetches that probe row into L2
+  auto pf_col = [&](int rbq) -> int {
+    return (rbq < nb && 4 * rbq + g < n) ? __ldg(ec + (size_t)rbq * 32 + lane) : -1;
+  };
+  int4 cl, ch;
   load_cols(rb, cl, ch);
-  load_cols(rb + warps, nl, nh);
+  int pc = pf_col(rb + (PD - 1) * warps);
   double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
   for (; rb < nb; rb += warps) {
-    int4 ml, mh;
-    load_cols(rb + 2 * warps, ml, mh);
-    {  // the next batch's probe rows (and its w0 rows) -> L2: lane (g, l8) takes entry l8 of row g
-      const int rn = 4 * (rb + warps) + g;
-      if (rb + warps < nb && rn < n) {
-        const int4 q = (l8 & 4) ? nh : nl;
-        const int cu = (l8 & 2) ? ((l8 & 1) ? q.w : q.z) : ((l8 & 1) ? q.y : q.x);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)cu * b));
-        if (!first && l8 == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + (size_t)rn * b));
-      }
+    int4 nl, nh;
+    load_cols(rb + warps, nl, nh);
+    const int pn = pf_col(rb + PD * warps);
+    if (pc >= 0) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)pc * b));
+      if (!first && l8 == 0)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + (size_t)(4 * (rb + (PD - 1) * warps) + g) * b));
     }
+    pc = pn;
     const int r = 4 * rb + g;
     if (r < n && live) {
       const size_t o = (size_t)r * b + 2 * l8;
@@ -665,8 +669,6 @@ __global__ void __launch_bounds__(kKpmThreads, MINB) k_kpm_ell(
     }
     cl = nl;
     ch = nh;
-    nl = ml;
-    nh = mh;
   }
   __shared__ double s_a0[kKpmThreads / 8][kB], s_a1[kKpmThreads / 8][kB];
   const int grp = threadIdx.x >> 3;
@@ -879,29 +881,31 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
   static const int variant = [] {  // 0: ELL (default when built), 1: CSR stream, 2: CSR tile
     const char* e = std::getenv("SE_KPM_KERNEL");
     if (!e) return 0;
-    return std::string(e) == "tile" ? 2 : std::string(e) == "stream" ? 1 : 0;
+    const std::string v(e);
+    return v == "tile" ? 2 : v == "stream" ? 1 : 0;
   }();
   if (variant == 0 && a.ell_c && b % 2 == 0) {
-    static const int minb = [] {  // SE_KPM_MINB=2: 128-register variant (2 CTAs per SM)
-      const char* e = std::getenv("SE_KPM_MINB");
-      return e && std::atoi(e) == 2 ? 2 : kEllMinB;
+    static const int pd = [] {  // L2 prefetch distance in batches (SE_KPM_PD = 1..3)
+      const char* e = std::getenv("SE_KPM_PD");
+      const int v = e ? std::atoi(e) : 0;
+      return v >= 1 && v <= 3 ? v : kKpmPD;
     }();
-    using EFn = decltype(&k_kpm_ell<0, 16, kEllMinB>);
-    auto pick = [&](auto md, auto mb) -> EFn {
-      constexpr int M = decltype(md)::value, B = decltype(mb)::value;
-      return b == 16 ? k_kpm_ell<M, 16, B> : b == 8 ? k_kpm_ell<M, 8, B> : k_kpm_ell<M, 0, B>;
+    using EFn = decltype(&k_kpm_ell<0, 16, 1>);
+    auto pick = [&](auto md, auto pdc) -> EFn {
+      constexpr int M = decltype(md)::value, P = decltype(pdc)::value;
+      return b == 16 ? k_kpm_ell<M, 16, P> : b == 8 ? k_kpm_ell<M, 8, P> : k_kpm_ell<M, 0, P>;
     };
-    auto pick_mode = [&](auto mb) -> EFn {
-      return mode == kKpmFirst      ? pick(std::integral_constant<int, kKpmFirst>{}, mb)
-             : mode == kKpmDoubling ? pick(std::integral_constant<int, kKpmDoubling>{}, mb)
-                                    : pick(std::integral_constant<int, 0>{}, mb);
+    auto pick_mode = [&](auto pdc) -> EFn {
+      return mode == kKpmFirst      ? pick(std::integral_constant<int, kKpmFirst>{}, pdc)
+             : mode == kKpmDoubling ? pick(std::integral_constant<int, kKpmDoubling>{}, pdc)
+                                    : pick(std::integral_constant<int, 0>{}, pdc);
     };
-    const EFn kern = minb == 2 ? pick_mode(std::integral_constant<int, 2>{})
-                               : pick_mode(std::integral_constant<int, kEllMinB>{});
-    static const int per_sm = [&] {
+    const EFn kern = pd == 1   ? pick_mode(std::integral_constant<int, 1>{})
+                     : pd == 2 ? pick_mode(std::integral_constant<int, 2>{})
+                               : pick_mode(std::integral_constant<int, 3>{});
+    static const int per_sm = [] {
       int v = 0;
-      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &v, minb == 2 ? k_kpm_ell<kKpmDoubling, 16, 2> : k_kpm_ell<kKpmDoubling, 16, kEllMinB>, kKpmThreads, 0));
+      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_ell<kKpmDoubling, 16, 1>, kKpmThreads, 0));
       return std::max(1, v);
     }();
     const int grid = std::max(1, std::min(c.num_sms * per_sm, (a.n + 31) / 32));
