@@ -1,6 +1,8 @@
 // extern "C" boundary of libsliceeig_cuda.so (declarations: include/sliceeig_cuda.h).
 // Every entry point converts exceptions into SE_* status codes + a thread-local message.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <future>
@@ -555,28 +557,47 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
   // Two pinned staging buffers: the host draws block q+1 (one mt19937_64 stream, probe order)
   // while the device runs the m-step recurrence of block q.
   double* hb[2] = {nullptr, nullptr};
-  SE_CUDA(cudaMallocHost(&hb[0], sizeof(double) * blk));
-  SE_CUDA(cudaMallocHost(&hb[1], sizeof(double) * blk));
+  // staging: a block of double probes (Gaussian) or of sign bits (Rademacher, 1/64 the size;
+  // pinning host memory costs ~0.2 ms per MB, so the bit path stays cheap)
+  const size_t hcap = gaussian ? blk : (size_t)kBlock * (((size_t)n + 63) / 64);
+  SE_CUDA(cudaMallocHost(&hb[0], sizeof(double) * hcap));
+  SE_CUDA(cudaMallocHost(&hb[1], sizeof(double) * hcap));
   double* hbuf = hb[0];
   Vec hz((size_t)(m + 3) * kBlock);
   auto fill = [&](int b0, double* buf) {
     // probe j = the next n values of the one stream (probe order), probe-major; the device
-    // transposes the block to the row-major layout the kernels read
-    fill_probes(rng, gaussian, n, std::min(kBlock, count - b0), buf);
+    // transposes the block to the row-major layout the kernels read.  Rademacher probes travel
+    // as sign bits (n / 8 bytes per probe) and are expanded on the device.
+    if (gaussian)
+      fill_probes(rng, gaussian, n, std::min(kBlock, count - b0), buf);
+    else
+      fill_rademacher_bits(rng, n, std::min(kBlock, count - b0), reinterpret_cast<std::uint64_t*>(buf));
   };
+  static const bool trace = std::getenv("SE_KPM_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(); };
   std::future<void> next = std::async(std::launch::async, fill, 0, hb[0]);
   try {
     for (int b0 = 0, q = 0; b0 < count; b0 += kBlock, ++q) {
       const int b = std::min(kBlock, count - b0);
+      if (trace) std::fprintf(stderr, "[kpm] block %d wait-fill at %.1f ms\n", q, since());
       // odd blocks carry one zero probe column (its moments are dropped): every row of the
       // row-major block is then 16-byte aligned for the kernels' paired loads
       const int bk = b + (b & 1);
       next.get();
       hbuf = hb[q & 1];
-      if (bk != b) std::fill(hbuf + (size_t)n * b, hbuf + (size_t)n * bk, 0.0);
-      SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(double) * (size_t)n * bk, cudaMemcpyHostToDevice, c.stream));
-      k::transpose_probes(c, X[2], V, n, bk);
+      if (gaussian) {
+        if (bk != b) std::fill(hbuf + (size_t)n * b, hbuf + (size_t)n * bk, 0.0);
+        SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(double) * (size_t)n * bk, cudaMemcpyHostToDevice, c.stream));
+        k::transpose_probes(c, X[2], V, n, bk);
+      } else {
+        const size_t words = ((size_t)n + 63) / 64;
+        SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(std::uint64_t) * words * b, cudaMemcpyHostToDevice, c.stream));
+        k::expand_rademacher(c, reinterpret_cast<const std::uint64_t*>(X[2]), V, n, b, bk);
+      }
+      if (trace) std::fprintf(stderr, "[kpm] block %d filled at %.1f ms\n", q, since());
       ctx_sync(c);  // hbuf consumed; the other buffer is free
+      if (trace) std::fprintf(stderr, "[kpm] block %d staged at %.1f ms\n", q, since());
       if (b0 + kBlock < count) next = std::async(std::launch::async, fill, b0 + kBlock, hb[(q + 1) & 1]);
       if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
       k::kpm_step(c, s, a, bk, 1, V, V, nullptr, X[0], cc, d, dz, 0);

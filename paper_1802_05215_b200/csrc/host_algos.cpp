@@ -65,6 +65,25 @@ void fill_probes(Rng& rng, bool gaussian, int n, int b, double* out) {
   for (int l = 0; l < b; ++l) draw(rng, out + (size_t)l * n);
 }
 
+void fill_rademacher_bits(Rng& rng, int n, int b, std::uint64_t* out) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t words = ((size_t)n + 63) / 64;
+  if (b > 1 && hw > 1 && (long)n * b >= (1L << 21)) {
+    std::vector<Rng> loc((size_t)b, rng);
+    std::vector<std::thread> th;
+    th.reserve((size_t)b);
+    for (int l = 0; l < b; ++l)
+      th.emplace_back([&, l] {
+        if (l) loc[(size_t)l].jump_draws(jump_poly((std::uint64_t)l * (std::uint64_t)n));
+        loc[(size_t)l].rademacher_bits(out + (size_t)l * words, n);
+      });
+    for (auto& t : th) t.join();
+    rng = loc[(size_t)b - 1];
+    return;
+  }
+  for (int l = 0; l < b; ++l) rng.rademacher_bits(out + (size_t)l * words, n);
+}
+
 void skip_probes(Rng& rng, bool gaussian, int n, long count) {
   if (count <= 0) return;
   if (!gaussian || (n % 2 == 0 && !rng.spare_pending())) {

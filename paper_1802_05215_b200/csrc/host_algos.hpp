@@ -25,6 +25,15 @@ class Rng {
   void rademacher_fill(double* out, long n) {
     for (long i = 0; i < n; ++i) out[i] = rademacher();
   }
+  // the signs of the next n Rademacher draws as bits (bit i of word i / 64: 1 -> +1, 0 -> -1)
+  void rademacher_bits(std::uint64_t* out, long n) {
+    for (long w = 0; w * 64 < n; ++w) {
+      const int lim = (int)std::min<long>(64, n - w * 64);
+      std::uint64_t word = 0;
+      for (int q = 0; q < lim; ++q) word |= (g_() & 1u) << q;
+      out[w] = word;
+    }
+  }
   // advance the engine by j draws (jump-ahead for large j); the Box-Muller spare is untouched
   void discard_draws(std::uint64_t j) { g_.discard(j); }
   void jump_draws(const std::vector<std::uint64_t>& g) { g_.jump(g); }
@@ -43,6 +52,9 @@ class Rng {
 // probes by jump-ahead when that is exact (Rademacher; Gaussian with n even and no pending
 // spare -- then every probe is exactly n draws); otherwise, or on a Box-Muller redraw, serial.
 void fill_probes(Rng& rng, bool gaussian, int n, int b, double* out);
+// Rademacher probes [0, b) as sign bits: probe l at out + l * ((n + 63) / 64) (same stream,
+// same jump-ahead threading; 1/64 of the host memory traffic of the double layout).
+void fill_rademacher_bits(Rng& rng, int n, int b, std::uint64_t* out);
 // Skip `count` probes of n values each (jump-ahead when exact, else serial draws).
 void skip_probes(Rng& rng, bool gaussian, int n, long count);
 

@@ -75,6 +75,9 @@ size_t kpm_scratch_doubles(const Ctx& c, int n);
 // 2: doubling (t = w_{k+1}; w_k.w_k -> slot 2 kmom, w_k.w_{k+1} -> slot 2 kmom + 1).
 // rm[i b + l] = pm[l n + i]: a probe-major host block to the row-major device layout
 void transpose_probes(Ctx& c, const double* pm, double* rm, int n, int b);
+// Rademacher sign bits (probe-major, (n + 63) / 64 words per probe; bit set -> +1) -> row-major
+// n x bk doubles, columns b .. bk-1 zero.
+void expand_rademacher(Ctx& c, const std::uint64_t* bits, double* rm, int n, int b, int bk);
 void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const double* v,
               const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
               int kmom);

@@ -698,6 +698,18 @@ __global__ void k_build_ell(int n, const int* __restrict__ rp, const int* __rest
   }
 }
 
+// Rademacher sign bits (probe-major, W words per probe) -> row-major n x bk doubles (+1 / -1;
+// columns b .. bk-1 zero)
+__global__ void k_expand_rademacher(const unsigned long long* __restrict__ bits, long W,
+                                    double* __restrict__ rm, int n, int b, int bk) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long)n * bk) return;
+  const int i = (int)(e / bk), l = (int)(e - (long)i * bk);
+  double v = 0.0;
+  if (l < b) v = ((__ldg(bits + l * W + (i >> 6)) >> (i & 63)) & 1ull) ? 1.0 : -1.0;
+  rm[e] = v;
+}
+
 // probe-major (b x n) -> row-major (n x b), 32 rows per CTA through shared memory
 __global__ void __launch_bounds__(256) k_transpose_probes(const double* __restrict__ pm,
                                                           double* __restrict__ rm, int n, int b) {
@@ -860,6 +872,16 @@ void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args) {
   if (args.nv > kMV) fail(SE_EINVAL, "spmv_cheb_multi: too many vectors");
   k_spmv_cheb_multi<<<(a.n + kMRows - 1) / kMRows, kMRows * kMV, 0, c.stream>>>(a.n, a.rp, a.ci,
                                                                                 a.v, args);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+void expand_rademacher(Ctx& c, const std::uint64_t* bits, double* rm, int n, int b, int bk) {
+  if (n == 0 || bk == 0) return;
+  if (bk > kB || b > bk) fail(SE_EINVAL, "expand_rademacher: block too wide");
+  const long tot = (long)n * bk;
+  k_expand_rademacher<<<(unsigned)((tot + 255) / 256), 256, 0, c.stream>>>(
+      reinterpret_cast<const unsigned long long*>(bits), ((long)n + 63) / 64, rm, n, b, bk);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }

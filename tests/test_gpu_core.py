@@ -142,3 +142,20 @@ def test_kpm_kernel_variants(gpu_ctx, variant):
     assert len(errs) == 9
     for k, e in errs.items():
         assert e <= 1e-12, (variant, k, e)
+
+
+def test_kpm_rademacher_threaded_bits_match_oracle(gpu_ctx):
+    """Large enough (n b >= 2^21) that the host draws each probe's sign bits on its own thread
+    from a jumped-ahead stream: moments still match the oracle's serial draws; a ragged second
+    block (16 + 3) and a later first probe (rank offset) too."""
+    api = _api()
+    a = api.gen_laplacian([64, 64, 64])
+    lo, hi = 0.0, 12.0
+    z = api.kpm_moments(a, api.SpectralBounds(lo, hi), 12, 19, seed=5)
+    zr = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, lo, hi, 12, 19, 5)
+    tol = 1e-12 * np.maximum(np.abs(zr), abs(zr[0]))
+    assert np.all(np.abs(z - zr) <= tol), np.max(np.abs(z - zr) / abs(zr[0]))
+    z2 = api.kpm_moments(a, api.SpectralBounds(lo, hi), 12, 19, seed=5, first=3, count=16)
+    zr2 = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, lo, hi, 12, 19, 5, first=3, count=16)
+    tol2 = 1e-12 * np.maximum(np.abs(zr2), abs(zr2[0]))
+    assert np.all(np.abs(z2 - zr2) <= tol2)
