@@ -532,9 +532,10 @@ struct Slice {
     if (std::getenv("SE_PROFILE"))
       std::fprintf(stderr,
                    "[se] n=%d its=%ld total %.3f mv %.3f orth %.3f check %.3f eig %.3f cand %.3f "
-                   "passes %lld check_kernel_ms %.1f wcap %d fused %d frees %ld chk %.2f/%.2f/%.2f\n",
+                   "passes %lld cols %lld (%.1f GB/s over t_orth) check_kernel_ms %.1f wcap %d fused %d frees %ld chk %.2f/%.2f/%.2f\n",
                    A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
-                   kr.get().passes_total, c.prof_kernel_ms, kr.W.cap, (int)kr.fused(), dev_frees().load(),
+                   kr.get().passes_total, kr.get().cols_total,
+                   16.0 * A.n * (double)kr.get().cols_total / std::max(1e-9, cnt.t_orth) / 1e9, c.prof_kernel_ms, kr.W.cap, (int)kr.fused(), dev_frees().load(),
                    c.prof_chk[0], c.prof_chk[1], c.prof_chk[2]);
     r->niter = its;
     r->hit_max_its = warn;

@@ -24,6 +24,7 @@ struct Ctl {
   unsigned long long ts0, ts1;  // %globaltimer stamps (ns) for the Counters timers
   double t_mv_ns, t_orth_ns;    // accumulated filter / orthogonalisation device time
   long long passes_total;       // CGS passes executed (DGKS statistics)
+  long long cols_total;         // basis columns summed over those passes (bytes: 16 n per column)
 };
 
 namespace k {

@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(kThreads) k_gemvn(int n, const double* __restr
     const double after = sqrt(q);
     ctl->npass += 1;
     ctl->passes_total += 1;
+    ctl->cols_total += ncols;
     if (!pass2) ctl->repass = after > kDgksEta * ctl->before ? 0 : 1;
     ctl->before = after;
     ctl->after = after;
