@@ -637,7 +637,16 @@ struct EigenResults {
 inline std::pair<double, double> rayleigh_and_residual(const CsrMatrix& a, const CsrMatrix* b,
                                                        const Vec& u) {
   if ((int)u.size() != a.n()) throw std::invalid_argument("rayleigh_and_residual: vector size mismatch");
-  if (b) throw std::invalid_argument("rayleigh_and_residual: generalized pencils are outside the device path");
+  if (b) {  // lambda = u'Au / u'Bu, r = ||Au - lambda Bu|| (eigensolvers.hpp:86-106); products on the GPU
+    if (b->n() != a.n()) throw std::invalid_argument("rayleigh_and_residual: pencil size mismatch");
+    const Vec au = a.matvec(u), bu = b->matvec(u);
+    const double uu = dot(u, bu);
+    if (!(uu > 0.0)) throw std::invalid_argument("rayleigh_and_residual: zero (or B-degenerate) vector");
+    const double lambda = dot(u, au) / uu;
+    Vec r = au;
+    axpy(-lambda, bu, r);
+    return {lambda, nrm2(r)};
+  }
   double lam = 0.0, res = 0.0;
   detail::ok(se_rayleigh_residual(detail::ctx(), a.device(), u.data(), &lam, &res));
   return {lam, res};
@@ -647,10 +656,63 @@ namespace detail {
 inline EigenResults collect(se_results* r, int n);
 inline EigenResults cheb_lan(int solver, const CsrMatrix& a, const CsrMatrix* b,
                              const PolynomialFilter& f, double xi, double eta,
+                             const SolverConfig& cfg, const DeflationSet* locked);
+
+// Generalized pencil (A, B) with a diagonal SPD B (lumped mass, BASELINE cfg5): B = D^-2,
+// D = diag(b_i^-1/2), and (A, B) has the eigenpairs (lambda, D y) of the standard matrix
+// D A D (vals[p] = (a_ij d_i) d_j, as se_csr_scale_sym).  The reference's B-weighted path
+// (eigensolvers.hpp:640-690, SpdFactor solves) reaches the same pencil eigenpairs; non-diagonal B
+// needs a sparse Cholesky, outside the device path.
+inline Vec pencil_diag(const CsrMatrix& a, const CsrMatrix& b, const std::string& who) {
+  if (b.n() != a.n()) throw std::invalid_argument(who + ": pencil size mismatch");
+  Vec bd(b.n());
+  for (int i = 0; i < b.n(); ++i) {
+    const int p0 = b.row_ptr()[i], p1 = b.row_ptr()[i + 1];
+    if (p1 - p0 != 1 || b.col_idx()[p0] != i || !(b.vals()[p0] > 0.0))
+      throw std::invalid_argument(who + ": generalized pencils need a diagonal SPD B on the device path");
+    bd[i] = b.vals()[p0];
+  }
+  return bd;
+}
+inline EigenResults cheb_lan_pencil(int solver, const CsrMatrix& a, const CsrMatrix& b,
+                                    const PolynomialFilter& f, double xi, double eta,
+                                    const SolverConfig& cfg, const DeflationSet* locked) {
+  const std::string who = solver ? "cheb_lan_tr" : "cheb_lan_nr";
+  const Vec bd = pencil_diag(a, b, who);
+  const int n = a.n();
+  Vec d(n);
+  for (int i = 0; i < n; ++i) d[i] = 1.0 / std::sqrt(bd[i]);
+  std::vector<int> rp = a.row_ptr(), ci = a.col_idx();
+  Vec v = a.vals();
+  for (int i = 0; i < n; ++i)
+    for (int p = rp[i]; p < rp[i + 1]; ++p) v[p] = (v[p] * d[i]) * d[ci[p]];
+  const CsrMatrix s = CsrMatrix::from_csr(n, std::move(rp), std::move(ci), std::move(v));
+  DeflationSet ly;
+  if (locked && locked->count() > 0) {  // locked pencil vectors x -> y = D^-1 x
+    ly.values = locked->values;
+    ly.u = DenseMat(locked->u.rows(), locked->u.cols());
+    for (int j = 0; j < ly.u.cols(); ++j)
+      for (int i = 0; i < std::min(n, ly.u.rows()); ++i) ly.u(i, j) = locked->u(i, j) / d[i];
+  }
+  EigenResults r = cheb_lan(solver, s, nullptr, f, xi, eta, cfg, locked ? &ly : nullptr);
+  // x = D y (B-normalised); residuals as the reference reports them: ||A x - lambda B x||
+  for (int j = 0; j < r.vectors.cols(); ++j) {
+    double* x = r.vectors.col(j);
+    for (int i = 0; i < n; ++i) x[i] *= d[i];
+    const Vec xv = r.vectors.col_vec(j);
+    Vec rr = a.matvec(xv);
+    for (int i = 0; i < n; ++i) rr[i] -= r.eigenvalues[j] * (bd[i] * xv[i]);
+    r.residuals[j] = nrm2(rr);
+  }
+  return r;
+}
+
+inline EigenResults cheb_lan(int solver, const CsrMatrix& a, const CsrMatrix* b,
+                             const PolynomialFilter& f, double xi, double eta,
                              const SolverConfig& cfg, const DeflationSet* locked) {
   const char* who = solver ? "cheb_lan_tr" : "cheb_lan_nr";
   if (b && b->n() != a.n()) throw std::invalid_argument(std::string(who) + ": pencil size mismatch");
-  if (b) throw std::invalid_argument(std::string(who) + ": generalized pencils are outside the device path");
+  if (b) return cheb_lan_pencil(solver, a, *b, f, xi, eta, cfg, locked);
   const se_poly_filter s = to_c(f);
   const se_solver_cfg c{cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed};
   int nd = 0;

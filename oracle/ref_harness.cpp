@@ -448,6 +448,35 @@ void* ref_cheb_lan(int n, const int* rp, const int* ci, const double* v, int sol
   return rs;
 }
 
+// Generalized pencil (A, B) with B = diag(bdiag): the reference's own B-weighted path
+// (cheb_lan_nr/tr with b != nullptr: SpdFactor solves, eigensolvers.hpp:640-690, 703-732).
+void* ref_cheb_lan_pencil(int n, const int* rp, const int* ci, const double* v, const double* bdiag,
+                          int solver, double xi, double eta, double lmin, double lmax, int damping,
+                          double res_tol, int est_count, std::uint64_t seed) {
+  auto* rs = new ResultSet();
+  int rc = guarded([&] {
+    CsrMatrix a = make_csr(n, rp, ci, v);
+    std::vector<Triplet> tb;
+    for (int i = 0; i < n; ++i) tb.push_back({i, i, bdiag[i]});
+    CsrMatrix b = CsrMatrix::from_triplets(n, std::move(tb));
+    PolyOpts po;
+    po.damping = damping_of(damping);
+    PolynomialFilter f = find_pol(xi, eta, SpectralBounds{lmin, lmax}, po);
+    SolverConfig cfg;
+    cfg.res_tol = res_tol;
+    cfg.est_count = est_count;
+    cfg.seed = (unsigned long)seed;
+    rs->degrees.push_back(f.k);
+    rs->slices.push_back(solver == 1 ? cheb_lan_tr(a, &b, f, xi, eta, cfg)
+                                     : cheb_lan_nr(a, &b, f, xi, eta, cfg));
+  });
+  if (rc != 0) {
+    delete rs;
+    return nullptr;
+  }
+  return rs;
+}
+
 // Full sliced solve mirroring `sliceeig solve` (tools/sliceeig_main.cpp:464-523):
 // bounds (lan_tr_bounds tol 1e-4, 60, 40, seed :128-136) -> DOS (:138-157) -> slice_clipped
 // (:270-278) -> per-slice find_pol + cheb_lan_nr/tr (:394-418) on a std::thread pool

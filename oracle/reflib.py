@@ -57,6 +57,10 @@ def lib():
         L.ref_cheb_lan.argtypes = [C.c_int, _ip, _ip, _dp, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_double, C.c_int, C.c_int, C.c_long, C.c_int,
                                    C.c_double, C.c_double, C.c_int, C.c_uint64]
+        L.ref_cheb_lan_pencil.restype = C.c_void_p
+        L.ref_cheb_lan_pencil.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_int, C.c_double,
+                                          C.c_double, C.c_double, C.c_double, C.c_int, C.c_double,
+                                          C.c_int, C.c_uint64]
         L.ref_solve.restype = C.c_void_p
         L.ref_solve.argtypes = [C.c_int, _ip, _ip, _dp, C.c_double, C.c_double, C.c_int, C.c_int,
                                 C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
@@ -336,6 +340,17 @@ def cheb_lan(rp, ci, v, solver, xi, eta, lmin, lmax, damping="sigma", m=0, max_i
     if not h:
         msg = lib().ref_last_error().decode()
         raise RefError(msg)
+    return _collect(h, False)["slices"][0]
+
+
+def cheb_lan_pencil(rp, ci, v, bdiag, solver, xi, eta, lmin, lmax, damping="sigma",
+                    res_tol=1e-8, est_count=20, seed=1234):
+    """The reference's B-weighted cheb_lan_nr/tr on (A, diag(bdiag))."""
+    h = lib().ref_cheb_lan_pencil(len(rp) - 1, rp, ci, v, np.ascontiguousarray(bdiag, np.float64),
+                                  SOLVER[solver], xi, eta, lmin, lmax, DAMPING[damping], res_tol,
+                                  est_count, seed)
+    if not h:
+        raise RefError(lib().ref_last_error().decode())
     return _collect(h, False)["slices"][0]
 
 

@@ -640,9 +640,7 @@ def _cheb_lan(solver: int, a, b, f: PolynomialFilter, xi, eta, cfg: SolverConfig
     who = "cheb_lan_tr" if solver == 1 else "cheb_lan_nr"
     d = _dev(a)
     if b is not None:
-        if getattr(b, "n", d.n) != d.n:
-            raise ValueError(f"{who}: pencil size mismatch")
-        raise ValueError(f"{who}: generalized pencils (b != nullptr) are outside the device path")
+        return _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who)
     s, _keep = f._c()
     c = _lib.SeSolverCfg(cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count,
                          cfg.seed)
@@ -661,6 +659,51 @@ def _cheb_lan(solver: int, a, b, f: PolynomialFilter, xi, eta, cfg: SolverConfig
          du.ctypes.data_as(_PD) if nd else None, _pd(dv) if nd else None, int(want_vectors),
          C.byref(h))
     return _collect_results(h, d, want_vectors)
+
+
+def _pencil_diag(b, n: int, who: str) -> np.ndarray:
+    """The diagonal of an SPD diagonal B (CsrMatrix or DeviceCsr); anything else raises."""
+    if getattr(b, "n", n) != n:
+        raise ValueError(f"{who}: pencil size mismatch")
+    hb = b.download() if isinstance(b, DeviceCsr) else b
+    rp, ci, v = np.asarray(hb.row_ptr), np.asarray(hb.col_idx), np.asarray(hb.vals, np.float64)
+    if not (np.all(np.diff(rp) == 1) and np.array_equal(ci, np.arange(n)) and np.all(v > 0.0)):
+        raise ValueError(f"{who}: generalized pencils need a diagonal SPD B on the device path")
+    return v.copy()
+
+
+def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who):
+    """(A, B) with diagonal SPD B = D^-2: the standard matrix D A D on the device (its eigenpairs
+    (lambda, y) give the pencil's (lambda, D y), B-normalised), residuals reported as the
+    reference's ||A x - lambda B x|| (eigensolvers.hpp:289-316).  The reference runs its B-weighted
+    recurrence with Cholesky solves of B (eigensolvers.hpp:640-690); a non-diagonal B would need a
+    sparse Cholesky, outside the device path."""
+    bd = _pencil_diag(b, d.n, who)
+    dsc = 1.0 / np.sqrt(bd)
+    host = a if isinstance(a, CsrMatrix) else (a.csr if isinstance(a, Operator) else d.download())
+    S = DeviceCsr.upload(host, d.ctx)
+    try:
+        S.scale_sym(dsc)
+        ly = None
+        if locked is not None and locked.count() > 0:
+            ly = DeflationSet(np.asarray(locked.u, np.float64) / dsc[:, None], locked.values)
+        r = _cheb_lan(solver, S, None, f, xi, eta, cfg, ly, True)
+    finally:
+        S.free()
+    x = r.vectors * dsc[:, None]
+    res = np.empty(r.eigenvalues.size)
+    for j in range(r.eigenvalues.size):
+        res[j] = np.linalg.norm(d_matvec(d, x[:, j]) - r.eigenvalues[j] * (bd * x[:, j]))
+    return EigenResults(r.eigenvalues, x if want_vectors else None, res, r.niter, r.counters,
+                        r.hit_max_its)
+
+
+def d_matvec(d: "DeviceCsr", x) -> np.ndarray:
+    """y = A x on the GPU (csr.hpp:98-105)."""
+    x = _f64(x)
+    y = np.empty(d.n)
+    call("se_spmv", d.ctx.handle, d.handle, _pd(x), _pd(y))
+    return y
 
 
 def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
@@ -714,12 +757,20 @@ def cheb_lan_tr(a, b, f: PolynomialFilter, xi: float, eta: float, cfg: SolverCon
 
 def rayleigh_and_residual(a, b, u) -> tuple[float, float]:
     """eigensolvers.hpp:86-106 (standard problem) on the GPU."""
-    if b is not None:
-        raise ValueError("rayleigh_and_residual: generalized pencils are outside the device path")
     d = _dev(a)
     u = _f64(u)
     if u.size != d.n:
         raise ValueError("rayleigh_and_residual: vector size mismatch")
+    if b is not None:  # lambda = u'Au / u'Bu, r = ||Au - lambda Bu|| (eigensolvers.hpp:86-106)
+        db = _dev(b)
+        if db.n != d.n:
+            raise ValueError("rayleigh_and_residual: pencil size mismatch")
+        au, bu = d_matvec(d, u), d_matvec(db, u)
+        uu = float(np.dot(u, bu))
+        if not uu > 0.0:
+            raise ValueError("rayleigh_and_residual: zero (or B-degenerate) vector")
+        lam = float(np.dot(u, au)) / uu
+        return lam, float(np.linalg.norm(au - lam * bu))
     lam, res = C.c_double(), C.c_double()
     call("se_rayleigh_residual", d.ctx.handle, d.handle, _pd(u), C.byref(lam), C.byref(res))
     return lam.value, res.value

@@ -47,6 +47,30 @@ int main() {
       expect(r.counters.n_A_matvec >= (long)pf.k * r.niter, "op accounting n_A_matvec >= k*niter");
     }
   }
+  // generalized pencil (A, B) with a diagonal SPD B (lumped mass): reference-style call with
+  // b != nullptr; B-normalised vectors and pencil residuals ||Ax - lambda Bx||
+  {
+    CsrMatrix a = gen_laplacian({12, 12, 12});
+    Vec bd((std::size_t)a.n());
+    for (int i = 0; i < a.n(); ++i) bd[i] = 0.5 + 0.25 * (1.0 + std::sin(0.37 * i));
+    CsrMatrix b = CsrMatrix::diag(bd);
+    PolynomialFilter pf = find_pol(1.0, 1.3, SpectralBounds{0.0, 24.0});
+    SolverConfig cfg;
+    cfg.est_count = 40;
+    EigenResults r = cheb_lan_tr(a, &b, pf, 1.0, 1.3, cfg);
+    double res = 0.0, nrm = 0.0;
+    for (int j = 0; j < (int)r.eigenvalues.size(); ++j) {
+      const Vec x = r.vectors.col_vec(j);
+      const auto rr = rayleigh_and_residual(a, &b, x);
+      res = std::max(res, rr.second / std::max(1.0, std::abs(rr.first)));
+      double xbx = 0.0;
+      for (int i = 0; i < a.n(); ++i) xbx += x[i] * bd[i] * x[i];
+      nrm = std::max(nrm, std::abs(xbx - 1.0));
+    }
+    expect(!r.eigenvalues.empty() && res <= 1e-8 && nrm <= 1e-12,
+           "cheb_lan_tr pencil (A, diag B) 12^3 [1.0,1.3]: " + std::to_string(r.eigenvalues.size()) +
+               " pairs, max ||Ax-lBx|| " + std::to_string(res));
+  }
   // criterion 3 (slicing + seam-exact union) on 20^3 through the CLI's stage calls
   {
     CsrMatrix a = gen_laplacian({20, 20, 20});

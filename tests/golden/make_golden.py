@@ -184,6 +184,24 @@ def cfg5p():
     save("cfg5p", **out)
 
 
+def pencil():
+    """Generalized pencil (A, B), A = 16^3 Laplacian, B = diag(0.5 + uniform) (seed 7): the
+    reference's own B-weighted cheb_lan_tr / cheb_lan_nr (b != nullptr, SpdFactor solves) on
+    [1.0, 1.4] with bounds fixed to [0, 24] (lambda(A, B) <= 12 / 0.5)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1802_05215_b200 import api
+    L = api.gen_laplacian([16, 16, 16])
+    b, _ = api.mass_scaling(L.n, 7)
+    out = dict(b=b, window=[1.0, 1.4], bounds=[0.0, 24.0])
+    for solver in ("tr", "nr"):
+        r = reflib.cheb_lan_pencil(L.row_ptr, L.col_idx, L.vals, b, solver, 1.0, 1.4, 0.0, 24.0,
+                                   est_count=80, seed=7)
+        out[f"{solver}_vals"] = r["eigenvalues"]
+        out[f"{solver}_res"] = r["residuals"]
+        out[f"{solver}_meta"] = [r["niter"], r["n_A_matvec"], r["degree"]]
+    save("pencil", **out)
+
+
 def cli():
     """`sliceeig solve --dims 30,30 --interval 0.4,0.6 --slices 4 [--solver tr]` with the CLI
     defaults (KPM deg 60 x 40 Rademacher probes, sigma damping, tol 1e-8, seed 1234): the
@@ -214,7 +232,7 @@ def cli():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-solve", action="store_true")
-    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli")
+    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli,pencil")
     a = ap.parse_args()
     only = a.only.split(",")
     if "kats" in only:
@@ -229,3 +247,5 @@ if __name__ == "__main__":
         cfg5p()
     if "cli" in only:
         cli()
+    if "pencil" in only:
+        pencil()

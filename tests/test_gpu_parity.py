@@ -368,3 +368,39 @@ def test_cheb_si_saturation_raises(gpu_ctx):
     f = api.find_pol(0.5, 1.5, b)
     with pytest.raises(RuntimeError):
         api.cheb_si(a, None, f, 0.5, 1.5, 1, api.SolverConfig(est_count=1, seed=1))
+
+
+@pytest.mark.parametrize("solver", ["tr", "nr"])
+def test_diagonal_pencil_matches_reference(gpu_ctx, golden, solver):
+    """Generalized pencil (A, B), B diagonal SPD (lumped mass): cheb_lan_tr/nr(A, &B, ...) against
+    the reference's own B-weighted solve (tests/golden/make_golden.py pencil()): identical count,
+    eigenvalues within 1e-10 relative, B-normalised vectors with ||Ax - lambda Bx|| <= tol, and the
+    pencil rayleigh_and_residual agrees."""
+    api = _api()
+    g = golden("pencil")
+    A = api.gen_laplacian([16, 16, 16])
+    B = api.CsrMatrix.diag(g["b"])
+    lo, hi = g["bounds"]
+    xi, eta = g["window"]
+    f = api.find_pol(xi, eta, api.SpectralBounds(lo, hi))
+    assert f.k == int(g[f"{solver}_meta"][2])
+    drv = api.cheb_lan_tr if solver == "tr" else api.cheb_lan_nr
+    r = drv(A, B, f, xi, eta, api.SolverConfig(res_tol=1e-8, est_count=80, seed=7))
+    ref = g[f"{solver}_vals"]
+    assert r.eigenvalues.size == ref.size
+    assert np.all(np.abs(r.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+    assert np.all(r.residuals <= 1e-8 * np.maximum(1.0, np.abs(r.eigenvalues)))
+    b = g["b"]
+    for j in range(0, ref.size, 7):
+        x = r.vectors[:, j]
+        assert abs(float(np.dot(x, b * x)) - 1.0) <= 1e-12
+        lam, res = api.rayleigh_and_residual(A, B, x)
+        assert abs(lam - r.eigenvalues[j]) <= 1e-10 * abs(lam) and res <= 1e-8
+
+
+def test_non_diagonal_pencil_rejected(gpu_ctx):
+    api = _api()
+    A = api.gen_laplacian([6, 6])
+    with pytest.raises(ValueError):
+        api.cheb_lan_tr(A, api.CsrMatrix.tridiag_toeplitz(36, 0.1, 2.0),
+                        api.find_pol(0.5, 0.8, api.SpectralBounds(0.0, 8.0)), 0.5, 0.8)

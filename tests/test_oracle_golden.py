@@ -129,3 +129,18 @@ def test_cfg2_kpm_gaussian_and_slices(golden):
     assert np.array_equal(bp, c["bp"]) and np.array_equal(est, c["est"])
     degs = [clib.find_pol(bp[i], bp[i + 1], lo, hi)["k"] for i in range(8)]
     assert degs == list(c["degrees"]) == [67, 115, 121, 126, 260, 133, 138, 367]
+
+
+@pytest.mark.skipif(not __import__("oracle.reflib", fromlist=["available"]).available(),
+                    reason="oracle/_ref (the reference build) not present")
+def test_pencil_golden_reproduced_by_reference(golden):
+    """tests/golden/pencil.npz is the reference's own B-weighted cheb_lan_tr/nr (b != nullptr) on
+    (16^3 Laplacian, diag B): rerunning it reproduces the stored eigenvalues bitwise."""
+    from oracle import reflib
+    from paper_1802_05215_b200 import api
+    g = golden("pencil")
+    L = api.gen_laplacian([16, 16, 16])
+    assert np.array_equal(api.mass_scaling(L.n, 7)[0], g["b"])
+    r = reflib.cheb_lan_pencil(L.row_ptr, L.col_idx, L.vals, g["b"], "tr", *g["window"], *g["bounds"],
+                               est_count=80, seed=7)
+    assert np.array_equal(r["eigenvalues"], g["tr_vals"])
