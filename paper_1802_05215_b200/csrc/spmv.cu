@@ -625,7 +625,9 @@ __global__ void __launch_bounds__(kKpmThreads, kEllMinB) k_kpm_ell(
 #pragma unroll
       for (int u = 0; u < kEllW; ++u)
         x[u] = __ldg(reinterpret_cast<const double2*>(src + (size_t)cs[u] * b + 2 * l8));
-      const double2 xr = __ldg(reinterpret_cast<const double2*>(src + o));
+      // the row's own probe row: the pad slot (col = row) when the row is not full
+      const double2 xr = cs[kEllW - 1] == r ? x[kEllW - 1]
+                                            : __ldg(reinterpret_cast<const double2*>(src + o));
       double2 vr = make_double2(0.0, 0.0), pr = vr;
       if (!dbl) vr = __ldg(reinterpret_cast<const double2*>(v + o));
       if (!first) pr = __ldg(reinterpret_cast<const double2*>(w0 + o));
