@@ -40,8 +40,10 @@ sys.path.insert(0, ROOT)
 
 CFG2 = dict(dims=[64, 64, 64], xi=0.6, eta=1.2, ns=8, solver="tr", damping="sigma", dos_m=100,
             dos_nvec=40, probes="gaussian", tol=1e-8, seed=1234)
-# CPU-boundable proxy of the same recipe (used only for the reference arm / cpu_baseline)
-PROXY = dict(CFG2, dims=[20, 20, 20])
+# CPU-boundable proxy of the same recipe (used only for the reference arm / cpu_baseline): the
+# largest grid whose full reference pipeline stays near 20-30 s per step on 8 host threads (per-
+# eigenpair cost grows ~n^2 with the grid: the 64^3 cfg2 itself takes ~2 h)
+PROXY = dict(CFG2, dims=[32, 32, 32])
 # side measurements (other BASELINE configs, reported under "other_configs")
 CFGS_OTHER = {"cfg1": dict(dims=[100, 100], xi=0.4, eta=1.6, ns=2, solver="nr", damping="jackson",
                            dos_m=80, dos_nvec=20, probes="rademacher", tol=1e-8, seed=0)}
