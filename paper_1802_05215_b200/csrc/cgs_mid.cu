@@ -249,14 +249,164 @@ __global__ void __launch_bounds__(kFT, 1) k_cgs_mid(const __grid_constant__ CUte
   }
 }
 
+// L2 two-read variant (SE_CGS_FUSED=2): no shared-memory staging of W.  A CTA (32 warps) walks
+// its contiguous range of 32-row blocks; per block, phase 1 streams W[rows, :] from HBM (warp w
+// takes columns w, w + 32, ...; lane = row, so every load is one 256-byte column segment) and
+// forms t1 = t - W c1; phase 2 re-reads the same block -- still in L2: the blocks in flight across
+// the grid are grid x 32 x ncols x 8 bytes -- and adds W[rows, j]^T t1[rows] to the CTA's c2
+// accumulator of column j (owned by one warp, summed in block order).  Same tail as k_cgs_mid.
+constexpr int kL2Rows = 32;
+constexpr int kL2Warps = 32;
+constexpr int kL2Unroll = 8;
+
+__global__ void __launch_bounds__(kL2Warps * 32) k_cgs_mid_l2(int n, const double* __restrict__ Q,
+                                                                double* __restrict__ t, Ctl* ctl,
+                                                                const double* __restrict__ coef1,
+                                                                double* c2part, int ldp, double* npart,
+                                                                unsigned* cnt, double* coef2, double* hdiag) {
+  if (ctl->halted) return;
+  const int ncols = ctl->i + 1;
+  extern __shared__ double smem_l2[];
+  double* s_c1 = smem_l2;                 // ncols
+  double* s_acc = smem_l2 + ldp;          // ncols: this CTA's c2 partials
+  __shared__ double s_red[kL2Warps][kL2Rows + 1];
+  __shared__ double s_t1[kL2Rows];
+  __shared__ double s_w[kL2Warps];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = (int)(blockDim.x >> 5);  // warps (column stride)
+  for (int j = tid; j < ncols; j += blockDim.x) {
+    s_c1[j] = __ldg(coef1 + j);
+    s_acc[j] = 0.0;
+  }
+  __syncthreads();
+  double nacc = 0.0;
+  const int nrb = (n + kL2Rows - 1) / kL2Rows;
+  const int b0 = (int)((long)blockIdx.x * nrb / gridDim.x);
+  const int b1 = (int)((long)(blockIdx.x + 1) * nrb / gridDim.x);
+  for (int b = b0; b < b1; ++b) {
+    const int r = b * kL2Rows + lane;
+    const bool live = r < n;
+    const double* __restrict__ qr = Q + r;
+    // phase 1: partial (W c1)[r] over this warp's columns
+    double p = 0.0;
+    {
+      int j = warp;
+      for (; j + (kL2Unroll - 1) * NW < ncols; j += kL2Unroll * NW) {
+        double w[kL2Unroll];
+#pragma unroll
+        for (int u = 0; u < kL2Unroll; ++u) w[u] = live ? __ldg(qr + (size_t)(j + u * NW) * n) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kL2Unroll; ++u) p = add(p, mul(s_c1[j + u * NW], w[u]));
+      }
+      for (; j < ncols; j += NW) p = add(p, mul(s_c1[j], live ? __ldg(qr + (size_t)j * n) : 0.0));
+    }
+    s_red[warp][lane] = p;
+    __syncthreads();
+    if (warp == 0) {
+      double sum = 0.0;
+      for (int q = 0; q < NW; ++q) sum = add(sum, s_red[q][lane]);
+      double x = 0.0;
+      if (live) {
+        x = sub(t[r], sum);
+        t[r] = x;
+      }
+      s_t1[lane] = x;
+      nacc = add(nacc, mul(x, x));
+    }
+    __syncthreads();
+    // phase 2: c2[j] += W[rows, j] . t1[rows]  (L2 re-read)
+    const double tv = s_t1[lane];
+    int j = warp;
+    for (; j + (kL2Unroll - 1) * NW < ncols; j += kL2Unroll * NW) {
+      double v[kL2Unroll];
+#pragma unroll
+      for (int u = 0; u < kL2Unroll; ++u) v[u] = live ? mul(__ldg(qr + (size_t)(j + u * NW) * n), tv) : 0.0;
+      // butterfly multi-reduction of the 32 x 8 products: at lane bits 4 / 3 / 2 each lane keeps
+      // half of its columns and receives its partner's other half (4 + 2 + 1 exchanges), then
+      // two plain xor steps; lane L ends with the full sum of column 4 b4 + 2 b3 + b2
+      const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double send = h4 ? v[k] : v[k + 4];
+        const double keep = h4 ? v[k + 4] : v[k];
+        v[k] = add(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double send = h3 ? v[k] : v[k + 2];
+        const double keep = h3 ? v[k + 2] : v[k];
+        v[k] = add(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+      }
+      {
+        const double send = h2 ? v[0] : v[1];
+        const double keep = h2 ? v[1] : v[0];
+        v[0] = add(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+      }
+      v[0] = add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 2));
+      v[0] = add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+      if ((lane & 3) == 0) {
+        const int col = j + ((h4 ? 4 : 0) + (h3 ? 2 : 0) + (h2 ? 1 : 0)) * NW;
+        s_acc[col] = add(s_acc[col], v[0]);
+      }
+    }
+    for (; j < ncols; j += NW) {
+      double v = live ? mul(__ldg(qr + (size_t)j * n), tv) : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) s_acc[j] = add(s_acc[j], v);
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < ncols; j += blockDim.x) c2part[(size_t)blockIdx.x * ldp + j] = s_acc[j];
+  if (warp == 0) {
+    const double v = warp_sum(nacc);
+    if (lane == 0) npart[blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ int s_repass;
+  if (warp == 0) {
+    double u = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) u = add(u, __ldcg(npart + b));
+    u = warp_sum(u);
+    if (lane == 0) {
+      const double after = sqrt(u);
+      const int rep = after > 0.70710678118654752 * ctl->before ? 0 : 1;
+      s_repass = rep;
+      ctl->npass += 1;
+      ctl->passes_total += 1;
+      ctl->cols_total += ncols;
+      ctl->repass = rep;
+      ctl->before = after;
+      ctl->after = after;
+      *cnt = 0u;
+    }
+  }
+  (void)s_w;
+  __syncthreads();
+  const int hcol = hdiag ? ctl->i : -1;
+  for (int j = tid; j < ncols; j += blockDim.x) {
+    double u = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) u = add(u, __ldcg(c2part + (size_t)b * ldp + j));
+    coef2[j] = u;
+    if (j == hcol && s_repass) hdiag[j] = add(hdiag[j], u);  // h[i] += c2_i (orth.hpp:30)
+  }
+}
+
 }  // namespace
 
 size_t cgs_mid_scratch_doubles(const Ctx& c, int cap_cols) {
-  const size_t grid = (size_t)c.num_sms;
+  const size_t grid = (size_t)c.num_sms * 4;
   return grid * (size_t)std::max(cap_cols, 1) + grid + 64;
 }
 
+bool cgs_mid_l2();
 bool cgs_mid_supported(int n, int cap_cols) {
+  if (cgs_mid_l2()) return cap_cols <= 12800;
   return n % 2 == 0 && cap_cols <= kMaxFusedCols && rows_for(cap_cols) >= 2;
 }
 
@@ -273,8 +423,36 @@ PFN_cuTensorMapEncodeTiled encode_fn() {
 }
 }  // namespace
 
+bool cgs_mid_l2() {
+  static const bool v = [] {
+    const char* e = std::getenv("SE_CGS_FUSED");
+    return e && std::atoi(e) == 2;
+  }();
+  return v;
+}
+
 void cgs_mid(Ctx& c, int n, double* t, const double* Q, Ctl* ctl, const double* coef1,
              double* coef2, double* hdiag, int cap, double* scratch, unsigned* cnt) {
+  if (cgs_mid_l2()) {
+    const size_t smem = sizeof(double) * 2 * (size_t)std::max(cap, 1);
+    static thread_local bool attr2 = false;
+    if (!attr2) {
+      SE_CUDA(cudaFuncSetAttribute(k_cgs_mid_l2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr2 = true;
+    }
+    if (smem > 200 * 1024) fail(SE_EINVAL, "cgs_mid: basis too wide for the fused path");
+    static const int cps = [] {  // CTAs per SM (SE_MID_CPS): 1 x 1024, 2 x 512, 4 x 256 threads
+      const char* e = std::getenv("SE_MID_CPS");
+      const int v = e ? std::atoi(e) : 1;
+      return v == 2 || v == 4 ? v : 1;
+    }();
+    const int grid = c.num_sms * cps;
+    k_cgs_mid_l2<<<grid, kL2Warps * 32 / cps, smem, c.stream>>>(n, Q, t, ctl, coef1, scratch, cap,
+                                                          scratch + (size_t)grid * cap, cnt, coef2, hdiag);
+    ++c.launches;
+    SE_CUDA(cudaGetLastError());
+    return;
+  }
   static thread_local bool attr = false;
   if (!attr) {
     SE_CUDA(cudaFuncSetAttribute(k_cgs_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRing));
