@@ -411,6 +411,7 @@ def main():
             d2h += sum(s.eigenvalues.nbytes + s.residuals.nbytes +
                        (s.vectors.nbytes if s.vectors is not None else 0) for s in mine)
             be.A.free()
+            del r2, mine  # the step's pinned result blocks go back to the host caching allocator
         torch.cuda.synchronize()
         el = _max_over_ranks(time.perf_counter() - t0, world)
         got_all = _sum_over_ranks(got, world)
