@@ -674,10 +674,11 @@ inline Vec pencil_diag(const CsrMatrix& a, const CsrMatrix& b, const std::string
   }
   return bd;
 }
-inline EigenResults cheb_lan_pencil(int solver, const CsrMatrix& a, const CsrMatrix& b,
-                                    const PolynomialFilter& f, double xi, double eta,
-                                    const SolverConfig& cfg, const DeflationSet* locked) {
-  const std::string who = solver ? "cheb_lan_tr" : "cheb_lan_nr";
+// Solve the scaled standard problem D A D with `solve(S, d)`, then map its eigenpairs back to the
+// pencil: x = D y (B-normalised) and the reference's residual ||A x - lambda B x||.
+template <class Solve>
+inline EigenResults pencil_scaled(const CsrMatrix& a, const CsrMatrix& b, const std::string& who,
+                                  Solve&& solve) {
   const Vec bd = pencil_diag(a, b, who);
   const int n = a.n();
   Vec d(n);
@@ -687,15 +688,7 @@ inline EigenResults cheb_lan_pencil(int solver, const CsrMatrix& a, const CsrMat
   for (int i = 0; i < n; ++i)
     for (int p = rp[i]; p < rp[i + 1]; ++p) v[p] = (v[p] * d[i]) * d[ci[p]];
   const CsrMatrix s = CsrMatrix::from_csr(n, std::move(rp), std::move(ci), std::move(v));
-  DeflationSet ly;
-  if (locked && locked->count() > 0) {  // locked pencil vectors x -> y = D^-1 x
-    ly.values = locked->values;
-    ly.u = DenseMat(locked->u.rows(), locked->u.cols());
-    for (int j = 0; j < ly.u.cols(); ++j)
-      for (int i = 0; i < std::min(n, ly.u.rows()); ++i) ly.u(i, j) = locked->u(i, j) / d[i];
-  }
-  EigenResults r = cheb_lan(solver, s, nullptr, f, xi, eta, cfg, locked ? &ly : nullptr);
-  // x = D y (B-normalised); residuals as the reference reports them: ||A x - lambda B x||
+  EigenResults r = solve(s, d);
   for (int j = 0; j < r.vectors.cols(); ++j) {
     double* x = r.vectors.col(j);
     for (int i = 0; i < n; ++i) x[i] *= d[i];
@@ -705,6 +698,22 @@ inline EigenResults cheb_lan_pencil(int solver, const CsrMatrix& a, const CsrMat
     r.residuals[j] = nrm2(rr);
   }
   return r;
+}
+
+inline EigenResults cheb_lan_pencil(int solver, const CsrMatrix& a, const CsrMatrix& b,
+                                    const PolynomialFilter& f, double xi, double eta,
+                                    const SolverConfig& cfg, const DeflationSet* locked) {
+  const std::string who = solver ? "cheb_lan_tr" : "cheb_lan_nr";
+  return pencil_scaled(a, b, who, [&](const CsrMatrix& s, const Vec& d) {
+    DeflationSet ly;
+    if (locked && locked->count() > 0) {  // locked pencil vectors x -> y = D^-1 x
+      ly.values = locked->values;
+      ly.u = DenseMat(locked->u.rows(), locked->u.cols());
+      for (int j = 0; j < ly.u.cols(); ++j)
+        for (int i = 0; i < std::min((int)d.size(), ly.u.rows()); ++i) ly.u(i, j) = locked->u(i, j) / d[i];
+    }
+    return cheb_lan(solver, s, nullptr, f, xi, eta, cfg, locked ? &ly : nullptr);
+  });
 }
 
 inline EigenResults cheb_lan(int solver, const CsrMatrix& a, const CsrMatrix* b,
@@ -762,7 +771,10 @@ inline EigenResults cheb_lan_tr(const CsrMatrix& a, const CsrMatrix* b, const Po
 inline EigenResults cheb_si(const CsrMatrix& a, const CsrMatrix* b, const PolynomialFilter& f,
                             double xi, double eta, int est_count, const SolverConfig& cfg = {}) {
   if (b && b->n() != a.n()) throw std::invalid_argument("cheb_si: pencil size mismatch");
-  if (b) throw std::invalid_argument("cheb_si: generalized pencils are outside the device path");
+  if (b)  // diagonal SPD B: the scaled standard problem (see detail::pencil_scaled)
+    return detail::pencil_scaled(a, *b, "cheb_si", [&](const CsrMatrix& s, const Vec&) {
+      return cheb_si(s, nullptr, f, xi, eta, est_count, cfg);
+    });
   const se_poly_filter s = detail::to_c(f);
   const se_solver_cfg c{cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed};
   se_results* r = nullptr;

@@ -467,8 +467,9 @@ void* ref_cheb_lan_pencil(int n, const int* rp, const int* ci, const double* v, 
     cfg.est_count = est_count;
     cfg.seed = (unsigned long)seed;
     rs->degrees.push_back(f.k);
-    rs->slices.push_back(solver == 1 ? cheb_lan_tr(a, &b, f, xi, eta, cfg)
-                                     : cheb_lan_nr(a, &b, f, xi, eta, cfg));
+    rs->slices.push_back(solver == 2   ? cheb_si(a, &b, f, xi, eta, est_count, cfg)
+                         : solver == 1 ? cheb_lan_tr(a, &b, f, xi, eta, cfg)
+                                       : cheb_lan_nr(a, &b, f, xi, eta, cfg));
   });
   if (rc != 0) {
     delete rs;

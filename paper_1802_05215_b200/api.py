@@ -672,22 +672,19 @@ def _pencil_diag(b, n: int, who: str) -> np.ndarray:
     return v.copy()
 
 
-def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who):
-    """(A, B) with diagonal SPD B = D^-2: the standard matrix D A D on the device (its eigenpairs
-    (lambda, y) give the pencil's (lambda, D y), B-normalised), residuals reported as the
-    reference's ||A x - lambda B x|| (eigensolvers.hpp:289-316).  The reference runs its B-weighted
-    recurrence with Cholesky solves of B (eigensolvers.hpp:640-690); a non-diagonal B would need a
-    sparse Cholesky, outside the device path."""
+def _pencil_scaled(a, d, b, who, solve, want_vectors=True):
+    """(A, B) with diagonal SPD B = D^-2: `solve(S, dsc)` on the standard matrix D A D (a scaled
+    device copy); its eigenpairs (lambda, y) give the pencil's (lambda, D y), B-normalised, with
+    residuals reported as the reference's ||A x - lambda B x|| (eigensolvers.hpp:289-316).  The
+    reference runs its B-weighted recurrence with Cholesky solves of B (eigensolvers.hpp:640-690);
+    a non-diagonal B would need a sparse Cholesky, outside the device path."""
     bd = _pencil_diag(b, d.n, who)
     dsc = 1.0 / np.sqrt(bd)
     host = a if isinstance(a, CsrMatrix) else (a.csr if isinstance(a, Operator) else d.download())
     S = DeviceCsr.upload(host, d.ctx)
     try:
         S.scale_sym(dsc)
-        ly = None
-        if locked is not None and locked.count() > 0:
-            ly = DeflationSet(np.asarray(locked.u, np.float64) / dsc[:, None], locked.values)
-        r = _cheb_lan(solver, S, None, f, xi, eta, cfg, ly, True)
+        r = solve(S, dsc)
     finally:
         S.free()
     x = r.vectors * dsc[:, None]
@@ -696,6 +693,15 @@ def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who
         res[j] = np.linalg.norm(d_matvec(d, x[:, j]) - r.eigenvalues[j] * (bd * x[:, j]))
     return EigenResults(r.eigenvalues, x if want_vectors else None, res, r.niter, r.counters,
                         r.hit_max_its)
+
+
+def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who):
+    def solve(S, dsc):
+        ly = None
+        if locked is not None and locked.count() > 0:  # locked pencil vectors x -> y = D^-1 x
+            ly = DeflationSet(np.asarray(locked.u, np.float64) / dsc[:, None], locked.values)
+        return _cheb_lan(solver, S, None, f, xi, eta, cfg, ly, True)
+    return _pencil_scaled(a, d, b, who, solve, want_vectors)
 
 
 def d_matvec(d: "DeviceCsr", x) -> np.ndarray:
@@ -732,10 +738,10 @@ def cheb_si(a, b, f: PolynomialFilter, xi: float, eta: float, est_count: int,
     """Filtered subspace iteration on a block of ceil(1.3 est_count) + 8 vectors
     (eigensolvers.hpp:760-940); raises RuntimeError when the block saturates above the bar."""
     d = _dev(a)
-    if b is not None:
-        if getattr(b, "n", d.n) != d.n:
-            raise ValueError("cheb_si: pencil size mismatch")
-        raise ValueError("cheb_si: generalized pencils (b != nullptr) are outside the device path")
+    if b is not None:  # diagonal SPD B: the scaled standard problem (_pencil_scaled)
+        return _pencil_scaled(a, d, b, "cheb_si",
+                              lambda S, dsc: cheb_si(S, None, f, xi, eta, est_count, cfg, True),
+                              want_vectors)
     s, _keep = f._c()
     c = _lib.SeSolverCfg(cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed)
     h = C.c_void_p()

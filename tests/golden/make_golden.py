@@ -186,16 +186,16 @@ def cfg5p():
 
 def pencil():
     """Generalized pencil (A, B), A = 16^3 Laplacian, B = diag(0.5 + uniform) (seed 7): the
-    reference's own B-weighted cheb_lan_tr / cheb_lan_nr (b != nullptr, SpdFactor solves) on
+    reference's own B-weighted cheb_lan_tr / cheb_lan_nr / cheb_si (b != nullptr, SpdFactor solves) on
     [1.0, 1.4] with bounds fixed to [0, 24] (lambda(A, B) <= 12 / 0.5)."""
     sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
     from paper_1802_05215_b200 import api
     L = api.gen_laplacian([16, 16, 16])
     b, _ = api.mass_scaling(L.n, 7)
     out = dict(b=b, window=[1.0, 1.4], bounds=[0.0, 24.0])
-    for solver in ("tr", "nr"):
+    for solver in ("tr", "nr", "si"):
         r = reflib.cheb_lan_pencil(L.row_ptr, L.col_idx, L.vals, b, solver, 1.0, 1.4, 0.0, 24.0,
-                                   est_count=80, seed=7)
+                                   est_count=80 if solver != "si" else 60, seed=7)
         out[f"{solver}_vals"] = r["eigenvalues"]
         out[f"{solver}_res"] = r["residuals"]
         out[f"{solver}_meta"] = [r["niter"], r["n_A_matvec"], r["degree"]]

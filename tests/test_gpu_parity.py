@@ -372,7 +372,7 @@ def test_cheb_si_saturation_raises(gpu_ctx):
         api.cheb_si(a, None, f, 0.5, 1.5, 1, api.SolverConfig(est_count=1, seed=1))
 
 
-@pytest.mark.parametrize("solver", ["tr", "nr"])
+@pytest.mark.parametrize("solver", ["tr", "nr", "si"])
 def test_diagonal_pencil_matches_reference(gpu_ctx, golden, solver):
     """Generalized pencil (A, B), B diagonal SPD (lumped mass): cheb_lan_tr/nr(A, &B, ...) against
     the reference's own B-weighted solve (tests/golden/make_golden.py pencil()): identical count,
@@ -386,8 +386,11 @@ def test_diagonal_pencil_matches_reference(gpu_ctx, golden, solver):
     xi, eta = g["window"]
     f = api.find_pol(xi, eta, api.SpectralBounds(lo, hi))
     assert f.k == int(g[f"{solver}_meta"][2])
-    drv = api.cheb_lan_tr if solver == "tr" else api.cheb_lan_nr
-    r = drv(A, B, f, xi, eta, api.SolverConfig(res_tol=1e-8, est_count=80, seed=7))
+    if solver == "si":
+        r = api.cheb_si(A, B, f, xi, eta, 60, api.SolverConfig(res_tol=1e-8, seed=7))
+    else:
+        drv = api.cheb_lan_tr if solver == "tr" else api.cheb_lan_nr
+        r = drv(A, B, f, xi, eta, api.SolverConfig(res_tol=1e-8, est_count=80, seed=7))
     ref = g[f"{solver}_vals"]
     assert r.eigenvalues.size == ref.size
     assert np.all(np.abs(r.eigenvalues - ref) <= 1e-10 * np.abs(ref))
