@@ -409,3 +409,32 @@ def test_non_diagonal_pencil_rejected(gpu_ctx):
     with pytest.raises(ValueError):
         api.cheb_lan_tr(A, api.CsrMatrix.tridiag_toeplitz(36, 0.1, 2.0),
                         api.find_pol(0.5, 0.8, api.SpectralBounds(0.0, 8.0)), 0.5, 0.8)
+
+
+@pytest.mark.parametrize("m,first,count", [(300, 16, 2), (40, 32, 16)])
+def test_cfg3_full_size_moments_probe_subset(gpu_ctx, m, first, count):
+    """BASELINE cfg3 at full size (160^3, bounds [0, 12], 128 Rademacher probes from seed 0): a
+    subset of the probes -- reached by jump-ahead on the device side, by serial draws in the oracle --
+    through the block KPM kernel (a 2-probe block at the full 300 moments; a full 16-probe block at
+    40), moments within 1e-12 of the oracle's."""
+    from oracle import clib
+    api = _api()
+    A = api.DeviceCsr.laplacian([160, 160, 160])
+    rp, ci, v = clib.laplacian([160, 160, 160])
+    z = api.kpm_moments(A, api.SpectralBounds(0.0, 12.0), m, 128, seed=0, first=first, count=count)
+    zr = clib.kpm_moments(rp, ci, v, 0.0, 12.0, m, 128, 0, first=first, count=count)
+    tol = 1e-12 * np.maximum(np.abs(zr), abs(zr[0]))
+    assert np.all(np.abs(z - zr) <= tol), np.max(np.abs(z - zr) / abs(zr[0]))
+
+
+def test_cfg5_full_size_scaling_bitwise(gpu_ctx):
+    """BASELINE cfg5 at full size: the device D A D of the 128^3 Laplacian with the seeded lumped
+    mass is bit-identical to the host formula (vals[p] = (a_ij d_i) d_j)."""
+    api = _api()
+    A = api.DeviceCsr.laplacian([128, 128, 128])
+    _, d = api.mass_scaling(A.n, 1234)
+    A.scale_sym(d)
+    got = A.download()
+    ref = api.scale_sym_host(api.gen_laplacian([128, 128, 128]), d)
+    assert np.array_equal(got.row_ptr, ref.row_ptr) and np.array_equal(got.col_idx, ref.col_idx)
+    assert np.array_equal(got.vals, ref.vals)
