@@ -438,3 +438,20 @@ def test_cfg5_full_size_scaling_bitwise(gpu_ctx):
     ref = api.scale_sym_host(api.gen_laplacian([128, 128, 128]), d)
     assert np.array_equal(got.row_ptr, ref.row_ptr) and np.array_equal(got.col_idx, ref.col_idx)
     assert np.array_equal(got.vals, ref.vals)
+
+
+def test_cfg4_full_size_spmv_and_moments(gpu_ctx):
+    """BASELINE cfg4 at full size (n = 2,000,000 random banded + 8 extras, ~46 M nnz): the device
+    SpMV is bit-identical to the oracle's row loop, and KPM moments of a 2-probe subset (the CSR
+    stream kernel: rows exceed the padded width) match the oracle within 1e-12."""
+    from oracle import clib
+    api = _api()
+    a = api.gen_random_sparse(2_000_000, 1234)
+    assert a.nnz > 40_000_000
+    x = clib.rng_vectors(3, "normal", a.n)[0]
+    assert np.array_equal(a.matvec(x), clib.matvec(a.row_ptr, a.col_idx, a.vals, x))
+    b = api.lan_tr_bounds(a, 1e-4, 60, 40, 1234)
+    z = api.kpm_moments(a, b, 60, 40, seed=1234, first=7, count=2)
+    zr = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, b.lmin, b.lmax, 60, 40, 1234, first=7, count=2)
+    tol = 1e-12 * np.maximum(np.abs(zr), abs(zr[0]))
+    assert np.all(np.abs(z - zr) <= tol), np.max(np.abs(z - zr) / abs(zr[0]))
