@@ -983,10 +983,18 @@ void apply_filter_block(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, con
     apply_filter_dev(c, a, op, nvec, v, out);
     return;
   }
+  // balanced groups of <= 8 columns (9 -> 5 + 4, not 8 + 1: a nearly empty multi-vector launch
+  // costs almost a full one); groups of one or two columns take the single-vector chain
+  const int ngroups = (nvec + 7) / 8;
   double* buf = dev_alloc<double>((size_t)n * 24);
   try {
-    for (int c0 = 0; c0 < nvec; c0 += 8) {
-      const int nv = std::min(8, nvec - c0);
+    for (int g = 0, c0 = 0; g < ngroups; ++g) {
+      const int nv = nvec / ngroups + (g < nvec % ngroups ? 1 : 0);
+      if (nv <= 2) {
+        apply_filter_dev(c, a, op, nv, v + (size_t)c0 * n, out + (size_t)c0 * n);
+        c0 += nv;
+        continue;
+      }
       for (int j = 1; j <= op.k; ++j) {
         k::MultiArgs m{};
         m.nv = nv;
@@ -1005,6 +1013,7 @@ void apply_filter_block(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, con
         }
         k::spmv_cheb_multi(c, a, m);
       }
+      c0 += nv;
     }
     ctx_sync(c);
   } catch (...) {

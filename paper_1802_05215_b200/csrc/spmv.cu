@@ -196,17 +196,31 @@ __global__ void __launch_bounds__(kMRows * kMV) k_spmv_cheb_multi(int n, const i
   const int r = r0 + lr;
   const int rend = min(r0 + kMRows, n);
   const int base = __ldg(rp + r0), end = __ldg(rp + rend);
+  int rs = end, re = end;
+  if (r < n) {
+    rs = __ldg(rp + r);
+    re = __ldg(rp + r + 1);
+  }
+  auto stage = [&](int c0) {  // independent of the previous kernel: issued before the PDL wait
+    const int cend = c0 + min(kStage, end - c0);
+    const int va = c0 & ~1, ca = c0 & ~3;
+    const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
+    for (int t = threadIdx.x; t < nv16; t += kMRows * kMV)
+      cp_async16(&s_v[2 * t], v + va + 2 * t, 8 * min(2, cend - (va + 2 * t)));
+    for (int t = threadIdx.x; t < nc16; t += kMRows * kMV)
+      cp_async16(&s_c[4 * t], ci + ca + 4 * t, 4 * min(4, cend - (ca + 4 * t)));
+  };
+  if (base < end) stage(base);
+  pdl_wait();
+  pdl_trigger();
   const bool on = q < a.nv && !(a.ctl[q] && a.ctl[q]->halted);
   const bool live = on && r < n;
   size_t ioff = 0;
   const double* __restrict__ x = nullptr;
-  int rs = end, re = end;
   double xr = 0.0, pv = 0.0, ov = 0.0;
   if (live) {
     ioff = a.ctl[q] ? (size_t)a.ctl[q]->i * a.ld : 0;
     x = a.x[q] + (a.x_ind[q] ? ioff : 0);
-    rs = __ldg(rp + r);
-    re = __ldg(rp + r + 1);
     xr = __ldg(x + r);
     if (!a.first[q]) {
       pv = __ldg(a.prev[q] + (a.prev_ind[q] ? ioff : 0) + r);
@@ -217,12 +231,10 @@ __global__ void __launch_bounds__(kMRows * kMV) k_spmv_cheb_multi(int n, const i
   for (int c0 = base; c0 < end; c0 += kStage) {
     const int cn = min(kStage, end - c0), cend = c0 + cn;
     const int va = c0 & ~1, ca = c0 & ~3;
-    const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
-    __syncthreads();
-    for (int t = threadIdx.x; t < nv16; t += kMRows * kMV)
-      cp_async16(&s_v[2 * t], v + va + 2 * t, 8 * min(2, cend - (va + 2 * t)));
-    for (int t = threadIdx.x; t < nc16; t += kMRows * kMV)
-      cp_async16(&s_c[4 * t], ci + ca + 4 * t, 4 * min(4, cend - (ca + 4 * t)));
+    if (c0 != base) {
+      __syncthreads();  // the previous chunk's readers are done
+      stage(c0);
+    }
     cp_async_wait_all();
     __syncthreads();
     if (live) {
@@ -872,10 +884,22 @@ size_t kpm_scratch_doubles(const Ctx& c, int n) {
 void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args) {
   if (a.n == 0 || args.nv == 0) return;
   if (args.nv > kMV) fail(SE_EINVAL, "spmv_cheb_multi: too many vectors");
-  k_spmv_cheb_multi<<<(a.n + kMRows - 1) / kMRows, kMRows * kMV, 0, c.stream>>>(a.n, a.rp, a.ci,
-                                                                                a.v, args);
+  // programmatic dependent launch (the A staging overlaps the previous degree's tail) and the
+  // filter launches' high priority, as for k_spmv_cheb
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((a.n + kMRows - 1) / kMRows);
+  cfg.blockDim = dim3(kMRows * kMV);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = c.prio_hi;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  SE_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_cheb_multi, a.n, (const int*)a.rp, (const int*)a.ci,
+                             (const double*)a.v, args));
   ++c.launches;
-  SE_CUDA(cudaGetLastError());
 }
 
 void expand_rademacher(Ctx& c, const std::uint64_t* bits, double* rm, int n, int b, int bk) {
