@@ -82,6 +82,8 @@ int grid_for(const Ctx& c, int n) {
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_norm_before(int n, const double* __restrict__ t,
                                                           Ctl* ctl, double* partial, unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl->halted) return;
   double s = 0.0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
@@ -100,6 +102,8 @@ __global__ void __launch_bounds__(kThreads) k_nr_beta_alpha(int n, double* __res
                                                             const double* __restrict__ W, Ctl* ctl,
                                                             double* alpha_arr, const double* beta_arr,
                                                             double* partial, unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl->halted) return;
   const int i = ctl->i;
   const double beta = i > 0 ? beta_arr[i - 1] : 0.0;
@@ -125,6 +129,8 @@ __global__ void __launch_bounds__(kThreads) k_nr_beta_alpha(int n, double* __res
 __global__ void __launch_bounds__(kThreads) k_nr_sub_alpha(int n, double* __restrict__ t,
                                                            const double* __restrict__ W, Ctl* ctl,
                                                            double* partial, unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl->halted) return;
   const double alpha = ctl->alpha;
   const double* __restrict__ w = W + (size_t)ctl->i * n;
@@ -162,7 +168,10 @@ __global__ void __launch_bounds__(kThreads) k_gemvt(int n, int rch, const double
                                                     unsigned* grp_cnt, double* coef, double* hdiag) {
   // One work item per CTA (short-lived CTAs keep SM slots turning over, so the latency-bound
   // kernels of other slices sharing the GPU are scheduled promptly).  Items beyond the current
-  // column count exit at once.
+  // column count exit at once.  Programmatic dependent launch: the CTA is resident before the
+  // previous kernel ends and waits here.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl && pass_skip(ctl, pass2)) return;
   const int ncols = pass_ncols(ctl, mode, fixed);
   const int nrb = (n + rch - 1) / rch;
@@ -224,6 +233,8 @@ __global__ void __launch_bounds__(kThreads) k_gemvn(int n, const double* __restr
                                                     const double* __restrict__ coef,
                                                     double* __restrict__ P, unsigned* rb_cnt,
                                                     double* npart, unsigned* gcnt, int nw) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl && pass_skip(ctl, pass2)) return;
   const int ncols = pass_ncols(ctl, mode, fixed);
   const int nchunks = (ncols + nw - 1) / nw;
@@ -294,6 +305,8 @@ __global__ void __launch_bounds__(kThreads) k_gemvn(int n, const double* __restr
 __global__ void __launch_bounds__(kThreads) k_normalize(int n, const double* __restrict__ t,
                                                         double* __restrict__ W, Ctl* ctl,
                                                         double* beta_arr, unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl->halted) return;
   const double beta = ctl->after;
   const int i = ctl->i;
@@ -375,6 +388,8 @@ __global__ void k_scale_copy(int n, double a, const double* __restrict__ src, do
 }
 
 __global__ void k_stamp(Ctl* ctl, int which) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl->halted) return;
   unsigned long long now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
@@ -395,6 +410,38 @@ int rch_for(int n) {
   }();
   if (force > 0) return std::min(force, kMaxRch);
   return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512);
+}
+
+// programmatic-dependent launch of a step kernel (the kernel starts with griddepcontrol.wait)
+template <class K, class... Args>
+void launch_pdl(const Ctx& c, K kern, dim3 grid, dim3 block, size_t smem, Args... args) {
+  static const bool pdl = std::getenv("SE_NO_GEMV_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  SE_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
+// launch attributes of the GEMV kernels: programmatic dependent launch (SE_NO_GEMV_PDL=1: off)
+cudaLaunchConfig_t gemv_cfg(const Ctx& c, dim3 grid, size_t smem, cudaLaunchAttribute* attr) {
+  static const bool pdl = std::getenv("SE_NO_GEMV_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cfg;
 }
 
 // columns per GEMV-N chunk (<= kNW)
@@ -430,7 +477,7 @@ static void need(const Scratch& s, size_t doubles, int slots) {
 void norm_before(Ctx& c, const Scratch& s, int n, const double* t, Ctl* ctl) {
   const int g = grid_for(c, n);
   need(s, g, kSlotMisc + 1);
-  k_norm_before<<<g, kThreads, 0, c.stream>>>(n, t, ctl, s.buf, s.cnt + kSlotNorm);
+  launch_pdl(c, k_norm_before, dim3(g), dim3(kThreads), 0, n, (const double*)t, ctl, s.buf, s.cnt + kSlotNorm);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -439,8 +486,8 @@ void nr_beta_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, 
                    double* alpha_arr, const double* beta_arr) {
   const int g = grid_for(c, n);
   need(s, g, kSlotMisc + 1);
-  k_nr_beta_alpha<<<g, kThreads, 0, c.stream>>>(n, t, W, ctl, alpha_arr, beta_arr, s.buf,
-                                                s.cnt + kSlotNorm);
+  launch_pdl(c, k_nr_beta_alpha, dim3(g), dim3(kThreads), 0, n, t, W, ctl, alpha_arr, beta_arr, s.buf,
+             s.cnt + kSlotNorm);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -448,7 +495,7 @@ void nr_beta_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, 
 void nr_sub_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, Ctl* ctl) {
   const int g = grid_for(c, n);
   need(s, g, kSlotMisc + 1);
-  k_nr_sub_alpha<<<g, kThreads, 0, c.stream>>>(n, t, W, ctl, s.buf, s.cnt + kSlotNorm);
+  launch_pdl(c, k_nr_sub_alpha, dim3(g), dim3(kThreads), 0, n, t, W, ctl, s.buf, s.cnt + kSlotNorm);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -466,12 +513,14 @@ static void cgs_impl(Ctx& c, const Scratch& s, int n, double* t, const double* Q
   double* part = s.buf;
   double* P = part + (size_t)nrb * ldp;
   double* npart = P + (size_t)ncc * n;
-  k_gemvt<<<nrb * ngrp_max, kThreads, rch * sizeof(double), c.stream>>>(n, rch, Q, t, ctl, mode, pass2 ? 1 : 0, fixed,
-                                                     part, ldp, s.cnt + kSlotGroups, coef, hdiag);
+  { cudaLaunchAttribute at[1]; const cudaLaunchConfig_t cf = gemv_cfg(c, dim3(nrb * ngrp_max), rch * sizeof(double), at);
+  SE_CUDA(cudaLaunchKernelEx(&cf, k_gemvt, n, rch, Q, t, ctl, mode, pass2 ? 1 : 0, fixed,
+                                                     part, ldp, s.cnt + kSlotGroups, coef, hdiag)); }
   ++c.launches;
-  k_gemvn<<<dim3(gn, ncc), kThreads, 0, c.stream>>>(n, Q, t, ctl, mode, pass2 ? 1 : 0, fixed, coef, P,
+  { cudaLaunchAttribute at[1]; const cudaLaunchConfig_t cf = gemv_cfg(c, dim3(gn, ncc), 0, at);
+  SE_CUDA(cudaLaunchKernelEx(&cf, k_gemvn, n, Q, t, ctl, mode, pass2 ? 1 : 0, fixed, coef, P,
                                                     s.cnt + kSlotGroups + ngrp_max, npart,
-                                                    s.cnt + kSlotMisc, nw_for());
+                                                    s.cnt + kSlotMisc, nw_for())); }
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -484,8 +533,9 @@ void gemvt_only(Ctx& c, const Scratch& s, int n, const double* t, const double* 
   const int nrb = (n + rch - 1) / rch;
   const int ngrp_max = (ldp + kCW - 1) / kCW;
   need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
-  k_gemvt<<<nrb * ngrp_max, kThreads, rch * sizeof(double), c.stream>>>(n, rch, Q, t, ctl, 0, pass2 ? 1 : 0, -1, s.buf,
-                                                     ldp, s.cnt + kSlotGroups, coef, hdiag);
+  { cudaLaunchAttribute at[1]; const cudaLaunchConfig_t cf = gemv_cfg(c, dim3(nrb * ngrp_max), rch * sizeof(double), at);
+  SE_CUDA(cudaLaunchKernelEx(&cf, k_gemvt, n, rch, Q, t, ctl, 0, pass2 ? 1 : 0, -1, s.buf,
+                                                     ldp, s.cnt + kSlotGroups, coef, hdiag)); }
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -502,9 +552,10 @@ void gemvn_only(Ctx& c, const Scratch& s, int n, double* t, const double* Q, boo
   need(s, cgs_scratch_doubles(c, n, ldp), cgs_counter_slots(n, ldp));
   double* P = s.buf + (size_t)nrb * ldp;
   double* npart = P + (size_t)ncc * n;
-  k_gemvn<<<dim3(gn, ncc), kThreads, 0, c.stream>>>(n, Q, t, ctl, 0, pass2 ? 1 : 0, -1, coef, P,
+  { cudaLaunchAttribute at[1]; const cudaLaunchConfig_t cf = gemv_cfg(c, dim3(gn, ncc), 0, at);
+  SE_CUDA(cudaLaunchKernelEx(&cf, k_gemvn, n, Q, t, ctl, 0, pass2 ? 1 : 0, -1, coef, P,
                                                     s.cnt + kSlotGroups + ngrp_max, npart,
-                                                    s.cnt + kSlotMisc, nw_for());
+                                                    s.cnt + kSlotMisc, nw_for())); }
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -524,7 +575,7 @@ void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W,
                     double* beta_arr) {
   const int g = grid_for(c, n);
   need(s, 0, kSlotMisc + 1);
-  k_normalize<<<g, kThreads, 0, c.stream>>>(n, t, W, ctl, beta_arr, s.cnt + kSlotNorm);
+  launch_pdl(c, k_normalize, dim3(g), dim3(kThreads), 0, n, t, W, ctl, beta_arr, s.cnt + kSlotNorm);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
@@ -552,7 +603,7 @@ void scale_copy(Ctx& c, int n, double a, const double* src, double* dst) {
 }
 
 void stamp(Ctx& c, Ctl* ctl, int which) {
-  k_stamp<<<1, 1, 0, c.stream>>>(ctl, which);
+  launch_pdl(c, k_stamp, dim3(1), dim3(1), 0, ctl, which);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }
