@@ -690,7 +690,7 @@ def _pencil_scaled(a, d, b, who, solve, want_vectors=True):
     x = r.vectors * dsc[:, None]
     res = np.empty(r.eigenvalues.size)
     for j in range(r.eigenvalues.size):
-        res[j] = np.linalg.norm(d_matvec(d, x[:, j]) - r.eigenvalues[j] * (bd * x[:, j]))
+        res[j] = np.linalg.norm(_d_matvec(d, x[:, j]) - r.eigenvalues[j] * (bd * x[:, j]))
     return EigenResults(r.eigenvalues, x if want_vectors else None, res, r.niter, r.counters,
                         r.hit_max_its)
 
@@ -704,7 +704,7 @@ def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who
     return _pencil_scaled(a, d, b, who, solve, want_vectors)
 
 
-def d_matvec(d: "DeviceCsr", x) -> np.ndarray:
+def _d_matvec(d: "DeviceCsr", x) -> np.ndarray:
     """y = A x on the GPU (csr.hpp:98-105)."""
     x = _f64(x)
     y = np.empty(d.n)
@@ -771,7 +771,7 @@ def rayleigh_and_residual(a, b, u) -> tuple[float, float]:
         db = _dev(b)
         if db.n != d.n:
             raise ValueError("rayleigh_and_residual: pencil size mismatch")
-        au, bu = d_matvec(d, u), d_matvec(db, u)
+        au, bu = _d_matvec(d, u), _d_matvec(db, u)
         uu = float(np.dot(u, bu))
         if not uu > 0.0:
             raise ValueError("rayleigh_and_residual: zero (or B-degenerate) vector")
