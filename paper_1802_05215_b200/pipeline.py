@@ -33,7 +33,7 @@ class Plan:
     xi: float
     eta: float
     ns: int = 1
-    solver: str = "nr"            # nr | tr
+    solver: str = "nr"            # nr | tr | si
     damping: str = "sigma"        # sigma | jackson | none
     dos_m: int = 60
     dos_nvec: int = 40
@@ -249,8 +249,13 @@ class GpuBackend:
             f = api.find_pol(lo, hi, api.SpectralBounds(lmin, lmax), api.PolyOpts(damping=plan.damping))
             cfg = api.SolverConfig(m=plan.solver_m, res_tol=plan.tol, seed=plan.seed,
                                    est_count=max(1, int(math.ceil(est))))
-            drv = api.cheb_lan_tr if plan.solver == "tr" else api.cheb_lan_nr
-            r = drv(A, None, f, lo, hi, cfg, want_vectors=plan.want_vectors)
+            if plan.solver == "si":  # filtered subspace iteration (eigensolvers.hpp:760-940)
+                r = api.cheb_si(A, None, f, lo, hi, cfg.est_count, cfg, want_vectors=plan.want_vectors)
+            elif plan.solver in ("tr", "nr"):
+                drv = api.cheb_lan_tr if plan.solver == "tr" else api.cheb_lan_nr
+                r = drv(A, None, f, lo, hi, cfg, want_vectors=plan.want_vectors)
+            else:
+                raise ValueError(f"unknown solver {plan.solver!r} (nr | tr | si)")
         finally:
             A.handle = None  # borrowed handle: do not free
         return f.k, r
