@@ -455,3 +455,22 @@ def test_cfg4_full_size_spmv_and_moments(gpu_ctx):
     zr = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, b.lmin, b.lmax, 60, 40, 1234, first=7, count=2)
     tol = 1e-12 * np.maximum(np.abs(zr), abs(zr[0]))
     assert np.all(np.abs(z - zr) <= tol), np.max(np.abs(z - zr) / abs(zr[0]))
+
+
+@pytest.mark.parametrize("solver", ["nr", "tr", "si"])
+def test_pipeline_solvers_match_reference_cli(gpu_ctx, golden, solver):
+    """The Python pipeline (pipeline.run, the bench's and the multi-rank path's driver) with each
+    solver on the reference CLI case `solve --dims 30,30 --interval 0.4,0.6 --slices 4` (KPM 60 x 40
+    Rademacher, sigma damping, tol 1e-8, seed 1234): same breakpoints and per-slice eigenvalues as
+    the reference's cmd_solve (tests/golden/cli.npz)."""
+    from paper_1802_05215_b200.pipeline import GpuBackend, Plan, run
+    g = golden("cli")
+    plan = Plan(xi=0.4, eta=0.6, ns=4, solver=solver, damping="sigma", dos_m=60, dos_nvec=40,
+                probes="rademacher", tol=1e-8, seed=1234)
+    r = run(plan, GpuBackend(dims=[30, 30]))
+    assert np.allclose(r.breakpoints, g[f"{solver}_bp"], rtol=1e-12, atol=0)
+    for s in r.slices:
+        assert s.error is None, s.error
+        ref = g[f"{solver}_slice{s.index}_vals"]
+        assert s.eigenvalues.size == ref.size, (s.index, s.eigenvalues.size, ref.size)
+        assert np.all(np.abs(s.eigenvalues - ref) <= 1e-10 * np.abs(ref))
