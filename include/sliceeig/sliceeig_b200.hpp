@@ -688,14 +688,15 @@ inline EigenResults pencil_scaled(const CsrMatrix& a, const CsrMatrix& b, const 
   for (int i = 0; i < n; ++i)
     for (int p = rp[i]; p < rp[i + 1]; ++p) v[p] = (v[p] * d[i]) * d[ci[p]];
   const CsrMatrix s = CsrMatrix::from_csr(n, std::move(rp), std::move(ci), std::move(v));
+  // candidates are judged on the pencil residual ||A x - lambda B x|| / sqrt(x'Bx) = ||D^-1 r_s||
+  // (eigensolvers.hpp:289-316), so acceptance matches the reference's B-weighted path
+  Vec w(n);
+  for (int i = 0; i < n; ++i) w[i] = std::sqrt(bd[i]);
+  ok(se_csr_set_residual_weight(ctx(), s.device(), w.data()));
   EigenResults r = solve(s, d);
   for (int j = 0; j < r.vectors.cols(); ++j) {
     double* x = r.vectors.col(j);
     for (int i = 0; i < n; ++i) x[i] *= d[i];
-    const Vec xv = r.vectors.col_vec(j);
-    Vec rr = a.matvec(xv);
-    for (int i = 0; i < n; ++i) rr[i] -= r.eigenvalues[j] * (bd[i] * xv[i]);
-    r.residuals[j] = nrm2(rr);
   }
   return r;
 }

@@ -21,6 +21,7 @@
 #ifndef SLICEEIG_CUDA_H
 #define SLICEEIG_CUDA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -91,6 +92,9 @@ typedef struct se_counters {
 SE_API const char* se_last_error(void);
 SE_API const char* se_version(void);
 SE_API int se_device_count(int* count);
+/* Free / total bytes of a device's memory (sizes the memory plan's solve windows; no reference
+   counterpart: the reference is host code). */
+SE_API int se_device_memory(int device, size_t* free_bytes, size_t* total_bytes);
 
 /* ---- contexts ----------------------------------------------------------------------------- */
 SE_API int se_ctx_create(int device, se_ctx** out);
@@ -126,6 +130,11 @@ SE_API int se_csr_info(const se_csr* a, int* n, long* nnz);
 SE_API int se_csr_download(se_ctx* ctx, const se_csr* a, int* row_ptr, int* col_idx, double* vals);
 /* vals[p] *= d[i] * d[j] for stored (i, j = col_idx[p]): diagonal congruence D A D (BASELINE cfg5). */
 SE_API int se_csr_scale_sym(se_ctx* ctx, se_csr* a, const double* d_host);
+/* Residual weights w (n doubles, NULL clears): candidate residuals become
+   ||w .* (A u - lambda u)|| / sqrt(u.u).  For S = D A D of a diagonal-B pencil, w = D^-1 makes
+   them the reference's ||A x - lambda B x|| / sqrt(x'Bx), x = D u (eigensolvers.hpp:289-316), so
+   convergence is decided on the pencil residual. */
+SE_API int se_csr_set_residual_weight(se_ctx* ctx, se_csr* a, const double* w_host);
 SE_API int se_csr_free(se_csr* a);
 
 /* ---- operator applications ---------------------------------------------------------------- */
@@ -238,6 +247,9 @@ SE_API int se_results_count(const se_results* r, int* nev);
 /* eigenvalues/residuals (nev each, ascending by eigenvalue), vectors (n x nev, may be NULL). */
 SE_API int se_results_copy(const se_results* r, double* eigenvalues, double* residuals, double* vectors);
 SE_API int se_results_info(const se_results* r, long* niter, int* hit_max_its, se_counters* counters);
+/* Reorthogonalisation accounting of a slice solve (extension, measurement only): projection
+   passes over the Krylov basis, basis columns summed over them, algorithmic HBM bytes. */
+SE_API int se_results_orth(const se_results* r, long long* passes, long long* cols, double* bytes);
 SE_API int se_results_free(se_results* r);
 
 /* ---- checks ---------------------------------------------------------------------------------- */

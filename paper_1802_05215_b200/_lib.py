@@ -65,6 +65,7 @@ SIGNATURES = {
     "se_csr_info": [_VP, _PI, _PL],
     "se_csr_download": [_VP, _VP, _PI, _PI, _PD],
     "se_csr_scale_sym": [_VP, _VP, _PD],
+    "se_csr_set_residual_weight": [_VP, _VP, _PD],
     "se_csr_free": [_VP],
     "se_spmv": [_VP, _VP, _PD, _PD],
     "se_cheb_apply": [_VP, _VP, C.POINTER(SePolyFilter), C.c_int, _PD, _PD, _PL],
@@ -90,6 +91,8 @@ SIGNATURES = {
                    _PD, _PD, _PD],
     "se_lan_dos": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double,
                    C.c_uint64, _PD, _PD, _PD],
+    "se_results_orth": [_VP, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), _PD],
+    "se_device_memory": [C.c_int, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)],
     "se_dos_count": [C.c_int, C.c_int, _PD, _PD, C.c_double, C.c_double, _PD],
     "se_slice_spectrum": [C.c_int, C.c_int, _PD, _PD, C.c_double, C.c_double, C.c_int, _PD, _PD],
     "se_lan_tr_bounds": [_VP, _VP, C.c_double, C.c_int, C.c_int, C.c_uint64, _PD, _PD],

@@ -84,6 +84,13 @@ def device_count() -> int:
     return v.value
 
 
+def device_memory(device: int = 0) -> tuple[int, int]:
+    """(free, total) bytes of a device's memory."""
+    f, t = C.c_size_t(), C.c_size_t()
+    call("se_device_memory", device, C.byref(f), C.byref(t))
+    return f.value, t.value
+
+
 # ---- matrices (csr.hpp, laplacian.hpp) ------------------------------------------------------------
 class DeviceCsr:
     """A CSR matrix resident in HBM (se_csr)."""
@@ -122,6 +129,12 @@ class DeviceCsr:
     def scale_sym(self, d: np.ndarray):
         d = _f64(d)
         call("se_csr_scale_sym", self.ctx.handle, self.handle, _pd(d))
+
+    def set_residual_weight(self, w: Optional[np.ndarray]):
+        """Candidate residuals ||w .* (A u - lambda u)|| / sqrt(u.u) (None clears)."""
+        wf = None if w is None else _f64(w)
+        call("se_csr_set_residual_weight", self.ctx.handle, self.handle,
+             _pd(wf) if wf is not None else None)
 
     def free(self):
         if self.handle:
@@ -614,6 +627,14 @@ class DeflationSet:
 
 
 @dataclass
+class OrthStats:
+    """Reorthogonalisation accounting of a device slice solve (extension, measurement only)."""
+    passes: int = 0
+    cols: int = 0
+    bytes: float = 0.0
+
+
+@dataclass
 class EigenResults:
     eigenvalues: np.ndarray
     vectors: Optional[np.ndarray]  # (n, nev): column i pairs with eigenvalues[i]
@@ -621,6 +642,7 @@ class EigenResults:
     niter: int
     counters: Counters
     hit_max_its: bool
+    orth: OrthStats = field(default_factory=OrthStats)
 
 
 def _host_buffer(shape):
@@ -684,15 +706,14 @@ def _pencil_scaled(a, d, b, who, solve, want_vectors=True):
     S = DeviceCsr.upload(host, d.ctx)
     try:
         S.scale_sym(dsc)
+        # candidates are judged (and reported) on the pencil residual
+        # ||A x - lambda B x|| / sqrt(x'Bx) = ||D^-1 (S y - lambda y)|| / sqrt(y'y), x = D y
+        S.set_residual_weight(np.sqrt(bd))
         r = solve(S, dsc)
     finally:
         S.free()
-    x = r.vectors * dsc[:, None]
-    res = np.empty(r.eigenvalues.size)
-    for j in range(r.eigenvalues.size):
-        res[j] = np.linalg.norm(_d_matvec(d, x[:, j]) - r.eigenvalues[j] * (bd * x[:, j]))
-    return EigenResults(r.eigenvalues, x if want_vectors else None, res, r.niter, r.counters,
-                        r.hit_max_its)
+    x = r.vectors * dsc[:, None] if (want_vectors and r.vectors is not None) else None
+    return EigenResults(r.eigenvalues, x, r.residuals, r.niter, r.counters, r.hit_max_its, r.orth)
 
 
 def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who):
@@ -700,7 +721,7 @@ def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who
         ly = None
         if locked is not None and locked.count() > 0:  # locked pencil vectors x -> y = D^-1 x
             ly = DeflationSet(np.asarray(locked.u, np.float64) / dsc[:, None], locked.values)
-        return _cheb_lan(solver, S, None, f, xi, eta, cfg, ly, True)
+        return _cheb_lan(solver, S, None, f, xi, eta, cfg, ly, want_vectors)
     return _pencil_scaled(a, d, b, who, solve, want_vectors)
 
 
@@ -725,12 +746,15 @@ def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
         niter, hit = C.c_long(), C.c_int()
         cn = _lib.SeCounters()
         call("se_results_info", h, C.byref(niter), C.byref(hit), C.byref(cn))
+        op, oc, ob = C.c_longlong(), C.c_longlong(), C.c_double()
+        call("se_results_orth", h, C.byref(op), C.byref(oc), C.byref(ob))
     finally:
         call("se_results_free", h)
     counters = Counters(cn.n_A_matvec, cn.n_B_matvec, cn.n_B_solve, cn.n_shift_solve, cn.t_mv,
                         cn.t_orth, cn.t_sv, cn.t_total)
     return EigenResults(vals, vecs.T if vecs is not None else (np.zeros((d.n, 0)) if want_vectors else None),
-                        res, niter.value, counters, bool(hit.value))
+                        res, niter.value, counters, bool(hit.value),
+                        OrthStats(op.value, oc.value, ob.value))
 
 
 def cheb_si(a, b, f: PolynomialFilter, xi: float, eta: float, est_count: int,
@@ -740,7 +764,8 @@ def cheb_si(a, b, f: PolynomialFilter, xi: float, eta: float, est_count: int,
     d = _dev(a)
     if b is not None:  # diagonal SPD B: the scaled standard problem (_pencil_scaled)
         return _pencil_scaled(a, d, b, "cheb_si",
-                              lambda S, dsc: cheb_si(S, None, f, xi, eta, est_count, cfg, True),
+                              lambda S, dsc: cheb_si(S, None, f, xi, eta, est_count, cfg,
+                                                     want_vectors),
                               want_vectors)
     s, _keep = f._c()
     c = _lib.SeSolverCfg(cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed)

@@ -104,6 +104,16 @@ extern "C" {
 const char* se_last_error(void) { return g_err.c_str(); }
 const char* se_version(void) { return "sliceeig-b200 0.1 (sm_100a)"; }
 
+int se_device_memory(int device, size_t* free_bytes, size_t* total_bytes) {
+  return guard([&] {
+    SE_CUDA(cudaSetDevice(device));
+    size_t f = 0, t = 0;
+    SE_CUDA(cudaMemGetInfo(&f, &t));
+    if (free_bytes) *free_bytes = f;
+    if (total_bytes) *total_bytes = t;
+  });
+}
+
 int se_device_count(int* count) {
   return guard([&] {
     int c = 0;
@@ -366,11 +376,29 @@ int se_csr_scale_sym(se_ctx* ctx, se_csr* a, const double* d_host) {
   });
 }
 
+int se_csr_set_residual_weight(se_ctx* ctx, se_csr* a, const double* w_host) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (!a) fail(SE_EINVAL, "null se_csr");
+    if (!w_host) {
+      ctx_sync(c);
+      dev_free_shared(a->a.resw);
+      a->a.resw = nullptr;
+      return;
+    }
+    if (!a->a.resw) a->a.resw = dev_alloc_shared<double>(std::max(a->a.n, 1));
+    SE_CUDA(cudaMemcpyAsync(a->a.resw, w_host, sizeof(double) * a->a.n, cudaMemcpyHostToDevice,
+                            c.stream));
+    ctx_sync(c);
+  });
+}
+
 int se_csr_free(se_csr* a) {
   return guard([&] {
     if (!a) return;
     cudaSetDevice(a->a.device);
     dev_free_shared(a->a.rp);
+    dev_free_shared(a->a.resw);
     a->a.free_entries();
     if (a->a.ell_c) {
       dev_free_shared(a->a.ell_c);
@@ -924,8 +952,10 @@ int se_cheb_si(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi,
     Ctx& c = C(ctx);
     if (!(eta > xi)) fail(SE_EINVAL, "cheb_si: degenerate interval");
     if (est_count < 0) fail(SE_EINVAL, "cheb_si: negative est_count");
-    se_solver_cfg rc = *cfg;  // est_count = max(cfg.est_count, est_count) (eigensolvers.hpp:770-772)
-    rc.est_count = std::max(cfg->est_count, est_count);
+    // NULL selects the defaults, as in se_cheb_lan (resolve_config);
+    // est_count = max(cfg.est_count, est_count) (eigensolvers.hpp:770-772)
+    se_solver_cfg rc = cfg ? *cfg : se_solver_cfg{0, 0, 30, 0.0, 1e-8, 20, 1234};
+    rc.est_count = std::max(rc.est_count, est_count);
     const SolverCfg sc = resolve_config(&rc, "cheb_si");
     auto res = std::make_unique<se_results>();
     res->device = c.device;
@@ -964,6 +994,15 @@ int se_results_info(const se_results* r, long* niter, int* hit_max_its, se_count
   });
 }
 
+int se_results_orth(const se_results* r, long long* passes, long long* cols, double* bytes) {
+  return guard([&] {
+    if (!r) fail(SE_EINVAL, "null results");
+    if (passes) *passes = r->r->orth_passes;
+    if (cols) *cols = r->r->orth_cols;
+    if (bytes) *bytes = r->r->orth_bytes;
+  });
+}
+
 int se_results_free(se_results* r) {
   return guard([&] {
     if (!r) return;
@@ -985,7 +1024,7 @@ int se_rayleigh_residual(se_ctx* ctx, const se_csr* a, const double* u, double* 
     SE_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * m.n, cudaMemcpyHostToDevice, c.stream));
     StepOp op;
     apply_filter_dev(c, m, op, 1, du, dau);
-    k::candidate_stats(c, m.n, 1, du, dau, st);
+    k::candidate_stats(c, m.n, 1, du, dau, st, m.resw);
     double h[3];
     SE_CUDA(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     ctx_sync(c);

@@ -43,6 +43,10 @@ struct DevCsr {
   int max_row_nnz = 0;
   int* ell_c = nullptr;     // padded copy (max_row_nnz <= kEllW), else null
   double* ell_a = nullptr;
+  // residual weights w (null: none): candidates report ||w .* (A u - lambda u)|| / sqrt(u.u).
+  // Set on D A D of a diagonal-B pencil with w = D^-1, which makes the residual the reference's
+  // ||A x - lambda B x|| / sqrt(x' B x) for x = D u (eigensolvers.hpp:289-316)
+  double* resw = nullptr;
   // vals and col_idx live in ONE allocation (vals first, col_idx right after) so a single L2
   // access-policy window covers the whole matrix stream of the filter SpMV
   void alloc_entries(long count);

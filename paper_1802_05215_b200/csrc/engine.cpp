@@ -379,7 +379,7 @@ struct CandBuf {
       a.ncols = std::min(65535, nc - j0);
       k::spmv_cheb(c, A, k::kPlain, a);
     }
-    k::candidate_stats(c, n, nc, U.p, AU.p, stats);
+    k::candidate_stats(c, n, nc, U.p, AU.p, stats, A.resw);
     out3.resize(3 * (size_t)nc);
     d2h(c, out3.data(), stats, sizeof(double) * 3 * nc);
     ctx_sync(c);
@@ -540,6 +540,10 @@ struct Slice {
     r->niter = its;
     r->hit_max_its = warn;
     r->counters = cnt;
+    const Ctl hc = kr.get();
+    r->orth_passes = hc.passes_total;
+    r->orth_cols = hc.cols_total;
+    r->orth_bytes = 16.0 * A.n * (double)hc.cols_total + 24.0 * A.n * (double)hc.passes_total;
     return r;
   }
 

@@ -37,6 +37,10 @@ struct SliceResult {
   bool hit_max_its = false;
   se_counters counters{};
   int n = 0;
+  // reorthogonalisation accounting (device counters): Krylov-basis projection passes, the
+  // basis columns they covered, and their algorithmic HBM bytes
+  long long orth_passes = 0, orth_cols = 0;
+  double orth_bytes = 0.0;
 };
 
 // Apply the filter (plain A or rho(Ahat)) to nvec column-major device vectors.

@@ -138,7 +138,8 @@ void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W,
                     double* beta_arr);
 // Candidate statistics (eigensolvers.hpp:289-316) per column of U (n x nc) and AU:
 // out3[3j..] = (lambda, residual, uu).  U is left unscaled (raw W y, kept for thick restart).
-void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3);
+void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3,
+                     const double* w = nullptr);
 void dot_dev(Ctx& c, const Scratch& s, int n, const double* x, const double* y, double* result_dev);
 void scale(Ctx& c, int n, double a, double* x);
 // dst = a * src (n doubles).

@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kThreads) k_normalize(int n, const double* __r
 //   uu = u.u, lambda = u.Au / uu, r = Au - lambda u, res = (1/sqrt(uu)) ||r||, u *= 1/sqrt(uu).
 __global__ void __launch_bounds__(kThreads) k_candidate_stats(int n, double* __restrict__ U,
                                                               const double* __restrict__ AU,
+                                                              const double* __restrict__ w,
                                                               double* out3) {
   const size_t off = (size_t)blockIdx.x * n;
   double* __restrict__ u = U + off;
@@ -356,7 +357,8 @@ __global__ void __launch_bounds__(kThreads) k_candidate_stats(int n, double* __r
   double srr = 0.0;
   if (uu > 0.0)
     for (int r = threadIdx.x; r < n; r += kThreads) {
-      const double rr = add(au[r], mul(-lam, u[r]));
+      double rr = add(au[r], mul(-lam, u[r]));
+      if (w) rr = mul(w[r], rr);
       srr = add(srr, mul(rr, rr));
     }
   const double trr = block_sum(srr);
@@ -580,9 +582,10 @@ void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W,
   SE_CUDA(cudaGetLastError());
 }
 
-void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3) {
+void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3,
+                     const double* w) {
   if (nc <= 0 || n == 0) return;
-  k_candidate_stats<<<nc, kThreads, 0, c.stream>>>(n, U, AU, out3);
+  k_candidate_stats<<<nc, kThreads, 0, c.stream>>>(n, U, AU, w, out3);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }

@@ -17,6 +17,7 @@ the test oracle (tests/test_pipeline_dist.py); the product backend is `GpuBacken
 """
 from __future__ import annotations
 
+import dataclasses
 import math
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -46,6 +47,24 @@ class Plan:
     jobs: int = 0                  # concurrent slices per rank (0: all of the rank's slices)
     only: Optional[Sequence[int]] = None  # debug/profiling: solve only these slice indices
     want_vectors: bool = False
+    # memory plan (SURVEY.md §7 hard part 4): a DOS slice whose estimate exceeds `window_est` is
+    # solved as consecutive sub-windows of near-equal DOS mass on its GPU (0: automatic -- the
+    # reference's m = 4 est must stay within dense_sym_eig's 5,000 guard, dense_eig.hpp:114-117,
+    # and each window's device footprint within the GPU's memory)
+    window_est: float = 0.0
+
+
+@dataclass
+class Window:
+    """One sub-window of a DOS slice (memory plan)."""
+    lo: float
+    hi: float
+    est: float
+    degree: int = 0
+    found: int = 0
+    niter: int = 0
+    seconds: float = 0.0
+    hit_max_its: bool = False
 
 
 @dataclass
@@ -67,6 +86,10 @@ class SliceOutcome:
     t_orth: float = 0.0
     error: Optional[str] = None
     rank: int = 0
+    windows: List[Window] = field(default_factory=list)
+    orth_passes: int = 0
+    orth_cols: int = 0
+    orth_bytes: float = 0.0
 
 
 @dataclass
@@ -204,6 +227,66 @@ def slice_clipped(curve: api.DosCurve, xi: float, eta: float, ns: int, slicer=No
     return bp, np.asarray(s.est_counts, np.float64)
 
 
+# ---- memory plan -----------------------------------------------------------------------------------
+# The reference sizes a slice solve as m = max(4 est, 80) basis columns (eigensolvers.hpp:144) and
+# its projected eigensolve refuses m > 5,000 (dense_eig.hpp:114-117), so a slice estimated above
+# 1,250 eigenpairs cannot run as one Lanczos window.  At BASELINE cfg4/cfg5 sizes (n ~ 2M, 5-13k
+# pairs per DOS slice) one window would also need 80-170 GB.  A large slice is therefore solved
+# as consecutive sub-windows of near-equal DOS mass, each an ordinary cheb_lan_* call whose result
+# is seam-trimmed exactly like neighbouring slices (sliceeig_main.cpp:422-442), with eigenvectors
+# copied to host memory as each window finishes, so device memory holds one window at a time.
+REF_WINDOW_EST = 1250.0      # 4 est <= 5,000 (dense_eig.hpp:114-117)
+MIN_WINDOW_EST = 100.0
+WINDOW_BYTES_PER_PAIR_ROW = 72.0  # 8 B x (m = 4 est basis + est locked + 2 x m/2 candidates)
+
+
+def window_estimate(n: int, mem_bytes: Optional[float], jobs: int, cap: float = 0.0) -> float:
+    """Largest DOS estimate one window may hold: the reference's m-guard limit, and a device
+    footprint of ~72 n est bytes (basis, locked set, Ritz candidates) within 80% of the GPU's
+    memory shared by `jobs` concurrent slices."""
+    if cap > 0.0:  # explicit (Plan.window_est)
+        return cap
+    est = REF_WINDOW_EST
+    if mem_bytes:
+        est = min(est, 0.8 * mem_bytes / (WINDOW_BYTES_PER_PAIR_ROW * n * max(jobs, 1)))
+    return max(est, MIN_WINDOW_EST)
+
+
+def concurrent_jobs(n: int, mem_bytes: Optional[float], nslices: int, requested: int) -> int:
+    """Slices solved at once on one GPU: all of them unless their windows would shrink below
+    ~4x MIN_WINDOW_EST (narrow windows need high filter degrees); then as many as fit."""
+    if requested > 0:
+        return requested
+    if not mem_bytes or nslices <= 1:
+        return max(1, nslices)
+    fit = int(0.8 * mem_bytes // (WINDOW_BYTES_PER_PAIR_ROW * n * 4 * MIN_WINDOW_EST))
+    return max(1, min(nslices, fit))
+
+
+def window_breakpoints(curve: api.DosCurve, lo: float, hi: float, est: float,
+                       max_est: float) -> np.ndarray:
+    """Split [lo, hi] into ceil(est / max_est) windows of equal DOS mass (bisection on
+    dos_count, dos.hpp:212-218; the DOS grid is too coarse for slice_spectrum inside one slice)."""
+    nw = max(1, int(math.ceil(est / max_est))) if est > max_est else 1
+    bp = [lo]
+    if nw > 1:
+        x0, x1 = float(curve.xdos[0]), float(curve.xdos[-1])
+        clo, chi = max(lo, x0), min(hi, x1)
+        total = api.dos_count(curve, clo, chi)
+        for i in range(1, nw):
+            target = total * i / nw
+            a, b = max(bp[-1], clo), chi
+            for _ in range(100):
+                mid = 0.5 * (a + b)
+                if api.dos_count(curve, clo, mid) < target:
+                    a = mid
+                else:
+                    b = mid
+            bp.append(b)
+    bp.append(hi)
+    return np.asarray(bp, np.float64)
+
+
 class GpuBackend:
     """The product path: every stage runs through libsliceeig_cuda.so on this rank's GPU."""
 
@@ -228,6 +311,10 @@ class GpuBackend:
 
     def launches(self) -> int:
         return self.ctx.kernel_launches() + sum(c.kernel_launches() for c in self._thread_ctx.values())
+
+    def memory(self) -> float:
+        """Total device memory in bytes (sizes the memory plan's windows)."""
+        return float(api.device_memory(self.device)[1])
 
     def bounds(self, seed: int):
         b = api.lan_tr_bounds(self.A, 1e-4, 60, 40, seed)
@@ -261,8 +348,15 @@ class GpuBackend:
         return f.k, r
 
 
-def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
-    """Full sliced solve; every rank returns the gathered result (slices in index order)."""
+def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> PipelineResult:
+    """Full sliced solve; every rank returns the gathered result (slices in index order).
+
+    sink(slice_index, window_index, window, eigenvalues, residuals, vectors): optional consumer
+    called on the owning rank as each solve window finishes (seam-trimmed; vectors (n, k) on the
+    host when plan.want_vectors).  With a sink the eigenvectors are streamed to it -- e.g. written
+    out like the CLI's vectors_<i>.bin -- instead of being accumulated, so neither device nor host
+    memory has to hold a whole large slice.  A sink returning True stops that slice after the
+    current window (a bounded partial solve)."""
     dist = dist or Dist()
     t0 = time.perf_counter()
     # bounds: deterministic on every rank; rank 0's copy is broadcast so all ranks agree bitwise
@@ -300,36 +394,74 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None) -> PipelineResult:
     mine_idx = [i for i in range(ns) if owners[i] == dist.rank
                 and (plan.only is None or i in plan.only)]
 
+    mem = backend.memory() if hasattr(backend, "memory") else None
+    jobs = concurrent_jobs(backend.n, mem, len(mine_idx), plan.jobs)
+    max_west = window_estimate(backend.n, mem, min(jobs, max(1, len(mine_idx))), plan.window_est)
+
     def work(i):
         out = SliceOutcome(i, float(bp[i]), float(bp[i + 1]), float(est[i]), rank=dist.rank)
         ts = time.perf_counter()
         out.t_start = ts - t2
         try:
-            k, r = backend.solve_slice(plan, lmin, lmax, out.lo, out.hi, out.est)
-            keep = trim_to_slice(r.eigenvalues, r.residuals, i, ns, out.lo, out.hi, delta)
-            out.degree = k
-            out.eigenvalues = np.asarray(r.eigenvalues)[keep]
-            out.residuals = np.asarray(r.residuals)[keep]
-            if plan.want_vectors and r.vectors is not None:
-                out.vectors = np.asarray(r.vectors)[:, keep]
-            out.niter = r.niter
-            out.n_A_matvec = r.counters.n_A_matvec
-            out.hit_max_its = r.hit_max_its
-            out.t_mv, out.t_orth = r.counters.t_mv, r.counters.t_orth
+            wbp = window_breakpoints(curve, out.lo, out.hi, out.est, max_west)
+            nw = len(wbp) - 1
+            vals, ress, vecs = [], [], []
+            for w in range(nw):
+                tw = time.perf_counter()
+                wlo, whi = float(wbp[w]), float(wbp[w + 1])
+                west = out.est if nw == 1 else api.dos_count(
+                    curve, max(wlo, curve.xdos[0]), min(whi, curve.xdos[-1]))
+                k, r = backend.solve_slice(plan, lmin, lmax, wlo, whi, west)
+                # window seams follow the slice-seam rule (sliceeig_main.cpp:422-442)
+                wk = trim_to_slice(r.eigenvalues, r.residuals, w, nw, wlo, whi, delta)
+                vals.append(np.asarray(r.eigenvalues)[wk])
+                ress.append(np.asarray(r.residuals)[wk])
+                wv = (np.asarray(r.vectors)[:, wk]
+                      if plan.want_vectors and r.vectors is not None else None)
+                if wv is not None and sink is None:
+                    vecs.append(wv)
+                out.degree = max(out.degree, k)
+                out.niter += r.niter
+                out.n_A_matvec += r.counters.n_A_matvec
+                out.hit_max_its = out.hit_max_its or r.hit_max_its
+                out.t_mv += r.counters.t_mv
+                out.t_orth += r.counters.t_orth
+                orth = getattr(r, "orth", None)
+                if orth is not None:
+                    out.orth_passes += orth.passes
+                    out.orth_cols += orth.cols
+                    out.orth_bytes += orth.bytes
+                out.windows.append(Window(wlo, whi, float(west), k, int(wk.size), r.niter,
+                                          time.perf_counter() - tw, r.hit_max_its))
+                del r
+                stop = sink is not None and sink(i, w, out.windows[-1], vals[-1], ress[-1], wv)
+                del wv
+                if stop:  # the sink asked for no more windows of this slice (partial solve)
+                    break
+            allv = np.concatenate(vals) if vals else np.zeros(0)
+            keep = trim_to_slice(allv, None, i, ns, out.lo, out.hi, delta)
+            out.eigenvalues = allv[keep]
+            out.residuals = np.concatenate(ress)[keep] if ress else np.zeros(0)
+            if vecs:
+                out.vectors = (vecs[0] if len(vecs) == 1 else np.concatenate(vecs, axis=1))[:, keep]
         except Exception as e:  # per-slice failure is recorded (sliceeig_main.cpp:506-514)
             out.error = f"{type(e).__name__}: {e}"
         out.seconds = time.perf_counter() - ts
         return out
 
-    jobs = plan.jobs if plan.jobs > 0 else max(1, len(mine_idx))
     if jobs == 1 or len(mine_idx) <= 1:
         local = [work(i) for i in mine_idx]
     else:
         with ThreadPoolExecutor(max_workers=jobs) as ex:
             local = list(ex.map(work, mine_idx))
     t3 = time.perf_counter()
-    gathered = dist.gather_objects(local)
-    slices = sorted([s for part in gathered for s in part], key=lambda s: s.index)
+    # only metadata crosses ranks (values, residuals, counters): eigenvectors stay with the rank
+    # that owns the slice, so a multi-GPU run never ships vector blocks
+    meta = [dataclasses.replace(s, vectors=None) for s in local]
+    gathered = dist.gather_objects(meta)
+    own = {s.index: s for s in local}
+    slices = sorted([own.get(s.index, s) if s.rank == dist.rank else s
+                     for part in gathered for s in part], key=lambda s: s.index)
     t4 = time.perf_counter()
     return PipelineResult(lmin, lmax, bp, est, slices, t1 - t0, t2 - t1, t3 - t2, t4 - t0,
                           backend.launches() if hasattr(backend, "launches") else 0)

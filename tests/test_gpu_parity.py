@@ -469,8 +469,16 @@ def test_pipeline_solvers_match_reference_cli(gpu_ctx, golden, solver):
                 probes="rademacher", tol=1e-8, seed=1234)
     r = run(plan, GpuBackend(dims=[30, 30]))
     assert np.allclose(r.breakpoints, g[f"{solver}_bp"], rtol=1e-12, atol=0)
+    assert [s.index for s in r.slices] == [0, 1, 2, 3]
     for s in r.slices:
         assert s.error is None, s.error
         ref = g[f"{solver}_slice{s.index}_vals"]
+        niter, _nmv, degree, hit = g[f"{solver}_slice{s.index}_meta"]
         assert s.eigenvalues.size == ref.size, (s.index, s.eigenvalues.size, ref.size)
         assert np.all(np.abs(s.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+        assert s.degree == degree
+        # the reference's exit status per slice (si slice 1 also runs out of cycles there)
+        assert s.hit_max_its == bool(hit), (s.index, s.hit_max_its, hit)
+        assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
+        if solver != "si":  # Lanczos iteration counts within one stagnation-check cycle
+            assert abs(s.niter - niter) <= 30, (s.index, s.niter, niter)
