@@ -479,6 +479,7 @@ def test_pipeline_solvers_match_reference_cli(gpu_ctx, golden, solver):
         assert s.degree == degree
         # the reference's exit status per slice (si slice 1 also runs out of cycles there)
         assert s.hit_max_its == bool(hit), (s.index, s.hit_max_its, hit)
-        assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
+        if not s.hit_max_its:  # out of budget, the reference also returns unconverged pairs
+            assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
         if solver != "si":  # Lanczos iteration counts within one stagnation-check cycle
             assert abs(s.niter - niter) <= 30, (s.index, s.niter, niter)
