@@ -580,6 +580,22 @@ inline DosCurve kpm_dos(const Operator& op, const SpectralBounds& bounds, const 
                         c.xdos.data(), c.ydos.data(), &c.nev_est));
   return c;
 }
+// B200 extension: kpm_dos with its probes split over several GPUs of this
+// process and the moments combined by one NCCL all-reduce; bit-identical to kpm_dos.
+inline DosCurve kpm_dos_devices(const CsrMatrix& a, const SpectralBounds& bounds,
+                                const DosConfig& cfg, const std::vector<int>& devices) {
+  DosCurve c;
+  c.n = a.n();
+  c.xdos.resize(std::max(cfg.npts, 0));
+  c.ydos.resize(std::max(cfg.npts, 0));
+  detail::ok(se_kpm_dos_multi((int)devices.size(), devices.data(), a.n(), a.row_ptr().data(),
+                              a.col_idx().data(), a.vals().data(), bounds.lmin, bounds.lmax, cfg.m,
+                              cfg.n_vec, cfg.npts, cfg.seed,
+                              cfg.probes == ProbeKind::Gaussian ? SE_PROBE_GAUSSIAN
+                                                                : SE_PROBE_RADEMACHER,
+                              c.xdos.data(), c.ydos.data(), &c.nev_est));
+  return c;
+}
 inline DosCurve lan_dos(const Operator& op, const SpectralBounds& bounds, const DosConfig& cfg = {}) {
   DosCurve c;
   c.n = op.n;

@@ -199,6 +199,21 @@ SE_API int se_kpm_curve(int m, const double* zeta, int n, double lmin, double lm
 /* kpm_dos (dos.hpp:82-132): moments on the device + curve on the host. */
 SE_API int se_kpm_dos(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec, int npts,
                uint64_t seed, int probe_kind, double* x, double* y, double* nev_est);
+/* kpm_dos (dos.hpp:82-132) over several GPUs of this process (the reference has
+ * one thread: its kpm_dos loop over probes dos.hpp:97-109 is what is split): probes in contiguous
+ * ranges (whole blocks of 16 where possible), one host thread + context + CSR copy per GPU, and
+ * ONE ncclAllReduce (NCCL loaded at run time) of an n_vec x (m+1) per-probe moment array in which
+ * each GPU fills only its own rows -- exact, so the result is bit-identical to se_kpm_dos on one
+ * GPU for any device list.  per_probe: n_vec x (m+1) row-major, unnormalised. */
+SE_API int se_kpm_moments_multi(int ngpu, const int* devices, int n, const int* row_ptr,
+                                const int* col_idx, const double* vals, double lmin, double lmax,
+                                int m, int n_vec, int probe_kind, uint64_t seed, double* per_probe);
+SE_API int se_kpm_dos_multi(int ngpu, const int* devices, int n, const int* row_ptr,
+                            const int* col_idx, const double* vals, double lmin, double lmax, int m,
+                            int n_vec, int npts, uint64_t seed, int probe_kind, double* x, double* y,
+                            double* nev_est);
+/* NCCL version linked at run time (e.g. 22809 for 2.28.9); SE_ECUDA when NCCL is absent. */
+SE_API int se_nccl_version(int* version);
 /* lan_dos (dos.hpp:136-154): device Lanczos per probe + host Ritz-Gaussian quadrature. */
 SE_API int se_lan_dos(se_ctx* ctx, const se_csr* a, double lmin, double lmax, int m, int n_vec, int npts,
                double sigma, uint64_t seed, double* x, double* y, double* nev_est);

@@ -86,6 +86,11 @@ SIGNATURES = {
     "se_kpm_moments_probes": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                               C.c_uint64, C.c_int, C.c_int, _PD],
     "se_probe_block": [C.c_uint64, C.c_int, C.c_int, C.c_long, C.c_int, _PD],
+    "se_kpm_moments_multi": [C.c_int, _PI, C.c_int, _PI, _PI, _PD, C.c_double, C.c_double, C.c_int,
+                             C.c_int, C.c_int, C.c_uint64, _PD],
+    "se_kpm_dos_multi": [C.c_int, _PI, C.c_int, _PI, _PI, _PD, C.c_double, C.c_double, C.c_int,
+                         C.c_int, C.c_int, C.c_uint64, C.c_int, _PD, _PD, _PD],
+    "se_nccl_version": [_PI],
     "se_kpm_curve": [C.c_int, _PD, C.c_int, C.c_double, C.c_double, C.c_int, _PD, _PD, _PD],
     "se_kpm_dos": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
                    _PD, _PD, _PD],

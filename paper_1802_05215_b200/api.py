@@ -491,6 +491,28 @@ def kpm_dos(op, bounds: SpectralBounds, cfg: DosConfig = DosConfig()) -> DosCurv
     return DosCurve(x, y, nev.value, d.n)
 
 
+def kpm_dos_devices(a: "CsrMatrix", bounds: SpectralBounds, cfg: DosConfig,
+                    devices: Sequence[int]) -> DosCurve:
+    """kpm_dos (dos.hpp:82-132) with the probes split over several GPUs of this process and the
+    per-probe moments combined by one NCCL all-reduce (se_kpm_dos_multi); bit-identical to
+    kpm_dos on one GPU."""
+    devs = np.ascontiguousarray(devices, np.int32)
+    x = np.empty(max(cfg.npts, 0), np.float64)
+    y = np.empty(max(cfg.npts, 0), np.float64)
+    nev = C.c_double()
+    call("se_kpm_dos_multi", int(devs.size), _pi(devs), a.n, _pi(a.row_ptr), _pi(a.col_idx),
+         _pd(a.vals), bounds.lmin, bounds.lmax, cfg.m, cfg.n_vec, cfg.npts, cfg.seed,
+         _lib.PROBES[cfg.probes], _pd(x), _pd(y), C.byref(nev))
+    return DosCurve(x, y, nev.value, a.n)
+
+
+def nccl_version() -> int:
+    """The NCCL the library resolves at run time (e.g. 22809), or raises when absent."""
+    v = C.c_int()
+    call("se_nccl_version", C.byref(v))
+    return v.value
+
+
 def lan_dos(op, bounds: SpectralBounds, cfg: DosConfig = DosConfig()) -> DosCurve:
     """dos.hpp:136-154."""
     d = _dev(op)

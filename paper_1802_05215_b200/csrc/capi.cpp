@@ -99,6 +99,10 @@ void check_csr_host(int n, const int* rp, const int* ci) {
 
 }  // namespace
 
+namespace se {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace se
+
 extern "C" {
 
 const char* se_last_error(void) { return g_err.c_str(); }

@@ -130,22 +130,23 @@ class Dist:
             return cls(td.get_rank(), td.get_world_size(), dev)
         return cls()
 
-    def allgather_rows(self, local: np.ndarray, counts: Sequence[int]) -> np.ndarray:
-        """All-gather row blocks (rank r contributes counts[r] rows) in rank order."""
+    def combine_probe_rows(self, local: np.ndarray, first: int, total: int) -> np.ndarray:
+        """The full probe-major (total, width) moment array from every rank's rows
+        [first, first + len(local)): ONE all-reduce (NCCL under the nccl backend) of an array that
+        is zero outside each rank's rows.  Adding exact zeros is exact in any order, so the result
+        is the per-probe matrix bit for bit (one allreduce of the moments)."""
+        width = local.shape[1]
+        full = np.zeros((total, width), np.float64)
+        full[first:first + local.shape[0]] = local
         if self.world == 1:
-            return local
+            return full
         import torch
         import torch.distributed as td
-        width = local.shape[1]
-        mx = max(counts)
-        buf = np.zeros((mx, width), np.float64)
-        buf[: local.shape[0]] = local
-        t = torch.from_numpy(buf)
+        t = torch.from_numpy(full)
         if self.device is not None:
             t = t.to(self.device)
-        outs = [torch.empty_like(t) for _ in range(self.world)]
-        td.all_gather(outs, t)
-        return np.concatenate([o.cpu().numpy()[: counts[r]] for r, o in enumerate(outs)])
+        td.all_reduce(t, op=td.ReduceOp.SUM)
+        return t.cpu().numpy()
 
     def broadcast_f64(self, vals: np.ndarray) -> np.ndarray:
         if self.world == 1:
@@ -366,12 +367,12 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
         lmin, lmax = backend.bounds(plan.seed)
         lmin, lmax = (float(v) for v in dist.broadcast_f64(np.array([lmin, lmax])))
     t1 = time.perf_counter()
-    # KPM: this rank's contiguous probe range, then an all-gather of per-probe moments
-    counts = [probe_split(plan.dos_nvec, dist.world, r)[1] for r in range(dist.world)]
+    # KPM: this rank's contiguous probe range, then one all-reduce of the per-probe moments
     first, count = probe_split(plan.dos_nvec, dist.world, dist.rank)
     mine = backend.moments(lmin, lmax, plan.dos_m, plan.dos_nvec, plan.seed, plan.probes, first,
                            count)
-    allp = dist.allgather_rows(np.asarray(mine, np.float64).reshape(count, plan.dos_m + 1), counts)
+    allp = dist.combine_probe_rows(np.asarray(mine, np.float64).reshape(count, plan.dos_m + 1),
+                                   first, plan.dos_nvec)
     zeta = np.zeros(plan.dos_m + 1)
     for row in allp:  # probe order (dos.hpp:100-106)
         zeta += row

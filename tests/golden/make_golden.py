@@ -202,6 +202,28 @@ def pencil():
     save("pencil", **out)
 
 
+def landos():
+    """lan_dos (dos.hpp:136-154, add_ritz_gaussians :63-75): the reference's Lanczos-quadrature
+    curves on seeded Gaussian probes, plus the slicing the CLI would derive from them."""
+    out = {}
+    cases = [("l20", [20, 20, 20], 40, 12, 1234, 0.0),
+             ("l60", [60, 60], 50, 16, 7, 0.0),
+             ("l60s", [60, 60], 30, 8, 99, 0.05)]   # explicit sigma
+    for tag, dims, m, nvec, seed, sigma in cases:
+        rp, ci, v = reflib.laplacian(dims)
+        lo, hi = reflib.lan_tr_bounds(rp, ci, v, 1e-4, 60, 40, seed)
+        x, y, nev = reflib.lan_dos(rp, ci, v, lo, hi, m=m, n_vec=nvec, npts=300, sigma=sigma, seed=seed)
+        xi, eta = lo + 0.1 * (hi - lo), lo + 0.4 * (hi - lo)
+        bp, est = reflib.slice_spectrum(x, y, len(v) and len(rp) - 1, xi, eta, 4)
+        out[f"{tag}_meta"] = [m, nvec, seed, sigma, lo, hi, nev, xi, eta]
+        out[f"{tag}_dims"] = dims
+        out[f"{tag}_x"] = x
+        out[f"{tag}_y"] = y
+        out[f"{tag}_bp"] = bp
+        out[f"{tag}_est"] = est
+    save("landos", **out)
+
+
 def cli():
     """`sliceeig solve --dims 30,30 --interval 0.4,0.6 --slices 4 [--solver tr]` with the CLI
     defaults (KPM deg 60 x 40 Rademacher probes, sigma damping, tol 1e-8, seed 1234): the
@@ -232,7 +254,7 @@ def cli():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-solve", action="store_true")
-    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli,pencil")
+    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli,pencil,landos")
     a = ap.parse_args()
     only = a.only.split(",")
     if "kats" in only:
@@ -249,3 +271,5 @@ if __name__ == "__main__":
         cli()
     if "pencil" in only:
         pencil()
+    if "landos" in only:
+        landos()

@@ -8,8 +8,9 @@
 //
 // In scope: polynomial filters with the nr / tr / si drivers, KPM or Lanczos densities, standard
 // problems.  Rational filters and B-pencils are reported as errors (nonzero exit), as the
-// reference does for invalid combinations.  B200 extension: --gpus N spreads the
-// slice pool over N GPUs of the node (slice i on GPU i mod N).
+// reference does for invalid combinations.  B200 extension: --gpus N spreads the slice pool over
+// N GPUs of the node (worker thread w on GPU w mod N) and splits the KPM probes over them with one
+// NCCL all-reduce of the moments (kpm_dos_devices).
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -382,53 +383,136 @@ int cmd_filter_dump(const Manifest& m) {
   return 0;
 }
 
-struct Task {
+// ---- solve: the slice pool ---------------------------------------------------------------------
+// One unit of work per DOS slice.  Workers are host threads pinned round-robin to the node's GPUs
+// (one slice context per thread); slices are handed out largest estimate first so a GPU does not
+// finish the run alone on the most expensive slice (reports stay in slice order).
+struct SliceJob {
   int index = 0;
   double lo = 0, hi = 0, est = 0;
 };
-struct Outcome {
+struct SliceRun {
   EigenResults res;
-  std::string error;
-  bool ok = false;
+  std::string error;   // non-empty: the driver threw (the slice is reported as failed)
+  int gpu = 0;
+  double seconds = 0;
+  bool converged() const { return error.empty() && !res.hit_max_its; }
 };
 
-EigenResults run_slice(const CsrMatrix& a, const SpectralBounds& bounds, const Task& t, const Manifest& m) {
-  SolverConfig cfg;
-  cfg.res_tol = m.tol;
-  cfg.seed = m.seed;
-  cfg.est_count = std::max(1, (int)std::lround(std::ceil(t.est)));
-  PolyOpts po;
-  po.damping = damping_of(m.damping);
-  const PolynomialFilter f = find_pol(t.lo, t.hi, bounds, po);
-  if (m.solver == "nr") return cheb_lan_nr(a, nullptr, f, t.lo, t.hi, cfg);
-  if (m.solver == "tr") return cheb_lan_tr(a, nullptr, f, t.lo, t.hi, cfg);
-  return cheb_si(a, nullptr, f, t.lo, t.hi, cfg.est_count, cfg);
-}
-
-// an eigenvalue within delta above an interior breakpoint belongs to the slice below
-// (sliceeig_main.cpp:420-442)
-void trim_to_slice(EigenResults& r, const Task& t, int ns, double delta) {
-  std::vector<int> keep;
-  for (int i = 0; i < (int)r.eigenvalues.size(); ++i) {
-    const double v = r.eigenvalues[i];
-    if (t.index > 0 && v <= t.lo + delta) continue;
-    if (t.index + 1 < ns && v > t.hi + delta) continue;
-    keep.push_back(i);
+// Which eigenvalues a slice reports.  Neighbouring windows overlap by the filter's slack, so a
+// pair near an interior breakpoint b can come back from both sides; it is assigned to the slice
+// whose window (b_i + delta, b_{i+1} + delta] contains it, the outermost windows open-ended
+// (the reference's seam rule, sliceeig_main.cpp:420-442, with delta = 1e-10 (lmax - lmin)).
+struct SeamOwner {
+  int ns = 1;
+  double delta = 0;
+  bool owns(const SliceJob& j, double v) const {
+    const bool above_lo = j.index == 0 || v > j.lo + delta;
+    const bool below_hi = j.index + 1 == ns || v <= j.hi + delta;
+    return above_lo && below_hi;
   }
-  if (keep.size() == r.eigenvalues.size()) return;
+};
+
+// the columns `pick` of a result (eigenvalues, residuals and vectors together)
+EigenResults select_pairs(const EigenResults& r, const std::vector<int>& pick) {
   EigenResults out;
   out.niter = r.niter;
   out.counters = r.counters;
   out.hit_max_its = r.hit_max_its;
   out.vectors = DenseMat(r.vectors.rows(), 0);
-  for (int i : keep) {
-    out.eigenvalues.push_back(r.eigenvalues[i]);
-    out.residuals.push_back(r.residuals[i]);
-    out.vectors.push_col(r.vectors.col_vec(i));
+  out.eigenvalues.reserve(pick.size());
+  out.residuals.reserve(pick.size());
+  for (int c : pick) {
+    out.eigenvalues.push_back(r.eigenvalues[c]);
+    out.residuals.push_back(r.residuals[c]);
+    out.vectors.push_col(r.vectors.col_vec(c));
   }
-  r = std::move(out);
+  return out;
 }
 
+using SliceDriver = EigenResults (*)(const CsrMatrix&, const PolynomialFilter&, const SliceJob&,
+                                     const SolverConfig&);
+SliceDriver driver_for(const std::string& solver) {
+  if (solver == "tr")
+    return [](const CsrMatrix& a, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
+      return cheb_lan_tr(a, nullptr, f, j.lo, j.hi, c);
+    };
+  if (solver == "si")
+    return [](const CsrMatrix& a, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
+      return cheb_si(a, nullptr, f, j.lo, j.hi, c.est_count, c);
+    };
+  return [](const CsrMatrix& a, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
+    return cheb_lan_nr(a, nullptr, f, j.lo, j.hi, c);
+  };
+}
+
+class SlicePool {
+ public:
+  SlicePool(const CsrMatrix& a, const SpectralBounds& b, const Manifest& m, SeamOwner seams)
+      : a_(a), bounds_(b), m_(m), seams_(seams), drive_(driver_for(m.solver)) {}
+
+  std::vector<SliceRun> run(const std::vector<SliceJob>& jobs, int workers) {
+    std::vector<SliceRun> runs(jobs.size());
+    std::vector<int> order(jobs.size());
+    for (std::size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return jobs[x].est > jobs[y].est; });
+    std::atomic<std::size_t> next{0};
+    std::vector<std::thread> threads;
+    for (int w = 0; w < workers; ++w)
+      threads.emplace_back([&, w] {
+        const int gpu = w % std::max(1, m_.gpus);
+        if (m_.gpus > 1) set_thread_device(gpu);
+        for (std::size_t q; (q = next.fetch_add(1)) < order.size();) {
+          const SliceJob& job = jobs[order[q]];
+          SliceRun& out = runs[order[q]];
+          out.gpu = gpu;
+          const auto t0 = std::chrono::steady_clock::now();
+          try {
+            out.res = solve_one(job);
+          } catch (const std::exception& e) {
+            out.error = e.what();
+          }
+          out.seconds = since(t0);
+        }
+      });
+    for (auto& t : threads) t.join();
+    return runs;
+  }
+
+ private:
+  EigenResults solve_one(const SliceJob& job) const {
+    SolverConfig cfg;
+    cfg.res_tol = m_.tol;
+    cfg.seed = m_.seed;
+    cfg.est_count = std::max(1, (int)std::lround(std::ceil(job.est)));
+    PolyOpts po;
+    po.damping = damping_of(m_.damping);
+    const PolynomialFilter f = find_pol(job.lo, job.hi, bounds_, po);
+    EigenResults r = drive_(a_, f, job, cfg);
+    std::vector<int> mine;
+    for (int c = 0; c < (int)r.eigenvalues.size(); ++c)
+      if (seams_.owns(job, r.eigenvalues[c])) mine.push_back(c);
+    return mine.size() == r.eigenvalues.size() ? std::move(r) : select_pairs(r, mine);
+  }
+
+  const CsrMatrix& a_;
+  const SpectralBounds& bounds_;
+  const Manifest& m_;
+  SeamOwner seams_;
+  SliceDriver drive_;
+};
+
+// pool width: the request (at least one thread per GPU), capped by the slice count and by the
+// SLICEEIG_THREADS environment variable of the reference front end
+int pool_width(const Manifest& m, int nslices) {
+  int want = std::max(m.jobs, m.gpus);
+  if (const char* e = std::getenv("SLICEEIG_THREADS"))
+    if (std::atoi(e) >= 1) want = std::min(want, std::atoi(e));
+  return std::max(1, std::min(want, nslices));
+}
+
+// ---- solve: reports -------------------------------------------------------------------------
 Json counters_json(const Counters& c) {
   Json j = Json::object();
   j["n_A_matvec"] = c.n_A_matvec;
@@ -446,115 +530,49 @@ Json times_json(const Counters& c) {
   return j;
 }
 
-int resolve_jobs(int requested, int ntasks) {  // SLICEEIG_THREADS caps the pool
-  int cap = INT_MAX;
-  if (const char* e = std::getenv("SLICEEIG_THREADS")) {
-    const int v = std::atoi(e);
-    if (v >= 1) cap = v;
-  }
-  return std::clamp(requested, 1, std::max(1, std::min(cap, ntasks)));
+// vectors_<i>.bin: the slice's eigenvectors as raw little-endian float64, column-major n x count,
+// described by a sidecar object in slice_<i>.json
+Json write_vector_block(const fs::path& dir, int slice, const DenseMat& v) {
+  const std::string name = "vectors_" + std::to_string(slice) + ".bin";
+  std::ofstream os(dir / name, std::ios::binary);
+  os.write(reinterpret_cast<const char*>(v.data()),
+           (std::streamsize)(sizeof(double) * (std::size_t)v.rows() * v.cols()));
+  if (!os) throw std::runtime_error("cannot write " + (dir / name).string());
+  Json d = Json::object();
+  d["file"] = name;
+  d["n"] = v.rows();
+  d["count"] = v.cols();
+  d["element"] = "float64";
+  d["byte_order"] = "little-endian";
+  d["layout"] = "column-major";
+  return d;
 }
 
-int cmd_solve(const Manifest& m) {
-  const auto t0 = std::chrono::steady_clock::now();
-  m.require_interval();
-  require_poly(m);
-  const double xi = m.interval[0], eta = m.interval[1];
-  const CsrMatrix a = load_problem(m);
-  const double t_load = since(t0);
-  const auto tb = std::chrono::steady_clock::now();
-  const SpectralBounds bounds = estimate_bounds(a, m.seed);
-  const double t_bounds = since(tb);
-  const auto td = std::chrono::steady_clock::now();
-  const DosCurve curve = estimate_dos(a, bounds, m);
-  std::vector<Task> tasks;
-  if (m.slices <= 1) {
-    const Overlap o = clip(curve, xi, eta);
-    tasks.push_back({0, xi, eta, o.empty ? 0.0 : dos_count(curve, o.lo, o.hi)});
-  } else {
-    const SliceSet s = slice_clipped(curve, xi, eta, m.slices);
-    for (int i = 0; i < s.ns(); ++i) tasks.push_back({i, s.breakpoints[i], s.breakpoints[i + 1], s.est_counts[i]});
+Json slice_report(const SliceJob& job, const SliceRun& run, const fs::path& dir, bool vectors) {
+  Json sj = Json::object();
+  sj["schema"] = 1;
+  sj["slice"] = job.index;
+  sj["lo"] = job.lo;
+  sj["hi"] = job.hi;
+  sj["est_count"] = job.est;
+  if (!run.error.empty()) {
+    sj["error"] = run.error;
+    sj["converged"] = false;
+    return sj;
   }
-  const double t_dos = since(td);
-  const fs::path dir = out_dir(m);
-  write_text(dir / "dos_curve.csv", curve_csv(curve));
+  const EigenResults& r = run.res;
+  sj["found"] = (long)r.eigenvalues.size();
+  sj["eigenvalues"] = Json(r.eigenvalues);
+  sj["residuals"] = Json(r.residuals);
+  sj["niter"] = r.niter;
+  sj["converged"] = !r.hit_max_its;
+  sj["counters"] = counters_json(r.counters);
+  sj["times"] = times_json(r.counters);
+  if (vectors) sj["vectors"] = write_vector_block(dir, job.index, r.vectors);
+  return sj;
+}
 
-  const int ns = (int)tasks.size();
-  const double delta = 1e-10 * (bounds.lmax - bounds.lmin);
-  const int jobs = resolve_jobs(std::max(m.jobs, m.gpus), ns);
-  std::vector<Outcome> outcomes(ns);
-  std::atomic<int> cursor{0};
-  const auto ts = std::chrono::steady_clock::now();
-  auto worker = [&](int w) {
-    if (m.gpus > 1) set_thread_device(w % m.gpus);
-    for (int i; (i = cursor.fetch_add(1)) < ns;) {
-      try {
-        EigenResults r = run_slice(a, bounds, tasks[i], m);
-        trim_to_slice(r, tasks[i], ns, delta);
-        outcomes[i].res = std::move(r);
-        outcomes[i].ok = !outcomes[i].res.hit_max_its;
-      } catch (const std::exception& e) {
-        outcomes[i].error = e.what();
-        outcomes[i].ok = false;
-      }
-    }
-  };
-  std::vector<std::thread> pool;
-  for (int w = 0; w < jobs; ++w) pool.emplace_back(worker, w);
-  for (auto& t : pool) t.join();
-  const double t_solve = since(ts);
-
-  Json slices = Json::array();
-  Counters total;
-  long found = 0, niter = 0;
-  bool all_ok = true;
-  for (int i = 0; i < ns; ++i) {
-    const Outcome& oc = outcomes[i];
-    Json sj = Json::object();
-    sj["schema"] = 1;
-    sj["slice"] = i;
-    sj["lo"] = tasks[i].lo;
-    sj["hi"] = tasks[i].hi;
-    sj["est_count"] = tasks[i].est;
-    if (!oc.error.empty()) {
-      sj["error"] = oc.error;
-      sj["converged"] = false;
-    } else {
-      const EigenResults& r = oc.res;
-      sj["found"] = (long)r.eigenvalues.size();
-      sj["eigenvalues"] = Json(r.eigenvalues);
-      sj["residuals"] = Json(r.residuals);
-      sj["niter"] = r.niter;
-      sj["converged"] = !r.hit_max_its;
-      sj["counters"] = counters_json(r.counters);
-      sj["times"] = times_json(r.counters);
-      if (m.write_vectors) {
-        const std::string bin = "vectors_" + std::to_string(i) + ".bin";
-        std::ofstream os(dir / bin, std::ios::binary);
-        os.write(reinterpret_cast<const char*>(r.vectors.data()),
-                 (std::streamsize)((std::size_t)r.vectors.rows() * r.vectors.cols() * sizeof(double)));
-        if (!os) throw std::runtime_error("cannot write " + (dir / bin).string());
-        Json v = Json::object();
-        v["file"] = bin;
-        v["n"] = r.vectors.rows();
-        v["count"] = r.vectors.cols();
-        v["element"] = "float64";
-        v["byte_order"] = "little-endian";
-        v["layout"] = "column-major";
-        sj["vectors"] = v;
-      }
-      found += (long)r.eigenvalues.size();
-      niter += r.niter;
-      total += r.counters;
-    }
-    all_ok = all_ok && oc.ok;
-    write_text(dir / ("slice_" + std::to_string(i) + ".json"), sj.dump(2) + "\n");
-    slices.push_back(sj);
-  }
-
-  Json rep = Json::object();
-  rep["schema"] = 1;
-  rep["command"] = "solve";
+Json solve_config_json(const Manifest& m, int workers) {
   Json cfg = Json::object();
   cfg["input"] = m.input_json();
   cfg["interval"] = Json(m.interval);
@@ -568,9 +586,88 @@ int cmd_solve(const Manifest& m) {
   cfg["tol"] = m.tol;
   cfg["seed"] = m.seed;
   cfg["jobs_requested"] = m.jobs;
-  cfg["jobs"] = jobs;
+  cfg["jobs"] = workers;
   cfg["gpus"] = m.gpus;
-  rep["config"] = cfg;
+  return cfg;
+}
+
+std::string pairs_csv(const std::vector<SliceRun>& runs) {
+  std::ostringstream os;
+  os.precision(17);
+  os << "slice,index,eigenvalue,residual\n";
+  for (std::size_t i = 0; i < runs.size(); ++i) {
+    if (!runs[i].error.empty()) continue;
+    const EigenResults& r = runs[i].res;
+    for (std::size_t k = 0; k < r.eigenvalues.size(); ++k)
+      os << i << "," << k << "," << r.eigenvalues[k] << "," << r.residuals[k] << "\n";
+  }
+  return os.str();
+}
+
+// The density for solve: with --gpus N > 1 and KPM the probes are split over the GPUs and the
+// moments combined by one NCCL all-reduce (bit-identical to the single-GPU curve).
+DosCurve solve_dos(const CsrMatrix& a, const SpectralBounds& b, const Manifest& m) {
+  if (m.gpus <= 1 || m.method != "kpm") return estimate_dos(a, b, m);
+  DosConfig cfg;
+  cfg.m = m.dos_deg;
+  cfg.n_vec = m.dos_vecs;
+  cfg.npts = m.dos_npts;
+  cfg.seed = m.seed;
+  std::vector<int> devices(m.gpus);
+  for (int g = 0; g < m.gpus; ++g) devices[g] = g;
+  return kpm_dos_devices(a, b, cfg, devices);
+}
+
+int cmd_solve(const Manifest& m) {
+  const auto t0 = std::chrono::steady_clock::now();
+  m.require_interval();
+  require_poly(m);
+  const double xi = m.interval[0], eta = m.interval[1];
+  const CsrMatrix a = load_problem(m);
+  const double t_load = since(t0);
+  auto tb = std::chrono::steady_clock::now();
+  const SpectralBounds bounds = estimate_bounds(a, m.seed);
+  const double t_bounds = since(tb);
+  tb = std::chrono::steady_clock::now();
+  const DosCurve curve = solve_dos(a, bounds, m);
+  std::vector<SliceJob> jobs;
+  if (m.slices > 1) {
+    const SliceSet s = slice_clipped(curve, xi, eta, m.slices);
+    for (int i = 0; i < s.ns(); ++i) jobs.push_back({i, s.breakpoints[i], s.breakpoints[i + 1], s.est_counts[i]});
+  } else {
+    const Overlap o = clip(curve, xi, eta);
+    jobs.push_back({0, xi, eta, o.empty ? 0.0 : dos_count(curve, o.lo, o.hi)});
+  }
+  const double t_dos = since(tb);
+  const fs::path dir = out_dir(m);
+  write_text(dir / "dos_curve.csv", curve_csv(curve));
+
+  const int ns = (int)jobs.size();
+  const int workers = pool_width(m, ns);
+  tb = std::chrono::steady_clock::now();
+  SlicePool pool(a, bounds, m, SeamOwner{ns, 1e-10 * (bounds.lmax - bounds.lmin)});
+  const std::vector<SliceRun> runs = pool.run(jobs, workers);
+  const double t_solve = since(tb);
+
+  Json slices = Json::array();
+  Counters total;
+  long found = 0, niter = 0;
+  bool all_ok = true;
+  for (int i = 0; i < ns; ++i) {
+    const Json sj = slice_report(jobs[i], runs[i], dir, m.write_vectors);
+    write_text(dir / ("slice_" + std::to_string(i) + ".json"), sj.dump(2) + "\n");
+    slices.push_back(sj);
+    all_ok = all_ok && runs[i].converged();
+    if (runs[i].error.empty()) {
+      found += (long)runs[i].res.eigenvalues.size();
+      niter += runs[i].res.niter;
+      total += runs[i].res.counters;
+    }
+  }
+  Json rep = Json::object();
+  rep["schema"] = 1;
+  rep["command"] = "solve";
+  rep["config"] = solve_config_json(m, workers);
   Json bj = Json::object();
   bj["lmin"] = bounds.lmin;
   bj["lmax"] = bounds.lmax;
@@ -595,20 +692,10 @@ int cmd_solve(const Manifest& m) {
   tj["t_total"] = since(t0);
   rep["timings"] = tj;
   write_text(dir / "report.json", rep.dump(2) + "\n");
-  if (m.format == "csv") {
-    std::ostringstream os;
-    os.precision(17);
-    os << "slice,index,eigenvalue,residual\n";
-    for (int i = 0; i < ns; ++i) {
-      if (!outcomes[i].error.empty()) continue;
-      const EigenResults& r = outcomes[i].res;
-      for (std::size_t k = 0; k < r.eigenvalues.size(); ++k)
-        os << i << "," << k << "," << r.eigenvalues[k] << "," << r.residuals[k] << "\n";
-    }
-    std::cout << os.str();
-  } else {
+  if (m.format == "csv")
+    std::cout << pairs_csv(runs);
+  else
     emit(rep);
-  }
   return all_ok ? 0 : 1;
 }
 
