@@ -159,8 +159,9 @@ SE_API int se_filter_bench(se_ctx* ctx, const se_csr* a, const se_poly_filter* f
  * ||t||) against an n x k basis, graph-captured and replayed `reps` times between CUDA events.
  * Algorithmic bytes per pass: 16 n k + 24 n. */
 SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
-/* A full CGS2 step with the re-pass forced: mode 0 = two unfused passes (4 reads of W),
- * mode 1 = the fused path T1 + cgs_mid + N2 (3 reads). */
+/* A full CGS2 step with the re-pass forced: mode 0 = two column-major passes (4 reads of W),
+ * mode 2 = the product path on the row-major basis, T1 + fused MID + N2 (3 reads); mode -1 =
+ * one column-major pass. */
 SE_API int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms);
 
 /* Production timing of kdeg degrees of the multi-vector filter (nv <= 8 recurrences sharing one

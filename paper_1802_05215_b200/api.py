@@ -491,11 +491,22 @@ def kpm_dos(op, bounds: SpectralBounds, cfg: DosConfig = DosConfig()) -> DosCurv
     return DosCurve(x, y, nev.value, d.n)
 
 
+def _one_nccl_per_process():
+    """The library resolves NCCL at run time and reuses a copy already in the process.  torch
+    links its own NCCL under the same soname, so import torch (when present) first: its copy is
+    then the one both use, instead of a system copy shadowing it for a later torch import."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def kpm_dos_devices(a: "CsrMatrix", bounds: SpectralBounds, cfg: DosConfig,
                     devices: Sequence[int]) -> DosCurve:
     """kpm_dos (dos.hpp:82-132) with the probes split over several GPUs of this process and the
     per-probe moments combined by one NCCL all-reduce (se_kpm_dos_multi); bit-identical to
     kpm_dos on one GPU."""
+    _one_nccl_per_process()
     devs = np.ascontiguousarray(devices, np.int32)
     x = np.empty(max(cfg.npts, 0), np.float64)
     y = np.empty(max(cfg.npts, 0), np.float64)
@@ -508,6 +519,7 @@ def kpm_dos_devices(a: "CsrMatrix", bounds: SpectralBounds, cfg: DosConfig,
 
 def nccl_version() -> int:
     """The NCCL the library resolves at run time (e.g. 22809), or raises when absent."""
+    _one_nccl_per_process()
     v = C.c_int()
     call("se_nccl_version", C.byref(v))
     return v.value

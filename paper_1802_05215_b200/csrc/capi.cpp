@@ -478,7 +478,6 @@ int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int re
 
 int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms) {
   return guard([&] {
-    if (mode == 1 && !k::cgs_mid_supported(n, k)) fail(SE_EINVAL, "se_cgs2_bench: k too large for the fused path");
     cgs2_bench(C(ctx), n, k, reps, mode, *ms);
   });
 }
@@ -563,7 +562,7 @@ constexpr int kBlock = 16;
 void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, int n_vec,
                       int probe_kind, std::uint64_t seed, int first, int count, Vec& zeta,
                       Vec* per_probe = nullptr) {
-  static const bool doubling = std::getenv("SE_KPM_DIRECT") == nullptr;
+  constexpr bool doubling = true;  // Chebyshev doubling: floor(m/2) block SpMMs instead of m - 1
   if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
   if (m < 1 || n_vec < 1) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
   if (a.n < 1) fail(SE_EINVAL, "dos: empty operator");
@@ -605,14 +604,10 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
     else
       fill_rademacher_bits(rng, n, std::min(kBlock, count - b0), reinterpret_cast<std::uint64_t*>(buf));
   };
-  static const bool trace = std::getenv("SE_KPM_TRACE") != nullptr;
-  const auto t_start = std::chrono::steady_clock::now();
-  auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(); };
   std::future<void> next = std::async(std::launch::async, fill, 0, hb[0]);
   try {
     for (int b0 = 0, q = 0; b0 < count; b0 += kBlock, ++q) {
       const int b = std::min(kBlock, count - b0);
-      if (trace) std::fprintf(stderr, "[kpm] block %d wait-fill at %.1f ms\n", q, since());
       // odd blocks carry one zero probe column (its moments are dropped): every row of the
       // row-major block is then 16-byte aligned for the kernels' paired loads
       const int bk = b + (b & 1);
@@ -627,9 +622,7 @@ void kpm_moments_impl(Ctx& c, const DevCsr& a, double lmin, double lmax, int m, 
         SE_CUDA(cudaMemcpyAsync(X[2], hbuf, sizeof(std::uint64_t) * words * b, cudaMemcpyHostToDevice, c.stream));
         k::expand_rademacher(c, reinterpret_cast<const std::uint64_t*>(X[2]), V, n, b, bk);
       }
-      if (trace) std::fprintf(stderr, "[kpm] block %d filled at %.1f ms\n", q, since());
       ctx_sync(c);  // hbuf consumed; the other buffer is free
-      if (trace) std::fprintf(stderr, "[kpm] block %d staged at %.1f ms\n", q, since());
       if (b0 + kBlock < count) next = std::async(std::launch::async, fill, b0 + kBlock, hb[(q + 1) & 1]);
       if (c.time_filter) SE_CUDA(cudaEventRecord(c.ev0, c.stream));
       k::kpm_step(c, s, a, bk, 1, V, V, nullptr, X[0], cc, d, dz, 0);
@@ -839,53 +832,45 @@ int se_lanczos_run(se_ctx* ctx, const se_csr* a, const double* start, int m, dou
 }
 
 int se_paired_cgs2(se_ctx* ctx, int n, int kq, const double* W, double* t, double* h) {
+  // The product's CGS2 (rowgs.cu): W staged row-major, T1 + fused MID + N2.
   return guard([&] {
     Ctx& c = C(ctx);
     if (n < 1 || kq < 0) fail(SE_EINVAL, "paired_cgs2: bad sizes");
-    double* dW = dev_alloc<double>((size_t)n * std::max(kq, 1));
+    // orth.hpp:72-73: nothing to do for a zero vector or an empty basis
+    double t2 = 0.0;
+    for (int r = 0; r < n; ++r) t2 += t[r] * t[r];
+    if (kq == 0 || t2 == 0.0) return;
+    const int ldw = k::rw_ldw(kq);
+    k::RowScratch rs = k::rw_scratch(c, ldw);
+    double* dW = dev_alloc<double>((size_t)n * ldw);
+    double* dcm = dev_alloc<double>((size_t)n * kq);
     double* dt = dev_alloc<double>(n);
-    double* coef = dev_alloc<double>(std::max(kq, 1));
-    double* hd = dev_alloc<double>(std::max(kq, 1));
+    double* cf = dev_alloc<double>(2 * (size_t)ldw);
+    double* rbuf = dev_alloc<double>(k::rw_scratch_doubles(rs));
     Ctl* ctl = dev_alloc<Ctl>(1);
-    k::Scratch s;
-    s.cap = k::cgs_scratch_doubles(c, n, kq);
-    s.ncnt = k::cgs_counter_slots(n, kq);
-    s.buf = dev_alloc<double>(s.cap);
-    s.cnt = dev_alloc<unsigned>(s.ncnt);
+    k::rw_bind(rs, rbuf);
     auto cleanup = [&] {
-      for (void* p : {(void*)dW, (void*)dt, (void*)coef, (void*)hd, (void*)ctl, (void*)s.buf, (void*)s.cnt})
-        dev_free(p);
+      for (void* p : {(void*)dW, (void*)dcm, (void*)dt, (void*)cf, (void*)rbuf, (void*)ctl}) dev_free(p);
     };
     try {
-      SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
-      SE_CUDA(cudaMemsetAsync(hd, 0, sizeof(double) * std::max(kq, 1), c.stream));
-      if (kq) SE_CUDA(cudaMemcpyAsync(dW, W, sizeof(double) * (size_t)n * kq, cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaMemcpyAsync(dcm, W, sizeof(double) * (size_t)n * kq, cudaMemcpyHostToDevice, c.stream));
       SE_CUDA(cudaMemcpyAsync(dt, t, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      k::rw_put_cols(c, n, dW, ldw, 0, kq, dcm, n, nullptr);
       Ctl z{};
       z.i = kq - 1;  // columns 0..i
       SE_CUDA(cudaMemcpyAsync(ctl, &z, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
-      k::norm_before(c, s, n, dt, ctl);
-      Ctl h0;
-      SE_CUDA(cudaMemcpyAsync(&h0, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
-      ctx_sync(c);
-      // orth.hpp:72-73: nothing to do for a zero vector or an empty basis
-      if (h0.before != 0.0 && kq > 0) {
-        // h accumulates every coefficient: run passes with hdiag bookkeeping per column
-        for (int pass = 0; pass < 2; ++pass) {
-          k::cgs_pass(c, s, n, dt, dW, false, pass == 1, ctl, nullptr, coef, kq);
-          if (h) {
-            Vec cf(kq);
-            Ctl hh;
-            SE_CUDA(cudaMemcpyAsync(&hh, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
-            SE_CUDA(cudaMemcpyAsync(cf.data(), coef, sizeof(double) * kq, cudaMemcpyDeviceToHost, c.stream));
-            ctx_sync(c);
-            if (pass == 0 || hh.npass == 2)
-              for (int j = 0; j < kq; ++j) h[j] += cf[j];
-          }
-        }
-      }
+      k::rw_cgs2(c, rs, n, dt, dW, ldw, ctl, nullptr, cf, cf + ldw, true);
+      Vec co(2 * (size_t)ldw);
+      Ctl hh;
+      SE_CUDA(cudaMemcpyAsync(&hh, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+      SE_CUDA(cudaMemcpyAsync(co.data(), cf, sizeof(double) * co.size(), cudaMemcpyDeviceToHost, c.stream));
       SE_CUDA(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
       ctx_sync(c);
+      if (h)
+        for (int q = 0; q < kq; ++q) {
+          h[q] += co[q];                       // pass 1 (orth.hpp:30)
+          if (hh.npass == 2) h[q] += co[ldw + q];  // the DGKS re-pass (orth.hpp:77-78)
+        }
     } catch (...) {
       cleanup();
       throw;

@@ -148,19 +148,6 @@ Ctx* ctx_create(int device) {
   SE_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
   c->prio_hi = greatest;
   c->prio_lo = least;
-  if (std::getenv("SE_L2_PERSIST") && prop.persistingL2CacheMaxSize > 0) {
-    // opt-in: set aside L2 for the filter's matrix stream (the concurrent slices'
-    // reorthogonalisation passes stream gigabytes through L2).  Measured neutral-to-slightly-
-    // negative on cfg2 (the GEMV loads already stream with evict-first), so off by default.
-    size_t cur = 0;
-    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    const size_t want = (size_t)prop.persistingL2CacheMaxSize;
-    if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    c->l2_persist = cur;
-    c->l2_window_max = (size_t)prop.accessPolicyMaxWindowSize;
-    cudaGetLastError();
-  }
   SE_CUDA(cudaStreamCreateWithPriority(&c->bulk, cudaStreamNonBlocking, least));
   SE_CUDA(cudaStreamCreateWithPriority(&c->hstream, cudaStreamNonBlocking, greatest));
   c->stream = c->bulk;
@@ -179,9 +166,7 @@ Ctx* ctx_create(int device) {
   cublasSetStream(c->blas, c->hstream);
   if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(SE_ECUDA, "cusolverDnCreate failed");
   cusolverDnSetStream(c->solver, c->hstream);
-  SE_CUDA(cudaEventCreateWithFlags(&c->evsync, std::getenv("SE_SPIN_SYNC")
-                                                   ? cudaEventDisableTiming
-                                                   : (cudaEventBlockingSync | cudaEventDisableTiming)));
+  SE_CUDA(cudaEventCreateWithFlags(&c->evsync, cudaEventBlockingSync | cudaEventDisableTiming));
   SE_CUDA(cudaEventCreateWithFlags(&c->evx, cudaEventDisableTiming));
   SE_CUDA(cudaEventCreate(&c->evk0));
   SE_CUDA(cudaEventCreate(&c->evk1));

@@ -16,8 +16,6 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   int prio_hi = 0, prio_lo = 0;  // stream/kernel priority range of the device
-  size_t l2_persist = 0;         // persisting-L2 set-aside granted (bytes; 0: disabled)
-  size_t l2_window_max = 0;      // largest access-policy window
   cudaStream_t stream = nullptr;   // current launch stream (bulk Lanczos work: low priority)
   cudaStream_t bulk = nullptr;     // the low-priority stream
   cudaStream_t hstream = nullptr;  // high priority: latency-bound host-driven phases

@@ -20,34 +20,64 @@ double now_s() {
 
 int grow(int want) { return std::max(want, 16) + std::max(want, 16) / 2; }
 
+// ---- the Krylov basis: row-major (rowgs.cu) ----------------------------------------------------
+// W[r * ld + j], ld = rw_ldw(cap): each row of the active basis is one contiguous run, which is
+// what lets the CGS2 step stage row blocks by TMA bulk copies and read W three times per step.
+struct RowBasis {
+  int n = 0;
+  int cap = 0;  // columns
+  int ld = 0;
+  double* p = nullptr;
+};
+
+void rowbasis_reserve(Ctx& c, RowBasis& w, int n, int cols, bool keep) {
+  if (w.p && w.n == n && w.cap >= cols) return;
+  const int ld = k::rw_ldw(cols);
+  double* p = dev_alloc<double>((size_t)n * ld);
+  if (keep && w.p && w.cap > 0)  // re-stride the kept rows
+    SE_CUDA(cudaMemcpy2DAsync(p, sizeof(double) * ld, w.p, sizeof(double) * w.ld,
+                              sizeof(double) * w.ld, n, cudaMemcpyDeviceToDevice, c.stream));
+  if (w.p) {
+    ctx_sync(c);
+    dev_free(w.p);
+  }
+  w.p = p;
+  w.n = n;
+  w.cap = cols;
+  w.ld = ld;
+}
+
 // ---- one device recurrence (basis W, locked set L, step graph) ------------------------------
 struct Krylov {
   Ctx& c;
   const DevCsr& A;
   const StepOp& op;
   int n;
-  DevMat W, L;
+  RowBasis W;
+  DevMat L;
   double* t = nullptr;
+  double* vsrc = nullptr;  // the step's source column W[:, i], contiguous (filter input)
   double* fb[3] = {nullptr, nullptr, nullptr};
   Ctl* ctl = nullptr;
-  double *alpha = nullptr, *beta = nullptr, *hdiag = nullptr, *coef = nullptr, *coef_l = nullptr;
+  double *alpha = nullptr, *beta = nullptr, *hdiag = nullptr, *coef = nullptr, *coef2 = nullptr,
+         *coef_l = nullptr;
   double* dscal = nullptr;  // device scalars for host-side dots
   int arr_cap = 0, coefl_cap = 0;
   k::Scratch s;
+  k::RowScratch rs;
+  double* rbuf = nullptr;
+  int* idx = nullptr;  // column indices for thick-restart copies
+  int idx_cap = 0;
   cudaGraphExec_t gexec = nullptr;
   int gnodes = 0;
   int gmode = -1;
   int nlock = 0;
 
   double* mu_dev = nullptr;
-  // fused CGS2 middle (cgs_mid.cu): second coefficient vector + its own scratch and counter
-  double* coef2 = nullptr;
-  double* mid_scratch = nullptr;
-  unsigned* mid_cnt = nullptr;
-  int mid_cap = 0;
 
   Krylov(Ctx& cc, const DevCsr& a, const StepOp& o) : c(cc), A(a), op(o), n(a.n) {
     t = dev_alloc<double>(n);
+    vsrc = dev_alloc<double>(n);
     if (!op.plain) {
       for (double*& b : fb) b = dev_alloc<double>(n);
       mu_dev = dev_alloc<double>(op.k + 1);
@@ -61,15 +91,13 @@ struct Krylov {
   ~Krylov() {
     cudaStreamSynchronize(c.stream);
     if (gexec) cudaGraphExecDestroy(gexec);
-    devmat_free(W);
+    dev_free(W.p);
     devmat_free(L);
     dev_free(mu_dev);
-    dev_free(coef2);
-    dev_free(mid_scratch);
-    dev_free(mid_cnt);
-    for (void* p : {(void*)t, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl, (void*)alpha,
-                    (void*)beta, (void*)hdiag, (void*)coef, (void*)coef_l, (void*)dscal,
-                    (void*)s.buf, (void*)s.cnt})
+    for (void* p : {(void*)t, (void*)vsrc, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl,
+                    (void*)alpha, (void*)beta, (void*)hdiag, (void*)coef, (void*)coef2,
+                    (void*)coef_l, (void*)dscal, (void*)s.buf, (void*)s.cnt, (void*)rbuf,
+                    (void*)idx})
       dev_free(p);
   }
 
@@ -87,18 +115,18 @@ struct Krylov {
   void ensure(int wcols, int lcols) {
     bool dirty = false;
     if (wcols > W.cap) {
-      devmat_reserve(c, W, n, grow(wcols), true);
+      rowbasis_reserve(c, W, n, grow(wcols), true);
       dirty = true;
     }
     if (lcols > L.cap) {
       devmat_reserve(c, L, n, grow(lcols), true);
       dirty = true;
     }
-    if (W.cap > arr_cap) {
+    if (W.ld > arr_cap) {
       ctx_sync(c);
       auto regrow = [&](double*& p) {
-        double* q = dev_alloc<double>(W.cap);
-        SE_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * W.cap, c.stream));
+        double* q = dev_alloc<double>(W.ld);
+        SE_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * W.ld, c.stream));
         if (p) SE_CUDA(cudaMemcpyAsync(q, p, sizeof(double) * arr_cap, cudaMemcpyDeviceToDevice, c.stream));
         ctx_sync(c);
         dev_free(p);
@@ -108,7 +136,13 @@ struct Krylov {
       regrow(beta);
       regrow(hdiag);
       regrow(coef);
-      arr_cap = W.cap;
+      regrow(coef2);
+      arr_cap = W.ld;
+      // streaming grid and partials of the row-major CGS2 for this capacity
+      rs = k::rw_scratch(c, W.ld);
+      dev_free(rbuf);
+      rbuf = dev_alloc<double>(k::rw_scratch_doubles(rs));
+      k::rw_bind(rs, rbuf);
       dirty = true;
     }
     if (std::max(L.cap, 1) > coefl_cap) {
@@ -117,7 +151,7 @@ struct Krylov {
       coef_l = dev_alloc<double>(coefl_cap);
       dirty = true;
     }
-    const int wide = std::max(W.cap, L.cap);
+    const int wide = std::max(L.cap, 1);
     const size_t need = k::cgs_scratch_doubles(c, n, wide);
     const int slots = k::cgs_counter_slots(n, wide);
     if (need > s.cap || slots > s.ncnt) {
@@ -131,28 +165,7 @@ struct Krylov {
       SE_CUDA(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * s.ncnt, c.stream));
       dirty = true;
     }
-    if (W.cap > mid_cap && k::cgs_mid_supported(n, W.cap) && std::getenv("SE_CGS_FUSED")) {
-      SE_CUDA(cudaStreamSynchronize(c.stream));
-      dev_free(coef2);
-      dev_free(mid_scratch);
-      if (!mid_cnt) {
-        mid_cnt = dev_alloc<unsigned>(1);
-        SE_CUDA(cudaMemsetAsync(mid_cnt, 0, sizeof(unsigned), c.stream));
-      }
-      coef2 = dev_alloc<double>(W.cap);
-      mid_scratch = dev_alloc<double>(k::cgs_mid_scratch_doubles(c, W.cap));
-      mid_cap = W.cap;
-      dirty = true;
-    }
     if (dirty) drop_graph();
-  }
-
-  bool fused() const {
-    // Opt-in (SE_CGS_FUSED=1): the fused middle saves one of four reads of W per step but stages
-    // narrow (R x 8-byte) column segments, and the per-SM request rate caps it below the two
-    // full-width unfused passes at basis widths above a few hundred ("CGS2 fusion").
-    static const bool want = std::getenv("SE_CGS_FUSED") != nullptr;
-    return want && mid_cap >= W.cap && k::cgs_mid_supported(n, W.cap);
   }
 
   Ctl get() {
@@ -173,33 +186,47 @@ struct Krylov {
     put(h);
   }
 
+  // Basis column access for the host-driven phases (start vectors, restarts, downloads).
+  void put_col(int col, const double* dev_src) { k::rw_put_cols(c, n, W.p, W.ld, col, 1, dev_src, n, nullptr); }
+  void get_col(int col, double* dev_dst) { k::rw_get_cols(c, n, W.p, W.ld, col, 1, dev_dst); }
+  // W[:, q] = U[:, cols[q]] for q < cols.size() (U column-major, ld n)
+  void put_cols(const std::vector<int>& cols, const double* U) {
+    if (cols.empty()) return;
+    if ((int)cols.size() > idx_cap) {
+      ctx_sync(c);
+      dev_free(idx);
+      idx_cap = grow((int)cols.size());
+      idx = dev_alloc<int>(idx_cap);
+    }
+    h2d(c, idx, cols.data(), sizeof(int) * cols.size());
+    k::rw_put_cols(c, n, W.p, W.ld, 0, (int)cols.size(), U, n, idx);
+  }
+
   // Filter W[:, ctl->i] into t (apply_pol filter_poly.hpp:256-277, or one op application).
   void record_filter() {
+    k::rw_col_get(c, n, W.p, W.ld, ctl, 0, vsrc);
     k::ChebArgs a;
-    a.src_ctl = ctl;
-    a.src_ld = n;
     a.halt = ctl;
     if (op.plain) {
-      a.x = W.p;
+      a.x = vsrc;
       a.y = t;
       k::spmv_cheb(c, A, k::kPlain, a);
       return;
     }
     a.c = op.c;
     a.invd = op.invd;
-    a.x = W.p;
+    a.x = vsrc;
     a.y = fb[0];
     a.out = t;
     a.mu0 = op.mu[0];
     a.muj = op.mu[1];
     k::spmv_cheb(c, A, k::kFirst, a);
-    // buffers: prev (j-2), cur (j-1), next; W[:, i] plays prev for j = 2
+    // buffers: prev (j-2), cur (j-1), next; the source column plays prev for j = 2
     int cur = 0, prv = -1, nxt = 1;
     for (int j = 2; j <= op.k; ++j) {
       k::ChebArgs b = a;
       b.x = fb[cur];
-      b.prev = prv < 0 ? W.p : fb[prv];
-      b.src_ctl = prv < 0 ? ctl : nullptr;
+      b.prev = prv < 0 ? vsrc : fb[prv];
       b.y = fb[nxt];
       b.muj = op.mu[j];
       k::spmv_cheb(c, A, k::kNext, b);
@@ -218,21 +245,12 @@ struct Krylov {
     k::stamp(c, ctl, 1);
     if (L.cap > 0) k::cgs_pass(c, s, n, t, L.p, true, false, ctl, nullptr, coef_l, L.cap);
     if (mode == 0) {
-      k::nr_beta_alpha(c, s, n, t, W.p, ctl, alpha, beta);
-      k::nr_sub_alpha(c, s, n, t, W.p, ctl);
-    } else {
-      k::norm_before(c, s, n, t, ctl);
+      k::rw_nr_beta_alpha(c, s, n, t, W.p, W.ld, ctl, alpha, beta);
+      k::rw_nr_sub_alpha(c, s, n, t, W.p, W.ld, ctl);
     }
-    double* h = mode == 1 ? hdiag : nullptr;
-    if (fused()) {  // CGS2 with three reads of W: T1, fused N1 + norm + T2, N2
-      k::gemvt_only(c, s, n, t, W.p, false, ctl, h, coef, W.cap);
-      k::cgs_mid(c, n, t, W.p, ctl, coef, coef2, h, W.cap, mid_scratch, mid_cnt);
-      k::gemvn_only(c, s, n, t, W.p, true, ctl, coef2, W.cap);
-    } else {
-      k::cgs_pass(c, s, n, t, W.p, false, false, ctl, h, coef, W.cap);
-      k::cgs_pass(c, s, n, t, W.p, false, true, ctl, h, coef, W.cap);
-    }
-    k::normalize_next(c, s, n, t, W.p, ctl, beta);
+    // CGS2 against W[:, 0..i] with three reads of W (TR: the T1 pass also takes ||t||)
+    k::rw_cgs2(c, rs, n, t, W.p, W.ld, ctl, mode == 1 ? hdiag : nullptr, coef, coef2, mode == 1);
+    k::rw_normalize(c, s.cnt, n, t, W.p, W.ld, ctl, beta);
     k::stamp(c, ctl, 2);
   }
 
@@ -353,9 +371,10 @@ struct CandBuf {
     devmat_free(AU);
     dev_free(stats);
   }
-  // U = W[:, :steps] Y (Y steps x nc, ld ldy), AU = A U, stats per column.
+  // U = W[:, :steps] Y (Y steps x nc, ld ldy), AU = A U, stats per column.  W is column-major
+  // (ld n) when w_row_ld == 0, else the row-major Krylov basis with row stride w_row_ld.
   void eval(const DevCsr& A, const double* W, int steps, const double* Y, int ldy, int nc,
-            Vec& out3) {
+            Vec& out3, int w_row_ld = 0) {
     HiPrio hp(c);
     const int n = A.n;
     // geometric growth: every reallocation is a cudaFree, which waits for the whole device
@@ -368,8 +387,13 @@ struct CandBuf {
       stats = dev_alloc<double>(3 * (size_t)stats_cap);
     }
     const double one = 1.0, zero = 0.0;
-    if (cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, nc, steps, &one, W, n, Y, ldy, &zero, U.p,
-                    n) != CUBLAS_STATUS_SUCCESS)
+    // row-major W is the column-major (steps x n, ld w_row_ld) matrix W^T: U = (W^T)^T Y
+    const cublasStatus_t st =
+        w_row_ld ? cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, n, nc, steps, &one, W, w_row_ld, Y,
+                               ldy, &zero, U.p, n)
+                 : cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, nc, steps, &one, W, n, Y, ldy,
+                               &zero, U.p, n);
+    if (st != CUBLAS_STATUS_SUCCESS)
       fail(SE_ECUDA, "cublasDgemm (Ritz combinations) failed");
     ++c.launches;
     for (int j0 = 0; j0 < nc; j0 += 65535) {
@@ -458,12 +482,13 @@ struct Slice {
     Vec w(n);
     for (int attempt = 0; attempt < 16; ++attempt) {
       rng.normal_fill(w.data(), n);
-      double* d = kr.W.col(col);
+      double* d = kr.t;  // staged contiguous, then stored into the row-major basis
       h2d(c, d, w.data(), sizeof(double) * n);
       if (kr.nlock > 0) k::project_out(c, kr.s, n, kr.nlock, kr.L.p, d, kr.coef_l);
       const double nb = std::sqrt(kr.dot(d, d));
       if (nb > 1e-14) {
         k::scale(c, n, 1.0 / nb, d);
+        kr.put_col(col, d);
         return;
       }
     }
@@ -535,7 +560,7 @@ struct Slice {
                    "passes %lld cols %lld (%.1f GB/s over t_orth) check_kernel_ms %.1f wcap %d fused %d frees %ld chk %.2f/%.2f/%.2f\n",
                    A.n, its, cnt.t_total, cnt.t_mv, cnt.t_orth, prof[0], prof[1], prof[2],
                    kr.get().passes_total, kr.get().cols_total,
-                   16.0 * A.n * (double)kr.get().cols_total / std::max(1e-9, cnt.t_orth) / 1e9, c.prof_kernel_ms, kr.W.cap, (int)kr.fused(), dev_frees().load(),
+                   16.0 * A.n * (double)kr.get().cols_total / std::max(1e-9, cnt.t_orth) / 1e9, c.prof_kernel_ms, kr.W.cap, 0, dev_frees().load(),
                    c.prof_chk[0], c.prof_chk[1], c.prof_chk[2]);
     r->niter = its;
     r->hit_max_its = warn;
@@ -623,7 +648,7 @@ std::unique_ptr<SliceResult> run_nr(Slice& s) {
         const int ncand = m - j0;
         Vec st;
         tq = now_s();
-        if (ncand > 0) s.cand.eval(s.A, kr.W.p, m, Y + (size_t)j0 * m, m, ncand, st);
+        if (ncand > 0) s.cand.eval(s.A, kr.W.p, m, Y + (size_t)j0 * m, m, ncand, st, kr.W.ld);
         s.prof[2] += now_s() - tq;
         s.cnt.n_A_matvec += ncand;
         std::vector<int> accepted;
@@ -735,7 +760,7 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
     const int ncand = steps - j0;
     Vec st;
     tq = now_s();
-    if (ncand > 0) s.cand.eval(s.A, kr.W.p, steps, Y + (size_t)j0 * steps, steps, ncand, st);
+    if (ncand > 0) s.cand.eval(s.A, kr.W.p, steps, Y + (size_t)j0 * steps, steps, ncand, st, kr.W.ld);
     s.prof[2] += now_s() - tq;
     s.cnt.n_A_matvec += ncand;
     const Vec ylast = s.last_row(Y, steps, j0, ncand);
@@ -769,15 +794,15 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
     tr_s.clear();
     if (!broke) {
       const int lnew = (int)trset.size();
-      if (lnew != steps)
-        SE_CUDA(cudaMemcpyAsync(kr.W.col(lnew), kr.W.col(steps), sizeof(double) * n,
-                                cudaMemcpyDeviceToDevice, s.c.stream));
+      // the last Lanczos vector moves to column lnew, the kept Ritz vectors fill 0..lnew-1
+      k::rw_col_move(s.c, n, kr.W.p, kr.W.ld, steps, lnew);
+      std::vector<int> cols;
       for (int q = 0; q < lnew; ++q) {
         tr_theta.push_back(trset[q].theta);
         tr_s.push_back(trailing * trset[q].ylast);
-        SE_CUDA(cudaMemcpyAsync(kr.W.col(q), s.cand.U.col(trset[q].col), sizeof(double) * n,
-                                cudaMemcpyDeviceToDevice, s.c.stream));
+        cols.push_back(trset[q].col);
       }
+      kr.put_cols(cols, s.cand.U.p);
     }
   }
   s.cnt.n_A_matvec += (long)s.op.k * its;
@@ -861,10 +886,11 @@ LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m,
   StepOp op;  // plain A
   Krylov kr(c, a, op);
   kr.ensure(m + 1, 0);
-  h2d(c, kr.W.col(0), start_host, sizeof(double) * n);
-  const double nb2 = kr.dot(kr.W.col(0), kr.W.col(0));
+  h2d(c, kr.t, start_host, sizeof(double) * n);
+  const double nb2 = kr.dot(kr.t, kr.t);
   if (nb2 <= 0.0) fail(SE_ENUMERIC, "lanczos_run: B-inner product is not positive");
-  k::scale(c, n, 1.0 / std::sqrt(nb2), kr.W.col(0));
+  k::scale(c, n, 1.0 / std::sqrt(nb2), kr.t);
+  kr.put_col(0, kr.t);
   kr.begin(0);
   kr.run(0, m);
   const Ctl h = kr.get();
@@ -880,9 +906,15 @@ LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m,
   } else {
     r.beta.assign(be.begin(), be.begin() + (r.steps - 1));
     r.next_beta = be[r.steps - 1];
-    kr.download(kr.W.col(r.steps), n, r.next_w);
+    kr.get_col(r.steps, kr.t);
+    kr.download(kr.t, n, r.next_w);
   }
-  if (want_basis) kr.download(kr.W.p, (int)((size_t)n * r.steps), r.basis);
+  if (want_basis) {
+    double* cm = dev_alloc<double>((size_t)n * std::max(r.steps, 1));
+    k::rw_get_cols(c, n, kr.W.p, kr.W.ld, 0, r.steps, cm);
+    kr.download(cm, (int)((size_t)n * r.steps), r.basis);
+    dev_free(cm);
+  }
   return r;
 }
 
@@ -907,9 +939,10 @@ void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max
       if (k0 == 0) {
         Vec w(n);
         rng.normal_fill(w.data(), n);
-        h2d(c, kr.W.col(0), w.data(), sizeof(double) * n);
-        const double nb = std::sqrt(kr.dot(kr.W.col(0), kr.W.col(0)));
-        k::scale(c, n, 1.0 / nb, kr.W.col(0));
+        h2d(c, kr.t, w.data(), sizeof(double) * n);
+        const double nb = std::sqrt(kr.dot(kr.t, kr.t));
+        k::scale(c, n, 1.0 / nb, kr.t);
+        kr.put_col(0, kr.t);
       }
       SE_CUDA(cudaMemsetAsync(kr.hdiag, 0, sizeof(double) * kr.arr_cap, c.stream));
       kr.begin(k0);
@@ -952,12 +985,10 @@ void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max
       h2d(c, dY, vecs.data(), sizeof(double) * steps);
       h2d(c, dY + steps, vecs.data() + (size_t)(steps - 1) * steps, sizeof(double) * steps);
       Vec st;
-      cand.eval(a, kr.W.p, steps, dY, steps, 2, st);
+      cand.eval(a, kr.W.p, steps, dY, steps, 2, st, kr.W.ld);
       // seed first (column steps -> 2), then the kept combinations into columns 0, 1
-      SE_CUDA(cudaMemcpyAsync(kr.W.col(2), kr.W.col(steps), sizeof(double) * n,
-                              cudaMemcpyDeviceToDevice, c.stream));
-      SE_CUDA(cudaMemcpyAsync(kr.W.col(0), cand.U.col(0), sizeof(double) * 2 * n,
-                              cudaMemcpyDeviceToDevice, c.stream));
+      k::rw_col_move(c, n, kr.W.p, kr.W.ld, steps, 2);
+      kr.put_cols({0, 1}, cand.U.p);
     }
   } catch (...) {
     dev_free(dY);
@@ -1307,8 +1338,9 @@ namespace se {
 // runs inside the Lanczos step graph (production path), replayed `reps` times between events.
 void cgs_bench(Ctx& c, int n, int kcols, int reps, double& ms) { cgs2_bench(c, n, kcols, reps, -1, ms); }
 
-// mode -1: one unfused pass; 0: a CGS2 step as two unfused passes; 1: the fused CGS2 step
-// (T1 + cgs_mid + N2).  The re-pass is forced (before = 1e300) so both paths do full work.
+// mode -1: one column-major pass (k_gemvt + k_gemvn, the locked-set / cheb_si path); 0: a CGS2
+// step as two column-major passes (4 reads of W); 2: the product's CGS2 step on the row-major
+// basis (T1 + fused MID + N2, 3 reads).  The re-pass is forced (before = 1e300).
 void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
   if (n < 1 || kcols < 1 || reps < 1) fail(SE_EINVAL, "se_cgs_bench: bad sizes");
   double* W = dev_alloc<double>((size_t)n * kcols);
@@ -1321,13 +1353,23 @@ void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
   s.ncnt = k::cgs_counter_slots(n, kcols);
   s.buf = dev_alloc<double>(s.cap);
   s.cnt = dev_alloc<unsigned>(s.ncnt);
-  double* mid = mode == 1 ? dev_alloc<double>(k::cgs_mid_scratch_doubles(c, kcols)) : nullptr;
+  // mode 2: row-major basis, three-read CGS2 (rowgs.cu)
+  const int ldw = k::rw_ldw(kcols);
+  k::RowScratch rs;
+  double* rbuf = nullptr;
+  if (mode == 2) {
+    rs = k::rw_scratch(c, ldw);
+    rbuf = dev_alloc<double>(k::rw_scratch_doubles(rs));
+    k::rw_bind(rs, rbuf);
+    dev_free(W);
+    W = dev_alloc<double>((size_t)n * ldw);
+  }
   unsigned* mcnt = dev_alloc<unsigned>(1);
   cudaGraphExec_t ge = nullptr;
   auto cleanup = [&] {
     if (ge) cudaGraphExecDestroy(ge);
     for (void* p : {(void*)W, (void*)t, (void*)coef, (void*)coef2, (void*)ctl, (void*)s.buf, (void*)s.cnt,
-                    (void*)mid, (void*)mcnt})
+                    (void*)mcnt, (void*)rbuf})
       dev_free(p);
   };
   try {
@@ -1337,8 +1379,19 @@ void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
     std::vector<double> h((size_t)n);
     Rng rng(7);
     rng.normal_fill(h.data(), n);
-    for (int j = 0; j < kcols; ++j)
-      h2d(c, W + (size_t)j * n, h.data(), sizeof(double) * n);
+    if (mode == 2) {
+      std::vector<double> row((size_t)ldw);
+      for (int j = 0; j < ldw; ++j) row[j] = h[j % n];
+      for (int r = 0; r < n; r += 4096) {
+        const int cnt = std::min(4096, n - r);
+        std::vector<double> blk((size_t)cnt * ldw);
+        for (int q = 0; q < cnt; ++q) std::copy(row.begin(), row.end(), blk.begin() + (size_t)q * ldw);
+        h2d(c, W + (size_t)r * ldw, blk.data(), sizeof(double) * blk.size());
+      }
+    } else {
+      for (int j = 0; j < kcols; ++j)
+        h2d(c, W + (size_t)j * n, h.data(), sizeof(double) * n);
+    }
     h2d(c, t, h.data(), sizeof(double) * n);
     Ctl z{};
     z.i = kcols - 1;
@@ -1354,10 +1407,10 @@ void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
     } else if (mode == 0) {
       k::cgs_pass(c, s, n, t, W, false, false, ctl, nullptr, coef, kcols);
       k::cgs_pass(c, s, n, t, W, false, true, ctl, nullptr, coef, kcols);
+    } else if (mode == 2) {
+      k::rw_cgs2(c, rs, n, t, W, ldw, ctl, nullptr, coef, coef2, false);
     } else {
-      k::gemvt_only(c, s, n, t, W, false, ctl, nullptr, coef, kcols);
-      k::cgs_mid(c, n, t, W, ctl, coef, coef2, nullptr, kcols, mid, mcnt);
-      k::gemvn_only(c, s, n, t, W, true, ctl, coef2, kcols);
+      fail(SE_EINVAL, "se_cgs2_bench: mode is -1, 0 or 2");
     }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));

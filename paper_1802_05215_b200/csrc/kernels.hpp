@@ -122,14 +122,43 @@ void gemvt_only(Ctx& c, const Scratch& s, int n, const double* t, const double* 
                 Ctl* ctl, double* hdiag, double* coef, int cap);
 void gemvn_only(Ctx& c, const Scratch& s, int n, double* t, const double* Q, bool pass2, Ctl* ctl,
                 const double* coef, int cap);
-// Fused middle of CGS2 (cgs_mid.cu): t1 = t - Q coef1, ||t1||, DGKS flag, coef2 = Q^T t1 with one
-// read of Q.  Needs an even n, a basis narrow enough for two-row blocks in shared memory
-// (cgs_mid_supported) and its own scratch (cgs_mid_scratch_doubles).
-constexpr int kMaxFusedCols = 3200;
-size_t cgs_mid_scratch_doubles(const Ctx& c, int cap_cols);
-bool cgs_mid_supported(int n, int cap_cols);
-void cgs_mid(Ctx& c, int n, double* t, const double* Q, Ctl* ctl, const double* coef1,
-             double* coef2, double* hdiag, int cap, double* scratch, unsigned* cnt);
+// ---- row-major Krylov basis (rowgs.cu) --------------------------------------------------------
+// The Lanczos basis W is row-major, W[r * ldw + j] with ldw = rw_ldw(capacity) (even, so every row
+// is a 16-byte aligned run a TMA bulk copy can stage).  One CGS2 step = T1 (coef1 = W^T t), MID
+// (t1 = t - W coef1, ||t1||, DGKS flag, coef2 = W^T t1 from the same staged rows) and N2 (t -= W
+// coef2, only when re-passed): three reads of W instead of four.
+constexpr size_t kRwMaxSmem = 227 * 1024;   // dynamic shared memory per CTA (sm_100a limit)
+constexpr size_t kRwSmemPerSm = 228 * 1024;
+struct RowScratch {
+  double* part = nullptr;   // grid x ldw per-CTA coefficient partials
+  double* npart = nullptr;  // grid per-CTA sums of squares
+  int grid = 0;             // persistent streaming CTAs
+  int ldw = 0;
+};
+int rw_ldw(int cols);
+RowScratch rw_scratch(const Ctx& c, int ldw);          // grid sizing for a basis capacity
+size_t rw_scratch_doubles(const RowScratch& s);
+void rw_bind(RowScratch& s, double* buf);              // buf: rw_scratch_doubles(s) doubles
+// CGS2 of t against W[:, 0..ctl->i] (orth.hpp:63-80): coef1/coef2 (>= ldw doubles) receive the
+// two passes' coefficients, hdiag[i] += c (TR, eigensolvers.hpp:534) when non-null; want_before:
+// the T1 pass also sets before = after = ||t|| and resets the DGKS flags (TR's step).
+void rw_cgs2(Ctx& c, const RowScratch& s, int n, double* t, const double* W, int ldw, Ctl* ctl,
+             double* hdiag, double* coef1, double* coef2, bool want_before);
+// dst = W[:, ctl->i + off] (contiguous copy of the step's source column)
+void rw_col_get(Ctx& c, int n, const double* W, int ldw, const Ctl* ctl, int off, double* dst);
+// beta = after; breakdown -> halted; else W[:, i+1] = t / beta, beta_arr[i] = beta, i++.
+void rw_normalize(Ctx& c, unsigned* cnt, int n, const double* t, double* W, int ldw, Ctl* ctl,
+                  double* beta_arr);
+void rw_nr_beta_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, int ldw,
+                      Ctl* ctl, double* alpha_arr, const double* beta_arr);
+void rw_nr_sub_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, int ldw, Ctl* ctl);
+// W[:, col0 + q] = U[:, idx[q]] (idx null: U[:, q]), U column-major with leading dimension ldu
+void rw_put_cols(Ctx& c, int n, double* W, int ldw, int col0, int cnt, const double* U, long ldu,
+                 const int* idx_dev);
+// dst (column-major, ld n) = W[:, col0 .. col0 + cnt)
+void rw_get_cols(Ctx& c, int n, const double* W, int ldw, int col0, int cnt, double* dst);
+void rw_col_move(Ctx& c, int n, double* W, int ldw, int from, int to);
+
 // t -= Q (Q^T t) with a host-side column count (project_x, eigensolvers.hpp:223-227).
 void project_out(Ctx& c, const Scratch& s, int n, int kq, const double* Q, double* t,
                  double* coef);

@@ -405,19 +405,11 @@ __global__ void k_stamp(Ctl* ctl, int which) {
   }
 }
 
-int rch_for(int n) {
-  static const int force = [] {
-    const char* e = std::getenv("SE_RCH");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (force > 0) return std::min(force, kMaxRch);
-  return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512);
-}
+int rch_for(int n) { return n >= (1 << 20) ? 4096 : (n >= (1 << 16) ? 2048 : 512); }
 
 // programmatic-dependent launch of a step kernel (the kernel starts with griddepcontrol.wait)
 template <class K, class... Args>
 void launch_pdl(const Ctx& c, K kern, dim3 grid, dim3 block, size_t smem, Args... args) {
-  static const bool pdl = std::getenv("SE_NO_GEMV_PDL") == nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -427,13 +419,12 @@ void launch_pdl(const Ctx& c, K kern, dim3 grid, dim3 block, size_t smem, Args..
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   SE_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
-// launch attributes of the GEMV kernels: programmatic dependent launch (SE_NO_GEMV_PDL=1: off)
+// launch attributes of the GEMV kernels: programmatic dependent launch
 cudaLaunchConfig_t gemv_cfg(const Ctx& c, dim3 grid, size_t smem, cudaLaunchAttribute* attr) {
-  static const bool pdl = std::getenv("SE_NO_GEMV_PDL") == nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -442,19 +433,12 @@ cudaLaunchConfig_t gemv_cfg(const Ctx& c, dim3 grid, size_t smem, cudaLaunchAttr
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   return cfg;
 }
 
-// columns per GEMV-N chunk (<= kNW)
-int nw_for() {
-  static const int nw = [] {
-    const char* e = std::getenv("SE_NW");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? std::min(v, kNW) : kNW;
-  }();
-  return nw;
-}
+// columns per GEMV-N chunk
+int nw_for() { return kNW; }
 
 }  // namespace
 

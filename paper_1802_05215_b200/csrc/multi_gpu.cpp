@@ -8,12 +8,14 @@
 // the rows in probe order (dos.hpp:100-106), so the curve equals se_kpm_dos on one GPU exactly,
 // for any GPU count.
 //
-// NCCL is resolved at run time (dlopen of libnccl.so.2): a Python process that already loaded
-// torch's NCCL shares that copy, and the library has no link-time NCCL dependency.
+// NCCL is resolved at run time (dlopen of libnccl.so.2, preferring a copy already loaded in the
+// process): a Python process shares torch's NCCL, and the library has no link-time NCCL
+// dependency.
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -40,9 +42,14 @@ const Nccl& nccl() {
   static Nccl api;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = nullptr;
+    // An NCCL already in the process (e.g. the one torch links) wins: a second copy under the
+    // same soname would shadow it for libraries loaded later.  SLICEEIG_NCCL names a specific
+    // library; else the loader's libnccl.so.2.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h)
+      if (const char* path = std::getenv("SLICEEIG_NCCL")) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
     for (const char* name : {"libnccl.so.2", "libnccl.so"})
-      if ((h = dlopen(name, RTLD_NOW | RTLD_GLOBAL))) break;
+      if (!h) h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       api.load_error = std::string("NCCL not found: ") + dlerror();
       return;

@@ -1,0 +1,578 @@
+// Row-major Krylov basis and the three-read CGS2 step (K4 of SURVEY.md §2.1; reference
+// orth.hpp:19-80 cgs_pass / paired_cgs2, eigensolvers.hpp:406-433 / 524-556 for the step).
+//
+// Layout: the Lanczos basis W is stored ROW-major, W[r * ldw + j] (ldw = column capacity, even),
+// so one row of the active basis (columns 0..i) is a single contiguous run of 8 (i+1) bytes.
+// That makes every row block of W one TMA bulk copy (cp.async.bulk, 1-D) straight into shared
+// memory, and lets the middle of CGS2 use each staged row block twice:
+//
+//   T1  : coef1 = W^T t                    (and ||t|| for the TR step)          one read of W
+//   MID : t1 = t - W coef1, ||t1||, coef2 = W^T t1   (same staged rows)         one read of W
+//   N2  : t2 = t1 - W coef2, ||t2||        (only when the DGKS test asks, orth.hpp:76-78)
+//
+// i.e. three reads of W per re-passed CGS2 step instead of four, and two when no re-pass is
+// needed (coef2 is then simply discarded).  Each streaming kernel is persistent (a fixed grid,
+// row blocks dealt round-robin), stages R rows per block through an S-deep ring of bulk copies,
+// and gives every thread a fixed set of columns (j = tid + 256 q) whose coefficient and partial
+// sums live in registers.  All reductions have a fixed order (thread columns -> warp xor tree ->
+// warps in order; CTA partials in CTA order), so reruns are bitwise identical.
+//
+// The basis is written one column at a time (k_rw_normalize: W[:, i+1] = t / beta) and read one
+// column at a time by the filter (k_rw_col_get): strided 8-byte accesses, ~4 n sectors per step,
+// negligible next to the 8 n (i+1) bytes of each pass.
+#include <atomic>
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace se {
+namespace k {
+
+namespace {
+
+constexpr double kEta = 0.70710678118654752;  // DGKS threshold, orth.hpp:13
+constexpr int kRT = 256;                      // threads per streaming CTA
+constexpr int kRW = kRT / 32;
+constexpr int kRR = 2;                        // rows per staged block
+constexpr int kRS = 2;                        // ring stages
+constexpr int kFinCols = 32;                  // columns per finishing CTA (8 threads each)
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_arm(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred done;\n RW_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra RW_WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// one contiguous global run -> shared memory, completion counted on `bar` (TMA bulk copy)
+__device__ __forceinline__ void row_copy(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+enum RwPhase { kT = 0, kMid = 1, kN = 2 };
+
+// The streaming pass.  PH = kT: part[g][j] = sum over this CTA's rows of W[r, j] t[r];
+// npart[g] = sum t[r]^2.  PH = kMid: t[r] -= W[r, :] coef (written back), npart = sum t1^2,
+// part = W^T t1 partials.  PH = kN (only when ctl->repass): t[r] -= W[r, :] coef, npart.
+template <int PH, int QMAX>
+__global__ void __launch_bounds__(kRT) k_rw_stream(int n, const double* __restrict__ W, int ldw,
+                                                   double* __restrict__ t, const Ctl* ctl,
+                                                   const double* __restrict__ coef,
+                                                   double* __restrict__ part,
+                                                   double* __restrict__ npart) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  if (PH == kN && !ctl->repass) return;
+  const int ncols = ctl->i + 1;
+  const int nblk = (n + kRR - 1) / kRR;
+  const unsigned row_bytes = (unsigned)(((ncols + 1) & ~1) * (int)sizeof(double));
+  extern __shared__ __align__(128) double ring[];  // [kRS][kRR][ldw]
+  __shared__ __align__(8) unsigned long long full[kRS];
+  __shared__ double s_red[kRW][kRR];
+  __shared__ double s_x[kRR];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  double cr[QMAX], acc[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int j = tid + kRT * q;
+    cr[q] = (PH != kT && j < ncols) ? coef[j] : 0.0;
+    acc[q] = 0.0;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kRS; ++s) bar_init(&full[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int s, int b) {  // thread 0: stage row block b into ring stage s
+    const int r0 = b * kRR, rows = min(kRR, n - r0);
+    bar_arm(&full[s], rows * row_bytes);
+    for (int r = 0; r < rows; ++r)
+      row_copy(ring + ((size_t)s * kRR + r) * ldw, W + (size_t)(r0 + r) * ldw, row_bytes, &full[s]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < kRS; ++s) {
+      const int b = blockIdx.x + s * gridDim.x;
+      if (b < nblk) issue(s, b);
+    }
+  double nrm = 0.0;  // thread 0: this CTA's sum of squares, in block order
+  int it = 0;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
+    const int s = it % kRS;
+    const int r0 = b * kRR, rows = min(kRR, n - r0);
+    bar_wait(&full[s], (unsigned)((it / kRS) & 1));
+    const double* st = ring + (size_t)s * kRR * ldw;
+    double x[kRR];
+    if (PH == kT) {
+#pragma unroll
+      for (int r = 0; r < kRR; ++r) x[r] = r < rows ? t[r0 + r] : 0.0;
+    } else {
+      // row dots W[r, :] coef over this thread's columns, then the block tree
+      double p[kRR];
+#pragma unroll
+      for (int r = 0; r < kRR; ++r) p[r] = 0.0;
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        const int j = tid + kRT * q;
+        if (j < ncols) {
+#pragma unroll
+          for (int r = 0; r < kRR; ++r) p[r] = add(p[r], mul(st[r * ldw + j], cr[q]));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kRR; ++r) p[r] = warp_sum(p[r]);
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < kRR; ++r) s_red[warp][r] = p[r];
+      __syncthreads();
+      if (tid < rows) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kRW; ++w) sum = add(sum, s_red[w][tid]);
+        const double xr = sub(t[r0 + tid], sum);
+        t[r0 + tid] = xr;
+        s_x[tid] = xr;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kRR; ++r) x[r] = r < rows ? s_x[r] : 0.0;
+    }
+    if (tid == 0)
+      for (int r = 0; r < rows; ++r) nrm = add(nrm, mul(x[r], x[r]));
+    if (PH != kN) {
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        const int j = tid + kRT * q;
+        if (j < ncols) {
+#pragma unroll
+          for (int r = 0; r < kRR; ++r)
+            if (r < rows) acc[q] = add(acc[q], mul(st[r * ldw + j], x[r]));
+        }
+      }
+    }
+    __syncthreads();  // stage s fully consumed (and s_x / s_red free)
+    if (tid == 0) {
+      const int nb = b + kRS * gridDim.x;
+      if (nb < nblk) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(s, nb);
+      }
+    }
+  }
+  if (PH != kN) {
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      const int j = tid + kRT * q;
+      if (j < ncols) part[(size_t)blockIdx.x * ldw + j] = acc[q];
+    }
+  }
+  if (tid == 0) npart[blockIdx.x] = nrm;
+}
+
+// sum of the G per-CTA squares, identical in every CTA (fixed thread assignment + tree)
+__device__ double grid_norm2(const double* npart, int G) {
+  __shared__ double s_w[kRW];
+  __shared__ double s_tot;
+  double v = 0.0;
+  for (int g = threadIdx.x; g < G; g += kRT) v = add(v, __ldcg(npart + g));
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double q = 0.0;
+    for (int w = 0; w < kRW; ++w) q = add(q, s_w[w]);
+    s_tot = q;
+  }
+  __syncthreads();
+  return s_tot;
+}
+
+// Finish a pass: coefficients (8 threads per column over the CTA partials, fixed order), the
+// norm, the DGKS bookkeeping (orth.hpp:72-78) and TR's H(i,i) += h[i] (eigensolvers.hpp:534).
+//   kT  : coef = sum part; hdiag[i] += coef[i]; want_before: before = after = ||t||, flags reset
+//   kMid: after = ||t1||; repass = !(after > eta before); coef = sum part (coef2);
+//         hdiag[i] += coef2[i] when the re-pass runs; pass statistics
+//   kN  : (grid 1, only when re-passed) before = after = ||t2||; pass statistics
+template <int PH>
+__global__ void __launch_bounds__(kRT) k_rw_finish(int G, int ldw, const double* part,
+                                                   const double* npart, Ctl* ctl, double* coef,
+                                                   double* hdiag, int want_before) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  if (PH == kN && !ctl->repass) return;
+  const int ncols = ctl->i + 1, icol = ctl->i;
+  const double nrm = sqrt(grid_norm2(npart, G));
+  if (PH == kN) {
+    if (threadIdx.x == 0) {
+      ctl->before = nrm;
+      ctl->after = nrm;
+      ctl->npass += 1;
+      ctl->passes_total += 1;
+      ctl->cols_total += ncols;
+    }
+    return;
+  }
+  // every CTA reads ctl->before, which only CTA 0 of the T finish writes (before the MID kernel)
+  const bool repass = PH == kMid ? !(nrm > kEta * ctl->before) : false;
+  const int jj = threadIdx.x >> 3, sub8 = threadIdx.x & 7;
+  const int j = blockIdx.x * kFinCols + jj;
+  double q = 0.0;
+  if (j < ncols)
+    for (int g = sub8; g < G; g += 8) q = add(q, __ldcg(part + (size_t)g * ldw + j));
+  for (int o = 4; o > 0; o >>= 1) q = add(q, __shfl_down_sync(0xffffffffu, q, o, 8));
+  if (sub8 == 0 && j < ncols) {
+    coef[j] = q;
+    if (hdiag && j == icol && (PH == kT || repass)) hdiag[j] = add(hdiag[j], q);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (PH == kT) {
+      if (want_before) {
+        ctl->before = nrm;
+        ctl->after = nrm;
+        ctl->repass = 0;
+        ctl->npass = 0;
+      }
+    } else {
+      ctl->after = nrm;  // `before` stays the pre-pass norm (other CTAs of this grid read it)
+      ctl->repass = repass ? 1 : 0;
+      ctl->npass += 1;
+      ctl->passes_total += 1;
+      ctl->cols_total += ncols;
+    }
+  }
+}
+
+// dst = W[:, ctl->i + off] (the filter's source column, contiguous)
+__global__ void k_rw_col_get(int n, const double* __restrict__ W, int ldw, const Ctl* ctl, int off,
+                             double* __restrict__ dst) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  const int col = ctl->i + off;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    dst[r] = W[(size_t)r * ldw + col];
+}
+
+// beta = after; breakdown (beta <= 1e-14, orth.hpp:14) halts the recurrence; otherwise
+// W[:, i+1] = t * (1/beta) (eigensolvers.hpp:431), beta_arr[i] = beta, i += 1.
+__global__ void k_rw_normalize(int n, const double* __restrict__ t, double* __restrict__ W, int ldw,
+                               Ctl* ctl, double* beta_arr, unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  const double beta = ctl->after;
+  const int i = ctl->i;
+  const bool brk = beta <= 1e-14;
+  if (!brk) {
+    const double inv = 1.0 / beta;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+      W[(size_t)r * ldw + i + 1] = mul(t[r], inv);
+  }
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    beta_arr[i] = beta;
+    if (brk)
+      ctl->halted = 1;
+    else
+      ctl->i = i + 1;
+    *cnt = 0u;
+  }
+}
+
+// Block sum, valid in thread 0 (deterministic tree).
+__device__ double block_sum0(double v) {
+  __shared__ double s_w[32];
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = add(r, s_w[w]);
+  return r;
+}
+
+// last-CTA reduction of per-CTA sums in CTA order (valid in thread 0 of the last CTA)
+__device__ bool grid_total(double mine, double* partial, unsigned* counter, double* total) {
+  __shared__ bool s_last;
+  const double bs = block_sum0(mine);
+  if (threadIdx.x == 0) partial[blockIdx.x] = bs;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double q = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) q = add(q, __ldcg(partial + b));
+  q = block_sum0(q);
+  if (threadIdx.x == 0) {
+    *total = q;
+    *counter = 0u;
+  }
+  return true;
+}
+
+// NR (eigensolvers.hpp:408-409): t -= beta W[:, i-1] (beta != 0), alpha = t . W[:, i]
+__global__ void __launch_bounds__(kRT) k_rw_nr_beta_alpha(int n, double* __restrict__ t,
+                                                          const double* __restrict__ W, int ldw,
+                                                          Ctl* ctl, double* alpha_arr,
+                                                          const double* beta_arr, double* partial,
+                                                          unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  const int i = ctl->i;
+  const double beta = i > 0 ? beta_arr[i - 1] : 0.0;
+  const int ip = i > 0 ? i - 1 : 0;
+  double s = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const double* row = W + (size_t)r * ldw;
+    double tr = t[r];
+    if (beta != 0.0) {
+      tr = add(tr, mul(-beta, row[ip]));
+      t[r] = tr;
+    }
+    s = add(s, mul(tr, row[i]));
+  }
+  double tot;
+  if (grid_total(s, partial, cnt, &tot) && threadIdx.x == 0) {
+    ctl->alpha = tot;
+    alpha_arr[i] = tot;
+  }
+}
+
+// NR (eigensolvers.hpp:410): t -= alpha W[:, i]; before = ||t|| for CGS2 (orth.hpp:72)
+__global__ void __launch_bounds__(kRT) k_rw_nr_sub_alpha(int n, double* __restrict__ t,
+                                                         const double* __restrict__ W, int ldw,
+                                                         Ctl* ctl, double* partial, unsigned* cnt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  const double alpha = ctl->alpha;
+  const int i = ctl->i;
+  double s = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const double tr = add(t[r], mul(-alpha, W[(size_t)r * ldw + i]));
+    t[r] = tr;
+    s = add(s, mul(tr, tr));
+  }
+  double tot;
+  if (grid_total(s, partial, cnt, &tot) && threadIdx.x == 0) {
+    ctl->before = sqrt(tot);
+    ctl->after = ctl->before;
+    ctl->repass = 0;
+    ctl->npass = 0;
+  }
+}
+
+// W[:, col0 + q] = src_q for q < cnt, src_q = U + idx[q] * ldu (column-major sources), through
+// a 32 x 32 shared tile so both sides are coalesced
+__global__ void k_rw_put_cols(int n, double* __restrict__ W, int ldw, int col0, int cnt,
+                              const double* __restrict__ U, long ldu, const int* __restrict__ idx) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.x * 32, q0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int q = q0 + k, r = r0 + tx;
+    if (q < cnt && r < n) tile[k][tx] = U[(size_t)(idx ? idx[q] : q) * ldu + r];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, q = q0 + tx;
+    if (q < cnt && r < n) W[(size_t)r * ldw + col0 + q] = tile[tx][k];
+  }
+}
+
+// dst (column-major, ld n) = W[:, col0 .. col0+cnt)
+__global__ void k_rw_get_cols(int n, const double* __restrict__ W, int ldw, int col0, int cnt,
+                              double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.x * 32, q0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, q = q0 + tx;
+    if (q < cnt && r < n) tile[k][tx] = W[(size_t)r * ldw + col0 + q];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int q = q0 + k, r = r0 + tx;
+    if (q < cnt && r < n) dst[(size_t)q * n + r] = tile[tx][k];
+  }
+}
+
+__global__ void k_rw_col_move(int n, double* __restrict__ W, int ldw, int from, int to) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    W[(size_t)r * ldw + to] = W[(size_t)r * ldw + from];
+}
+
+template <class K, class... Args>
+void launch_pdl(const Ctx& c, K kern, dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SE_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
+int grid_small(const Ctx& c, int n) { return std::max(1, std::min(c.num_sms * 4, (n + kRT - 1) / kRT)); }
+
+size_t ring_bytes(int ldw) { return sizeof(double) * (size_t)kRS * kRR * ldw; }
+
+// register columns per thread for a capacity (template instance)
+template <int PH>
+void stream_launch(Ctx& c, const RowScratch& s, int n, const double* W, int ldw, double* t,
+                   const Ctl* ctl, const double* coef) {
+  const size_t smem = ring_bytes(ldw);
+  const dim3 grid(s.grid), block(kRT);
+  const int q = (ldw + kRT - 1) / kRT;
+#define SE_RW_CASE(QM)                                                                             \
+  if (q <= QM) {                                                                                   \
+    static std::atomic<unsigned long long> attr_set{0};  /* one bit per device */              \
+    const unsigned long long bit = 1ull << (c.device & 63);                                        \
+    if (!(attr_set.load() & bit)) {                                                                \
+      SE_CUDA(cudaFuncSetAttribute(k_rw_stream<PH, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)kRwMaxSmem));                                               \
+      attr_set.fetch_or(bit);                                                                      \
+    }                                                                                              \
+    launch_pdl(c, k_rw_stream<PH, QM>, grid, block, smem, n, W, ldw, t, ctl, coef, s.part, s.npart); \
+    ++c.launches;                                                                                  \
+    return;                                                                                        \
+  }
+  SE_RW_CASE(2)
+  SE_RW_CASE(4)
+  SE_RW_CASE(8)
+  SE_RW_CASE(12)
+  SE_RW_CASE(16)
+  SE_RW_CASE(20)
+  SE_RW_CASE(24)
+  SE_RW_CASE(32)
+#undef SE_RW_CASE
+  fail(SE_EINVAL, "row-major Krylov basis: capacity beyond 8192 columns");
+}
+
+template <int PH>
+void finish_launch(Ctx& c, const RowScratch& s, int ldw, Ctl* ctl, double* coef, double* hdiag,
+                   int want_before) {
+  const dim3 grid(PH == kN ? 1 : (ldw + kFinCols - 1) / kFinCols);
+  launch_pdl(c, k_rw_finish<PH>, grid, dim3(kRT), 0, s.grid, ldw, (const double*)s.part,
+             (const double*)s.npart, ctl, coef, hdiag, want_before);
+  ++c.launches;
+}
+
+}  // namespace
+
+int rw_ldw(int cols) { return std::max(2, (cols + 1) & ~1); }
+
+RowScratch rw_scratch(const Ctx& c, int ldw) {
+  RowScratch s;
+  const size_t smem = ring_bytes(ldw);
+  if (smem > kRwMaxSmem) fail(SE_EINVAL, "row-major Krylov basis: capacity beyond 8192 columns");
+  const int per_sm = std::max(1, std::min(2, (int)(kRwSmemPerSm / (smem + 2048))));
+  s.grid = c.num_sms * per_sm;
+  s.ldw = ldw;
+  return s;
+}
+size_t rw_scratch_doubles(const RowScratch& s) { return (size_t)s.grid * s.ldw + s.grid; }
+void rw_bind(RowScratch& s, double* buf) {
+  s.part = buf;
+  s.npart = buf + (size_t)s.grid * s.ldw;
+}
+
+void rw_cgs2(Ctx& c, const RowScratch& s, int n, double* t, const double* W, int ldw, Ctl* ctl,
+             double* hdiag, double* coef1, double* coef2, bool want_before) {
+  stream_launch<kT>(c, s, n, W, ldw, t, ctl, nullptr);
+  finish_launch<kT>(c, s, ldw, ctl, coef1, hdiag, want_before ? 1 : 0);
+  stream_launch<kMid>(c, s, n, W, ldw, t, ctl, coef1);
+  finish_launch<kMid>(c, s, ldw, ctl, coef2, hdiag, 0);
+  stream_launch<kN>(c, s, n, W, ldw, t, ctl, coef2);
+  finish_launch<kN>(c, s, ldw, ctl, nullptr, nullptr, 0);
+}
+
+void rw_col_get(Ctx& c, int n, const double* W, int ldw, const Ctl* ctl, int off, double* dst) {
+  launch_pdl(c, k_rw_col_get, dim3(grid_small(c, n)), dim3(kRT), 0, n, W, ldw, ctl, off, dst);
+  ++c.launches;
+}
+
+void rw_normalize(Ctx& c, unsigned* cnt, int n, const double* t, double* W, int ldw, Ctl* ctl,
+                  double* beta_arr) {
+  launch_pdl(c, k_rw_normalize, dim3(grid_small(c, n)), dim3(kRT), 0, n, t, W, ldw, ctl, beta_arr,
+             cnt);
+  ++c.launches;
+}
+
+void rw_nr_beta_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, int ldw,
+                      Ctl* ctl, double* alpha_arr, const double* beta_arr) {
+  launch_pdl(c, k_rw_nr_beta_alpha, dim3(grid_small(c, n)), dim3(kRT), 0, n, t, W, ldw, ctl,
+             alpha_arr, beta_arr, s.buf, s.cnt);
+  ++c.launches;
+}
+
+void rw_nr_sub_alpha(Ctx& c, const Scratch& s, int n, double* t, const double* W, int ldw, Ctl* ctl) {
+  launch_pdl(c, k_rw_nr_sub_alpha, dim3(grid_small(c, n)), dim3(kRT), 0, n, t, W, ldw, ctl, s.buf,
+             s.cnt);
+  ++c.launches;
+}
+
+void rw_put_cols(Ctx& c, int n, double* W, int ldw, int col0, int cnt, const double* U, long ldu,
+                 const int* idx_dev) {
+  if (cnt <= 0) return;
+  k_rw_put_cols<<<dim3((n + 31) / 32, (cnt + 31) / 32), 256, 0, c.stream>>>(n, W, ldw, col0, cnt,
+                                                                            U, ldu, idx_dev);
+  SE_CUDA(cudaGetLastError());
+  ++c.launches;
+}
+
+void rw_get_cols(Ctx& c, int n, const double* W, int ldw, int col0, int cnt, double* dst) {
+  if (cnt <= 0) return;
+  k_rw_get_cols<<<dim3((n + 31) / 32, (cnt + 31) / 32), 256, 0, c.stream>>>(n, W, ldw, col0, cnt, dst);
+  SE_CUDA(cudaGetLastError());
+  ++c.launches;
+}
+
+void rw_col_move(Ctx& c, int n, double* W, int ldw, int from, int to) {
+  if (from == to) return;
+  k_rw_col_move<<<grid_small(c, n), kRT, 0, c.stream>>>(n, W, ldw, from, to);
+  SE_CUDA(cudaGetLastError());
+  ++c.launches;
+}
+
+}  // namespace k
+}  // namespace se

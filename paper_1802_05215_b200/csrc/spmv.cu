@@ -271,8 +271,6 @@ constexpr int kKpmThreads = 256;
 constexpr int kEllMinB = 3;  // resident CTAs per SM the ELL kernel is register-capped for
 constexpr int kKpmPD = 1;    // default L2 prefetch distance (batches) of the ELL kernel
 
-constexpr int kKRows = 64;   // rows per tile: 16 half-warps x 4 rows
-constexpr int kKSlots = 512; // A entries (and gathered probe rows) staged per pass
 
 // x / d from the correctly rounded reciprocal with one FMA correction (Markstein): the
 // correctly rounded quotient for finite, non-extreme operands, at 3 instructions instead of the
@@ -326,111 +324,6 @@ __device__ __forceinline__ void kpm_finish(double acc0, double acc1, int b, bool
     }
   }
   if (threadIdx.x == 0) *counter = 0u;
-}
-
-// Tile kernel with the gathers done by cp.async: (1) the tile's A entries are staged into shared
-// memory; (2) every probe row they reference (16 doubles = 128 B) is copied into shared memory
-// with 16-byte cp.async -- all of a tile's gathers are in flight at once without occupying
-// registers; (3) each half-warp sums its rows from shared memory in storage order.
-__global__ void __launch_bounds__(kKpmThreads, 3) k_kpm_step(
-    int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vals,
-    int b, int mode, const double* __restrict__ v, const double* __restrict__ w0,
-    const double* __restrict__ w1, double* __restrict__ t, double cc, double d,
-    double* __restrict__ partial, unsigned* counter, double* __restrict__ zeta, int kmom) {
-  const bool first = mode == kKpmFirst;
-  const bool dbl = mode == kKpmDoubling;
-  extern __shared__ __align__(16) unsigned char kpm_smem[];
-  double(*s_x)[kB] = reinterpret_cast<double(*)[kB]>(kpm_smem);
-  double* s_v = reinterpret_cast<double*>(kpm_smem + sizeof(double) * kKSlots * kB);
-  int* s_c = reinterpret_cast<int*>(kpm_smem + sizeof(double) * (kKSlots * kB + kKSlots + 8));
-  const int lane = threadIdx.x & (kB - 1);
-  const int hw = threadIdx.x / kB;
-  const bool live = lane < b;
-  const double* __restrict__ src = first ? w0 : w1;
-  double acc0 = 0.0, acc1 = 0.0;
-  const int ntiles = (n + kKRows - 1) / kKRows;
-  const int parts = (b * 8 + 15) / 16;  // 16-byte pieces per probe row
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int r0 = tile * kKRows, rend = min(r0 + kKRows, n);
-    const int base = __ldg(rp + r0), end = __ldg(rp + rend);
-    int rs[4], re[4];
-    double xr[4], pr[4], vr[4], accr[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = r0 + hw + 16 * q;
-      rs[q] = re[q] = 0;
-      xr[q] = pr[q] = vr[q] = accr[q] = 0.0;
-      if (r < n) {
-        rs[q] = __ldg(rp + r);
-        re[q] = __ldg(rp + r + 1);
-        if (live) {
-          const size_t o = (size_t)r * b + lane;
-          xr[q] = __ldg(src + o);
-          if (!dbl) vr[q] = __ldg(v + o);
-          if (!first) pr[q] = __ldg(w0 + o);
-        }
-      }
-    }
-    for (int c0 = base; c0 < end; c0 += kKSlots) {
-      const int cn = min(kKSlots, end - c0), cend = c0 + cn;
-      const int va = c0 & ~1, ca = c0 & ~3;
-      const int nv16 = (cend - va + 1) >> 1, nc16 = (cend - ca + 3) >> 2;
-      __syncthreads();
-      for (int q = threadIdx.x; q < nv16; q += kKpmThreads)
-        cp_async16(&s_v[2 * q], vals + va + 2 * q, 8 * min(2, cend - (va + 2 * q)));
-      for (int q = threadIdx.x; q < nc16; q += kKpmThreads)
-        cp_async16(&s_c[4 * q], ci + ca + 4 * q, 4 * min(4, cend - (ca + 4 * q)));
-      cp_async_wait_all();
-      __syncthreads();
-      // gather the referenced probe rows (slot p <-> entry c0 + p)
-      if (b == kB) {  // full blocks: 8 x 16-byte pieces per 128-byte probe row
-        for (int q = threadIdx.x; q < cn * 8; q += kKpmThreads) {
-          const int p = q >> 3, part = q & 7;
-          cp_async16(&s_x[p][2 * part], src + (size_t)s_c[c0 + p - ca] * kB + 2 * part, 16);
-        }
-      } else {
-        for (int q = threadIdx.x; q < cn * parts; q += kKpmThreads) {
-          const int p = q / parts, part = q - p * parts;
-          const int bytes = min(16, b * 8 - part * 16);
-          cp_async16(&s_x[p][2 * part], src + (size_t)s_c[c0 + p - ca] * b + 2 * part, bytes);
-        }
-      }
-      cp_async_wait_all();
-      __syncthreads();
-      if (live) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int p0 = max(rs[q], c0), pend = min(re[q], cend);
-          for (int p = p0; p < pend; ++p) accr[q] = add(accr[q], mul(s_v[p - va], s_x[p - c0][lane]));
-        }
-      }
-    }
-    if (live) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = r0 + hw + 16 * q;
-        if (r >= n) continue;
-        const size_t o = (size_t)r * b + lane;
-        // (A w - c w) / d   (dos.hpp:99: division by d, unlike the filter's 1/d multiply)
-        const double m = __ddiv_rn(sub(accr[q], mul(cc, xr[q])), d);
-        if (first) {
-          t[o] = m;  // w1
-          acc0 = add(acc0, mul(vr[q], xr[q]));
-          acc1 = add(acc1, mul(vr[q], m));
-        } else {
-          const double tk = sub(mul(2.0, m), pr[q]);
-          t[o] = tk;
-          if (dbl) {  // w_k.w_k and w_k.w_{k+1} (T_2k = 2 T_k^2 - 1, T_2k+1 = 2 T_k T_k+1 - T_1)
-            acc0 = add(acc0, mul(xr[q], xr[q]));
-            acc1 = add(acc1, mul(xr[q], tk));
-          } else {
-            acc0 = add(acc0, mul(vr[q], tk));
-          }
-        }
-      }
-    }
-  }
-  kpm_finish(acc0, acc1, b, first, dbl, partial, counter, zeta, kmom);
 }
 
 // Pipelined direct-gather block step (default for even probe counts): no shared-memory staging;
@@ -805,46 +698,25 @@ void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
     k.x_indirect = (mode == kFirst || mode == kPlain);
     k.prev_indirect = (mode == kNext);
   }
-  static const int cap = [] {
-    const char* e = std::getenv("SE_FILTER_CTAS");
-    return e ? std::atoi(e) : 0;
-  }();
   const int ntiles = (a.n + kRows - 1) / kRows;
-  dim3 grid(cap > 0 ? std::min(cap, ntiles) : ntiles, mode == kPlain ? args.ncols : 1);
-  static const bool pdl = std::getenv("SE_NO_PDL") == nullptr;
+  dim3 grid(ntiles, mode == kPlain ? args.ncols : 1);
   // The filter chain is latency-bound (k dependent launches per Lanczos step) while the slices'
   // reorthogonalisation passes sharing the GPU are bandwidth-bound: filter launches (and their
   // graph nodes) get the device's highest priority so their CTAs are scheduled ahead of queued
   // GEMV CTAs of other slices.
-  static const bool prio = std::getenv("SE_NO_FILTER_PRIO") == nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kRows);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = c.stream;
-  cudaLaunchAttribute attr[3];
+  cudaLaunchAttribute attr[2];
   int na = 0;
-  const size_t eb = a.entries_bytes();
-  if (c.l2_persist > 0 && eb <= c.l2_persist && eb <= c.l2_window_max) {
-    // the CSR entries (vals + col_idx, one allocation) persist in the L2 set-aside
-    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[na].val.accessPolicyWindow.base_ptr = a.v;
-    attr[na].val.accessPolicyWindow.num_bytes = eb;
-    attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    ++na;
-  }
-  if (pdl) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  if (prio) {
-    attr[na].id = cudaLaunchAttributePriority;
-    attr[na].val.priority = c.prio_hi;
-    ++na;
-  }
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  attr[na].id = cudaLaunchAttributePriority;
+  attr[na].val.priority = c.prio_hi;
+  ++na;
   cfg.attrs = attr;
   cfg.numAttrs = na;
   switch (mode) {
@@ -863,22 +735,9 @@ void spmv_cheb(Ctx& c, const DevCsr& a, int mode, const ChebArgs& args) {
   ++c.launches;
 }
 
-constexpr size_t kKpmSmem = sizeof(double) * (kKSlots * kB + kKSlots + 8) + sizeof(int) * (kKSlots + 8);
-
-// Exactly the resident CTAs: the grid-stride tile loop then sweeps one contiguous window of
-// rows, so the probe rows a tile gathers from its neighbours (+-nx, +-nx ny for stencils) were
-// just loaded, or are about to be, by the CTAs next to it -- L2 hits instead of HBM re-reads.
-int kpm_blocks(const Ctx& c, int n) {
-  static const int per_sm = [] {
-    SE_CUDA(cudaFuncSetAttribute(k_kpm_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpmSmem));
-    int v = 0;
-    SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_step, kKpmThreads, kKpmSmem));
-    return std::max(1, v);
-  }();
-  return std::max(1, std::min(c.num_sms * per_sm, (n + kKRows - 1) / kKRows));
-}
 size_t kpm_scratch_doubles(const Ctx& c, int n) {
-  return (size_t)2 * kB * std::max(kpm_blocks(c, n), c.num_sms * 8);
+  (void)n;
+  return (size_t)2 * kB * c.num_sms * 8;  // per-CTA partials of the (<= 8 per SM) resident grid
 }
 
 void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args) {
@@ -924,37 +783,22 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
               const double* w0, const double* w1, double* t, double cc, double d, double* zeta_dev,
               int kmom) {
   if (kpm_scratch_doubles(c, a.n) > s.cap || s.ncnt < 1) fail(SE_EINVAL, "internal: kpm scratch");
-  // default: the pipelined direct-gather kernel (even probe counts); odd counts take the
-  // shared-memory tile kernel.  SE_KPM_KERNEL=tile forces the latter (A/B comparisons).
-  static const int variant = [] {  // 0: ELL (default when built), 1: CSR stream, 2: CSR tile
-    const char* e = std::getenv("SE_KPM_KERNEL");
-    if (!e) return 0;
-    const std::string v(e);
-    return v == "tile" ? 2 : v == "stream" ? 1 : 0;
-  }();
-  if (variant == 0 && a.ell_c && b % 2 == 0) {
-    static const int pd = [] {  // L2 prefetch distance in batches (SE_KPM_PD = 1..3)
-      const char* e = std::getenv("SE_KPM_PD");
-      const int v = e ? std::atoi(e) : 0;
-      return v >= 1 && v <= 3 ? v : kKpmPD;
-    }();
-    using EFn = decltype(&k_kpm_ell<0, 16, 1>);
-    auto pick = [&](auto md, auto pdc) -> EFn {
-      constexpr int M = decltype(md)::value, P = decltype(pdc)::value;
-      return b == 16 ? k_kpm_ell<M, 16, P> : b == 8 ? k_kpm_ell<M, 8, P> : k_kpm_ell<M, 0, P>;
+  if (b % 2 != 0) fail(SE_EINVAL, "internal: kpm blocks carry an even probe count");
+  // Matrices with <= kEllW entries per row (stencils) keep a padded-row copy: the ELL kernel.
+  // Longer rows (random sparse, cfg4) stream the CSR entries.
+  if (a.ell_c) {
+    using EFn = decltype(&k_kpm_ell<0, 16, kKpmPD>);
+    auto pick = [&](auto md) -> EFn {
+      constexpr int M = decltype(md)::value;
+      return b == 16 ? k_kpm_ell<M, 16, kKpmPD> : b == 8 ? k_kpm_ell<M, 8, kKpmPD> : k_kpm_ell<M, 0, kKpmPD>;
     };
-    auto pick_mode = [&](auto pdc) -> EFn {
-      return mode == kKpmFirst      ? pick(std::integral_constant<int, kKpmFirst>{}, pdc)
-             : mode == kKpmDoubling ? pick(std::integral_constant<int, kKpmDoubling>{}, pdc)
-                                    : pick(std::integral_constant<int, 0>{}, pdc);
-    };
-    const EFn kern = pd == 1   ? pick_mode(std::integral_constant<int, 1>{})
-                     : pd == 2 ? pick_mode(std::integral_constant<int, 2>{})
-                               : pick_mode(std::integral_constant<int, 3>{});
+    const EFn kern = mode == kKpmFirst      ? pick(std::integral_constant<int, kKpmFirst>{})
+                     : mode == kKpmDoubling ? pick(std::integral_constant<int, kKpmDoubling>{})
+                                            : pick(std::integral_constant<int, 0>{});
     static const int per_sm = [] {
       int v = 0;
-      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_ell<kKpmDoubling, 16, 1>, kKpmThreads, 0));
-      return std::max(1, v);
+      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_ell<kKpmDoubling, 16, kKpmPD>, kKpmThreads, 0));
+      return std::max(1, std::min(v, 8));
     }();
     const int grid = std::max(1, std::min(c.num_sms * per_sm, (a.n + 31) / 32));
     kern<<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.ell_c, a.ell_a, b, v, w0, w1, t, cc, d, s.buf, s.cnt,
@@ -963,31 +807,23 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
     SE_CUDA(cudaGetLastError());
     return;
   }
-  if (variant != 2 && b % 2 == 0) {
-    static const int per_sm = [] {
-      int v = 0;
-      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_stream<8, 0>, kKpmThreads, 0));
-      return std::max(1, v);
-    }();
-    const int grid = std::max(1, std::min(c.num_sms * per_sm, (a.n + 31) / 32));
-    // U = entries gathered per row in one round: the matrix's row length (stencils: 5 or 7)
-    using KFn = decltype(&k_kpm_stream<8, 0>);
-    auto pick = [&](auto u) -> KFn {
-      constexpr int U = decltype(u)::value;
-      return b == 16 ? k_kpm_stream<U, 16> : b == 8 ? k_kpm_stream<U, 8> : k_kpm_stream<U, 0>;
-    };
-    const KFn kern = a.max_row_nnz <= 5 ? pick(std::integral_constant<int, 5>{})
-                     : a.max_row_nnz <= 7 ? pick(std::integral_constant<int, 7>{})
-                                          : pick(std::integral_constant<int, 8>{});
-    kern<<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc, d, s.buf,
-                                             s.cnt, zeta_dev, kmom);
-    ++c.launches;
-    SE_CUDA(cudaGetLastError());
-    return;
-  }
-  const int blocks = kpm_blocks(c, a.n);
-  k_kpm_step<<<blocks, kKpmThreads, kKpmSmem, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t,
-                                                      cc, d, s.buf, s.cnt, zeta_dev, kmom);
+  static const int per_sm = [] {
+    int v = 0;
+    SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_kpm_stream<8, 0>, kKpmThreads, 0));
+    return std::max(1, std::min(v, 8));
+  }();
+  const int grid = std::max(1, std::min(c.num_sms * per_sm, (a.n + 31) / 32));
+  // U = entries gathered per row in one round: the matrix's row length (stencils: 5 or 7)
+  using KFn = decltype(&k_kpm_stream<8, 0>);
+  auto pick = [&](auto u) -> KFn {
+    constexpr int U = decltype(u)::value;
+    return b == 16 ? k_kpm_stream<U, 16> : b == 8 ? k_kpm_stream<U, 8> : k_kpm_stream<U, 0>;
+  };
+  const KFn kern = a.max_row_nnz <= 5 ? pick(std::integral_constant<int, 5>{})
+                   : a.max_row_nnz <= 7 ? pick(std::integral_constant<int, 7>{})
+                                        : pick(std::integral_constant<int, 8>{});
+  kern<<<grid, kKpmThreads, 0, c.stream>>>(a.n, a.rp, a.ci, a.v, b, mode, v, w0, w1, t, cc, d, s.buf,
+                                           s.cnt, zeta_dev, kmom);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }

@@ -6,6 +6,8 @@
 #include <cfloat>
 
 #include <chrono>
+#include <cmath>
+#include <vector>
 
 #include "kernels.hpp"
 
@@ -14,63 +16,58 @@ namespace k {
 
 namespace {
 
+// 1/q to full double precision without the division subroutine: the 23-bit hardware estimate
+// refined by two Newton steps (the count below depends only on signs, and bisection on it is
+// backward stable; results are deterministic).
+__device__ __forceinline__ double recip(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = fma(r, fma(-q, r, 1.0), r);
+  r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
+// Sturm count (number of eigenvalues < x) of the tridiagonal (d, e2 = e^2), pivot floor piv.
 __device__ __forceinline__ int sturm_count(int m, const double* __restrict__ d,
-                                           const double* __restrict__ e, double x, double piv) {
+                                           const double* __restrict__ e2, double x, double piv) {
   int cnt = 0;
   double q = d[0] - x;
   if (fabs(q) < piv) q = -piv;
   cnt += q < 0.0;
   for (int i = 1; i < m; ++i) {
-    q = (d[i] - x) - (e[i - 1] * e[i - 1]) / q;
+    q = (d[i] - x) - e2[i - 1] * recip(q);
     if (fabs(q) < piv) q = -piv;
     cnt += q < 0.0;
   }
   return cnt;
 }
 
-// One warp per wanted eigenvalue (ascending index idx = nbelow + warp): 32-point multisection,
+// One warp per wanted eigenvalue (ascending index idx = below + warp): 32-point multisection,
 // each lane evaluating one Sturm count, so the bracket shrinks 33x per round (~10 rounds to
-// machine precision instead of ~55 bisection steps).
-__global__ void k_tridiag_above(int m, const double* __restrict__ d, const double* __restrict__ e,
-                                double bar, double* __restrict__ vals, int* __restrict__ count) {
-  __shared__ double s_lo, s_hi, s_piv;
-  __shared__ int s_below;
-  if (threadIdx.x == 0) {
-    double lo = DBL_MAX, hi = -DBL_MAX, emax = 0.0;
-    for (int i = 0; i < m; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0);
-      lo = fmin(lo, d[i] - r);
-      hi = fmax(hi, d[i] + r);
-      if (i + 1 < m) emax = fmax(emax, e[i] * e[i]);
-    }
-    s_piv = DBL_MIN * fmax(1.0, emax);
-    const double pad = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + s_piv;
-    s_lo = lo - pad;
-    s_hi = hi + pad;
-    s_below = sturm_count(m, d, e, bar, s_piv);
-    if (blockIdx.x == 0) *count = m - s_below;
-  }
-  __syncthreads();
+// machine precision instead of ~55 bisection steps).  The Gershgorin bracket, pivot floor and
+// the count below `bar` are computed once on the host (O(m)) and passed in.
+__global__ void k_tridiag_above(int m, const double* __restrict__ d, const double* __restrict__ e2,
+                                double bar, double glo, double ghi, double piv, int below,
+                                double* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
-  const int idx = s_below + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int idx = below + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (idx >= m) return;
-  const double piv = s_piv;
-  double a = fmax(bar, s_lo), b = s_hi;
+  double a = fmax(bar, glo), b = ghi;
   if (a > b) a = b;
   for (int round = 0; round < 40; ++round) {
     if ((b - a) <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b)) + piv) break;
     const double x = a + (b - a) * (double)(lane + 1) / 33.0;
-    const int c = sturm_count(m, d, e, x, piv);
+    const int c = sturm_count(m, d, e2, x, piv);
     // points with count <= idx lie left of the wanted eigenvalue
     const unsigned left = __ballot_sync(0xffffffffu, c <= idx);
     const int nl = __popc(left);  // points 0..nl-1 are left (counts are monotone in x)
     const double na = nl > 0 ? __shfl_sync(0xffffffffu, x, nl - 1) : a;
     const double nb = nl < 32 ? __shfl_sync(0xffffffffu, x, nl < 32 ? nl : 31) : b;
-    if (!(na >= a && nb <= b) || na == a && nb == b) break;
+    if (!(na >= a && nb <= b) || (na == a && nb == b)) break;
     a = na;
     b = nb;
   }
-  if (lane == 0) vals[idx - s_below] = 0.5 * (a + b);
+  if (lane == 0) vals[idx - below] = 0.5 * (a + b);
 }
 
 }  // namespace
@@ -82,31 +79,55 @@ void tridiag_eigs_above(Ctx& c, int m, const double* d_host, const double* e_hos
   out.clear();
   if (m <= 0) return;
   double* d = work;
-  double* e = work + m;
+  double* e2 = work + m;
   double* vals = work + 3 * m;
-  int* cnt = reinterpret_cast<int*>(work + 4 * m);
   const auto t0 = std::chrono::steady_clock::now();
+  // host O(m): Gershgorin bracket, pivot floor, squared off-diagonal, count below bar (the same
+  // recurrence the device runs, so the device's indices start exactly at the first value >= bar)
+  std::vector<double> h2((size_t)std::max(m - 1, 1));
+  double glo = DBL_MAX, ghi = -DBL_MAX, emax = 0.0;
+  for (int i = 0; i < m; ++i) {
+    const double r = (i > 0 ? std::fabs(e_host[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(e_host[i]) : 0.0);
+    glo = std::fmin(glo, d_host[i] - r);
+    ghi = std::fmax(ghi, d_host[i] + r);
+    if (i + 1 < m) {
+      h2[i] = e_host[i] * e_host[i];
+      emax = std::fmax(emax, h2[i]);
+    }
+  }
+  const double piv = DBL_MIN * std::fmax(1.0, emax);
+  const double pad = 2.0 * DBL_EPSILON * std::fmax(std::fabs(glo), std::fabs(ghi)) + piv;
+  glo -= pad;
+  ghi += pad;
+  int below = 0;
+  {
+    double q = d_host[0] - bar;
+    if (std::fabs(q) < piv) q = -piv;
+    below += q < 0.0;
+    for (int i = 1; i < m; ++i) {
+      q = (d_host[i] - bar) - h2[i - 1] / q;
+      if (std::fabs(q) < piv) q = -piv;
+      below += q < 0.0;
+    }
+  }
+  const int h = m - below;
+  out.resize(h);
+  if (h == 0) return;
   h2d(c, d, d_host, sizeof(double) * m);
-  if (m > 1)
-    h2d(c, e, e_host, sizeof(double) * (m - 1));
+  if (m > 1) h2d(c, e2, h2.data(), sizeof(double) * (m - 1));
   const auto t1 = std::chrono::steady_clock::now();
   const int tb = 128;  // 4 eigenvalues (warps) per CTA
   SE_CUDA(cudaEventRecord(c.evk0, c.stream));
-  k_tridiag_above<<<(m + 3) / 4, tb, 0, c.stream>>>(m, d, e, bar, vals, cnt);
+  k_tridiag_above<<<(h + 3) / 4, tb, 0, c.stream>>>(m, d, e2, bar, glo, ghi, piv, below, vals);
   SE_CUDA(cudaEventRecord(c.evk1, c.stream));
   ++c.launches;
   SE_CUDA(cudaGetLastError());
-  int h = 0;
-  d2h(c, &h, cnt, sizeof(int));
+  d2h(c, out.data(), vals, sizeof(double) * h);
   ctx_sync(c);
   const auto t2 = std::chrono::steady_clock::now();
   float kms = 0.f;
   SE_CUDA(cudaEventElapsedTime(&kms, c.evk0, c.evk1));
   c.prof_kernel_ms += kms;
-  out.resize(h);
-  if (h)
-    d2h(c, out.data(), vals, sizeof(double) * h);
-  ctx_sync(c);
   const auto t3 = std::chrono::steady_clock::now();
   auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
   c.prof_chk[0] += sec(t0, t1);

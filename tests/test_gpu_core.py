@@ -126,22 +126,61 @@ def test_laplacian_60x60_window(gpu_ctx, driver):
         assert abs(res - r.residuals[i]) <= 1e-10
 
 
-@pytest.mark.parametrize("variant", ["ell", "stream", "tile"])
-def test_kpm_kernel_variants(gpu_ctx, variant):
-    """Every block-KPM kernel (padded-row default, CSR stream, CSR tile) against the oracle on
-    stencils and an irregular matrix with 0..8 entries per row (empty rows included), with full
-    (16), ragged (21 = 16 + 5) and narrow (6) probe blocks."""
-    import json, os, subprocess, sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SE_KPM_KERNEL=variant,
-               PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")]))
-    r = subprocess.run([sys.executable, os.path.join(root, "tests", "_kpm_variant_case.py")],
-                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    errs = json.loads(r.stdout.strip().splitlines()[-1])
-    assert len(errs) == 9
-    for k, e in errs.items():
-        assert e <= 1e-12, (variant, k, e)
+def _irregular(n, seed, maxdeg):
+    """Symmetric matrix with 0..maxdeg entries per row (some empty rows)."""
+    rng = np.random.default_rng(seed)
+    deg = np.zeros(n, int)
+    rows, cols, vals = [], [], []
+    seen = set()
+    for i in range(n):
+        if i % 11 == 5:
+            continue  # empty row (and column)
+        rows.append(i); cols.append(i); vals.append(2.0 + rng.random())
+        deg[i] += 1
+    for i in range(n):
+        for _ in range(int(rng.integers(0, maxdeg // 2 + 1))):
+            j = int(rng.integers(0, n))
+            if j == i or i % 11 == 5 or j % 11 == 5 or deg[i] >= maxdeg or deg[j] >= maxdeg:
+                continue
+            if (min(i, j), max(i, j)) in seen:
+                continue
+            seen.add((min(i, j), max(i, j)))
+            v = float(rng.standard_normal()) * 0.3
+            rows += [i, j]; cols += [j, i]; vals += [v, v]
+            deg[i] += 1; deg[j] += 1
+    return _api().CsrMatrix.from_triplets(n, rows, cols, vals)
+
+
+@pytest.mark.parametrize("case", ["lap20", "lap2d", "irr8", "irr24", "banded"])
+def test_kpm_block_kernels(gpu_ctx, case):
+    """Both block-KPM kernels against the oracle: the padded-row kernel (rows <= 8: stencils and
+    an irregular matrix with 0..8 entries per row, empty rows included) and the CSR-stream
+    kernel (longer rows: an irregular matrix with up to 24 per row, a cfg4-recipe random banded
+    matrix), with full (16), ragged (21 = 16 + 5) and narrow (6) probe blocks."""
+    api = _api()
+    if case == "lap20":
+        a, (lo, hi) = api.gen_laplacian([20, 20, 20]), (0.0, 12.0)
+    elif case == "lap2d":
+        a, (lo, hi) = api.gen_laplacian([37, 23]), (0.0, 8.0)
+    elif case == "irr8":
+        a, (lo, hi) = _irregular(3001, 7, 8), (-4.0, 6.0)
+    elif case == "irr24":
+        a, (lo, hi) = _irregular(2003, 9, 24), (-6.0, 8.0)
+    else:
+        a = api.gen_random_sparse(4000, 11)
+        rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+        diag = np.zeros(a.n)
+        diag[rows[a.col_idx == rows]] = a.vals[a.col_idx == rows]
+        rad = np.bincount(rows, weights=np.abs(a.vals), minlength=a.n) - np.abs(diag)
+        lo, hi = float(np.min(diag - rad)), float(np.max(diag + rad))  # Gershgorin
+    mx = int(np.max(np.diff(a.row_ptr)))
+    assert (mx <= 8) == (case in ("lap20", "lap2d", "irr8")), mx
+    for nvec in (16, 21, 6):
+        z = api.kpm_moments(a, api.SpectralBounds(lo, hi), 40, nvec, seed=3)
+        zr = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, lo, hi, 40, nvec, 3)
+        zn, zrn = z / (nvec * a.n), zr / (nvec * a.n)
+        err = np.abs(zn - zrn) / np.maximum(np.abs(zrn), abs(zrn[0]))
+        assert err.max() <= 1e-12, (case, nvec, err.max())
 
 
 def test_kpm_rademacher_threaded_bits_match_oracle(gpu_ctx):
@@ -159,3 +198,32 @@ def test_kpm_rademacher_threaded_bits_match_oracle(gpu_ctx):
     zr2 = clib.kpm_moments(a.row_ptr, a.col_idx, a.vals, lo, hi, 12, 19, 5, first=3, count=16)
     tol2 = 1e-12 * np.maximum(np.abs(zr2), abs(zr2[0]))
     assert np.all(np.abs(z2 - zr2) <= tol2)
+
+
+@pytest.mark.parametrize("n,k,repass", [(4097, 1, True), (5000, 300, True), (5000, 300, False),
+                                        (20001, 1300, True), (3000, 2900, True), (9000, 6000, True)])
+def test_paired_cgs2_row_major_vs_numpy(gpu_ctx, n, k, repass):
+    """The product CGS2 (row-major basis, T1 + fused N1/T2 + N2, rowgs.cu) against a numpy
+    restatement of paired_cgs2 (orth.hpp:63-80), with and without the DGKS re-pass, across the
+    register-column templates (k = 1 .. 6000)."""
+    api = _api()
+    rng = np.random.default_rng(n + k)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    t = rng.standard_normal(n)
+    if repass:
+        t = t + Q @ rng.standard_normal(k) * 50.0
+    h = np.zeros(k)
+    before = np.linalg.norm(t)
+    c1 = Q.T @ t
+    t1 = t - Q @ c1
+    h += c1
+    if not np.linalg.norm(t1) > 0.70710678118654752 * before:
+        c2 = Q.T @ t1
+        t1 = t1 - Q @ c2
+        h += c2
+        assert repass
+    else:
+        assert not repass
+    tg, hg = api.paired_cgs2(t, np.ascontiguousarray(Q.T), np.zeros(k))
+    assert np.max(np.abs(tg - t1)) <= 1e-12 * before
+    assert np.max(np.abs(hg - h)) <= 1e-12 * before

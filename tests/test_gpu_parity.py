@@ -349,21 +349,6 @@ def test_cfg5_proxy_scaled_slices_match_reference(gpu_ctx, golden):
         assert np.all(r.residuals <= 1e-8 * np.maximum(1.0, np.abs(r.eigenvalues)))
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
-def test_fused_cgs2_opt_in_matches_reference(gpu_ctx, variant):
-    """The opt-in fused CGS2 middle kernels (SE_CGS_FUSED=1: TMA-staged row blocks; 2: L2
-    two-read, cgs_mid.cu) reproduce the reference on the cfg5 proxy slices (run in a fresh
-    process: the switch is read once per process)."""
-    import os
-    import subprocess
-    import sys
-    here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, SE_CGS_FUSED=variant)
-    out = subprocess.run([sys.executable, os.path.join(here, "_fused_cgs_case.py")], env=env,
-                         capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "fused-ok" in out.stdout, out.stderr[-2000:]
-
-
 @pytest.mark.parametrize("case", [0, 1])
 def test_cheb_si_matches_reference(gpu_ctx, golden, case):
     """cheb_si (eigensolvers.hpp:760-940) on 60x60 windows against the reference's own run:
