@@ -13,8 +13,8 @@ One step = one full pipeline pass: bounds -> KPM -> slicing -> 8 filtered-Lanczo
 `value`  : eigenpairs/s with the matrix already resident in HBM (device generator) at t0.
 `e2e`    : the same pipeline through the public API from a pinned HOST CSR: H2D of the matrix and
            D2H of all eigenpairs (values + vectors) inside the timed region.
-`roofline`: the dominant kernel on cfg2, the reorthogonalisation pass (k_gemvt + k_gemvn, bytes
-           16 n k + 24 n), and beside it the fused Chebyshev-filter SpMV (bytes Abytes + 40 n per
+`roofline`: the dominant kernel class on cfg2, the CGS2 step on the row-major basis (T1 + fused
+           MID + N2, bytes 24 n k + 40 n), and beside it the fused Chebyshev-filter SpMV (bytes Abytes + 40 n per
            degree) on the workload matrix and on 160^3 (A > L2); all timed live with
            CUDA events on the launching stream, graph-captured as in production.
 `cpu_baseline` / `--impl reference`: the unmodified reference (oracle/_ref, compiled from
@@ -169,14 +169,19 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
     peak, peak_kind = _peaks()
     ctx = api.Context(local_gpu)
     out = {}
-    # reorthogonalisation pass on the workload's basis shape (n = 64^3, k = mean active columns)
+    # the CGS2 step on the workload's basis shape (n = 64^3, k = mean active columns), re-pass
+    # forced as in TR: row-major basis, T1 + fused MID + N2 = three reads of W (rowgs.cu)
     n = int(np.prod(dims))
     ms = C.c_double()
     reps = 20
-    _lib.call("se_cgs_bench", ctx.handle, n, cfg2_mean_cols, reps, C.byref(ms))
+    _lib.call("se_cgs2_bench", ctx.handle, n, cfg2_mean_cols, reps, 2, C.byref(ms))
     per = ms.value / reps * 1e-3
-    by = 16.0 * n * cfg2_mean_cols + 24.0 * n
+    by = 24.0 * n * cfg2_mean_cols + 40.0 * n
     out["cgs"] = (by / per / 1e9, per, by)
+    # the column-major two-pass step it replaced (four reads of W), same shape, for reference
+    ms0 = C.c_double()
+    _lib.call("se_cgs2_bench", ctx.handle, n, cfg2_mean_cols, reps, 0, C.byref(ms0))
+    out["cgs_colmajor"] = ms0.value / reps * 1e-3
     # filter SpMV on the workload matrix (L2-resident) and on 160^3 (A = 359 MB > L2)
     for tag, dd in (("workload", dims), ("hbm", [160, 160, 160])):
         A = api.DeviceCsr.laplacian(dd, ctx)
@@ -207,11 +212,15 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
             traffic = json.load(fh)
     def _t(key):
         return traffic.get(key, {}).get("traffic_bytes")
-    roof = {"bound": "hbm", "kernel": "reorthogonalisation pass k_gemvt + k_gemvn (CGS, orth.hpp:19-32)",
+    roof = {"bound": "hbm",
+            "kernel": "CGS2 step on the row-major Krylov basis: k_rw_stream T1 + fused MID (N1, "
+                      "||t1||, T2) + N2 with their finishing reductions (orth.hpp:63-80, rowgs.cu)",
             "achieved": round(g, 1), "peak": peak, "unit": "GB/s", "frac": round(g / peak, 4),
-            "peak_kind": peak_kind, "traffic": _t("cgs_pass_n262144_k1440"),
-            "shape": f"n={n}, k={cfg2_mean_cols} basis columns (mean over the cfg2 run)",
-            "us_per_pass": round(per * 1e6, 2), "bytes_per_pass": by,
+            "peak_kind": peak_kind, "traffic": _t("rw_cgs2_step_n262144"),
+            "shape": f"n={n}, k={cfg2_mean_cols} basis columns (mean over the cfg2 run), re-pass forced",
+            "us_per_step": round(per * 1e6, 2), "bytes_per_step": by,
+            "algorithmic_bytes": "24 n k + 40 n (three reads of W; t read by T1, read+written by MID and N2)",
+            "column_major_4read_us": round(out["cgs_colmajor"] * 1e6, 2),
             "filter_spmv": {"kernel": "k_spmv_cheb<kNext> (fused filter degree)",
                             "hbm_160^3": {"achieved": round(out["hbm"][0], 1),
                                           "frac": round(out["hbm"][0] / peak, 4),
@@ -464,9 +473,9 @@ def main():
         step_s = ms * 1e-3 / args.steps
         rate = obytes / step_s / 1e9
         roof["in_situ"] = {
-            "what": "reorthogonalisation bytes of one timed step (all slices, device counters) / "
-                    "that step's wall time: the rate the dominant kernel class sustains inside the "
-                    "concurrent step",
+            "what": "CGS2 bytes of one timed step (every streamed basis column, 8 n each, + vector "
+                    "traffic; device counters of all slices) / that step's wall time: the rate the "
+                    "dominant kernel class sustains inside the concurrent step",
             "orth_bytes_per_step": obytes, "orth_passes": passes, "mean_cols": mean_cols,
             "step_s": round(step_s, 3), "achieved": round(rate, 1),
             "frac": round(rate / roof["peak"], 4)}

@@ -22,6 +22,8 @@
 #include <thread>
 #include <vector>
 
+#include "sliceeig/cheb_approx.hpp"
+#include "sliceeig/cholesky.hpp"
 #include "sliceeig/dos.hpp"
 #include "sliceeig/eigensolvers.hpp"
 #include "sliceeig/filter_poly.hpp"
@@ -459,6 +461,99 @@ void* ref_cheb_lan_pencil(int n, const int* rp, const int* ci, const double* v, 
     std::vector<Triplet> tb;
     for (int i = 0; i < n; ++i) tb.push_back({i, i, bdiag[i]});
     CsrMatrix b = CsrMatrix::from_triplets(n, std::move(tb));
+    PolyOpts po;
+    po.damping = damping_of(damping);
+    PolynomialFilter f = find_pol(xi, eta, SpectralBounds{lmin, lmax}, po);
+    SolverConfig cfg;
+    cfg.res_tol = res_tol;
+    cfg.est_count = est_count;
+    cfg.seed = (unsigned long)seed;
+    rs->degrees.push_back(f.k);
+    rs->slices.push_back(solver == 2   ? cheb_si(a, &b, f, xi, eta, est_count, cfg)
+                         : solver == 1 ? cheb_lan_tr(a, &b, f, xi, eta, cfg)
+                                       : cheb_lan_nr(a, &b, f, xi, eta, cfg));
+  });
+  if (rc != 0) {
+    delete rs;
+    return nullptr;
+  }
+  return rs;
+}
+
+// ---- general SPD-B pencils (the reference's Cholesky-backed path) -----------------------------
+// ls_pol_approx (cheb_approx.hpp:40-88): fun 0 = B^-1, 1 = B^-1/2; coefficients out (cap).
+int ref_ls_pol_approx(int fun, double lmin, double lmax, double tol, int max_deg, int cap,
+                      int* degree, double* coeff, double* achieved) {
+  return guarded([&] {
+    ChebApprox ap = ls_pol_approx(fun == 1 ? ScalarFun::InverseSqrt : ScalarFun::Inverse,
+                                  SpectralBounds{lmin, lmax}, tol, max_deg);
+    if (ap.degree() + 1 > cap) throw std::runtime_error("ref_ls_pol_approx: buffer too small");
+    *degree = ap.degree();
+    std::memcpy(coeff, ap.coeff.data(), sizeof(double) * ap.coeff.size());
+    *achieved = ap.achieved_rel_error;
+  });
+}
+
+// apply_cheb (cheb_approx.hpp:91-112) with the approximation given by its coefficients
+int ref_apply_cheb(int n, const int* rp, const int* ci, const double* v, int fun, double lmin,
+                   double lmax, int degree, const double* coeff, const double* x, double* y) {
+  return guarded([&] {
+    CsrMatrix b = make_csr(n, rp, ci, v);
+    ChebApprox ap{fun == 1 ? ScalarFun::InverseSqrt : ScalarFun::Inverse, lmin, lmax,
+                  Vec(coeff, coeff + degree + 1), 0.0};
+    Vec out;
+    apply_cheb(ap, make_operator(b), Vec(x, x + n), out);
+    std::memcpy(y, out.data(), sizeof(double) * n);
+  });
+}
+
+// Pencil (A, B) with a general sparse SPD B given in CSR: lan_tr_bounds in the B inner product
+// (sliceeig_main.cpp:128-136), dos_generalized with Cholesky solves (:138-157), and one
+// cheb_lan_nr/tr slice with b != nullptr (eigensolvers.hpp:640-732).
+int ref_pencil_bounds(int n, const int* rp, const int* ci, const double* v, const int* brp,
+                      const int* bci, const double* bv, std::uint64_t seed, double* lmin,
+                      double* lmax) {
+  return guarded([&] {
+    CsrMatrix a = make_csr(n, rp, ci, v), b = make_csr(n, brp, bci, bv);
+    Operator opa = make_operator(a), opb = make_operator(b);
+    SpdFactor bf = SpdFactor::factor(b);
+    Operator bsolve{n, [&](const Vec& x, Vec& y) { y = bf.solve(x); }};
+    InnerProduct ip{&opb, &bsolve};
+    SpectralBounds r = lan_tr_bounds(opa, ip, 1e-4, 60, 40, (unsigned long)seed);
+    *lmin = r.lmin;
+    *lmax = r.lmax;
+  });
+}
+
+int ref_pencil_dos(int n, const int* rp, const int* ci, const double* v, const int* brp,
+                   const int* bci, const double* bv, double lmin, double lmax, int m, int n_vec,
+                   int npts, std::uint64_t seed, double* x, double* y, double* nev_est) {
+  return guarded([&] {
+    CsrMatrix a = make_csr(n, rp, ci, v), b = make_csr(n, brp, bci, bv);
+    Operator opa = make_operator(a), opb = make_operator(b);
+    SpdFactor bf = SpdFactor::factor(b);
+    Operator bsolve{n, [&](const Vec& xx, Vec& yy) { yy = bf.solve(xx); }};
+    Operator bhalf{n, [&](const Vec& xx, Vec& yy) { yy = bf.solve_gt(xx); }};
+    DosConfig cfg;
+    cfg.method = DosMethod::Lanczos;
+    cfg.m = m;
+    cfg.n_vec = n_vec;
+    cfg.npts = npts;
+    cfg.seed = seed;
+    DosCurve c = dos_generalized(opa, bsolve, bhalf, opb, {lmin, lmax}, cfg);
+    std::memcpy(x, c.xdos.data(), sizeof(double) * npts);
+    std::memcpy(y, c.ydos.data(), sizeof(double) * npts);
+    *nev_est = c.nev_est;
+  });
+}
+
+void* ref_cheb_lan_pencil_csr(int n, const int* rp, const int* ci, const double* v,
+                              const int* brp, const int* bci, const double* bv, int solver,
+                              double xi, double eta, double lmin, double lmax, int damping,
+                              double res_tol, int est_count, std::uint64_t seed) {
+  auto* rs = new ResultSet();
+  int rc = guarded([&] {
+    CsrMatrix a = make_csr(n, rp, ci, v), b = make_csr(n, brp, bci, bv);
     PolyOpts po;
     po.damping = damping_of(damping);
     PolynomialFilter f = find_pol(xi, eta, SpectralBounds{lmin, lmax}, po);

@@ -61,6 +61,10 @@ def lib():
         L.ref_cheb_lan_pencil.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_int, C.c_double,
                                           C.c_double, C.c_double, C.c_double, C.c_int, C.c_double,
                                           C.c_int, C.c_uint64]
+        L.ref_cheb_lan_pencil_csr.restype = C.c_void_p
+        L.ref_cheb_lan_pencil_csr.argtypes = [C.c_int, _ip, _ip, _dp, _ip, _ip, _dp, C.c_int,
+                                              C.c_double, C.c_double, C.c_double, C.c_double,
+                                              C.c_int, C.c_double, C.c_int, C.c_uint64]
         L.ref_solve.restype = C.c_void_p
         L.ref_solve.argtypes = [C.c_int, _ip, _ip, _dp, C.c_double, C.c_double, C.c_int, C.c_int,
                                 C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
@@ -362,3 +366,59 @@ def solve(rp, ci, v, xi, eta, ns, solver="nr", damping="sigma", dos_m=60, dos_nv
     if not h:
         raise RefError(lib().ref_last_error().decode())
     return _collect(h, True)
+
+
+# ---- general SPD-B pencils (the reference's Cholesky-backed path) --------------------------------
+def ls_pol_approx(fun, lmin, lmax, tol, max_deg=300):
+    """cheb_approx.hpp:40-88.  fun: "inverse" | "inverse_sqrt".  Returns (coeff, achieved)."""
+    cap = max_deg + 1
+    co = np.empty(cap, np.float64)
+    deg, ach = C.c_int(), C.c_double()
+    _chk(lib().ref_ls_pol_approx(C.c_int(1 if fun == "inverse_sqrt" else 0), C.c_double(lmin),
+                                 C.c_double(lmax), C.c_double(tol), C.c_int(max_deg), C.c_int(cap),
+                                 C.byref(deg), co.ctypes.data_as(_PD), C.byref(ach)))
+    return co[: deg.value + 1].copy(), ach.value
+
+
+def apply_cheb(rp, ci, v, fun, lmin, lmax, coeff, x):
+    """cheb_approx.hpp:91-112: y = p(B) x."""
+    coeff = np.ascontiguousarray(coeff, np.float64)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    _chk(lib().ref_apply_cheb(*_csr_args(rp, ci, v), C.c_int(1 if fun == "inverse_sqrt" else 0),
+                              C.c_double(lmin), C.c_double(lmax), C.c_int(coeff.size - 1),
+                              coeff.ctypes.data_as(_PD), x.ctypes.data_as(_PD), y.ctypes.data_as(_PD)))
+    return y
+
+
+def _csr_b(brp, bci, bv):
+    return (brp.ctypes.data_as(_PI), bci.ctypes.data_as(_PI), bv.ctypes.data_as(_PD))
+
+
+def pencil_bounds(rp, ci, v, brp, bci, bv, seed=1234):
+    lo, hi = C.c_double(), C.c_double()
+    _chk(lib().ref_pencil_bounds(*_csr_args(rp, ci, v), *_csr_b(brp, bci, bv), C.c_uint64(seed),
+                                 C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def pencil_dos(rp, ci, v, brp, bci, bv, lmin, lmax, m=60, n_vec=40, npts=300, seed=1234):
+    x = np.empty(npts, np.float64)
+    y = np.empty(npts, np.float64)
+    nev = C.c_double()
+    _chk(lib().ref_pencil_dos(*_csr_args(rp, ci, v), *_csr_b(brp, bci, bv), C.c_double(lmin),
+                              C.c_double(lmax), C.c_int(m), C.c_int(n_vec), C.c_int(npts),
+                              C.c_uint64(seed), x.ctypes.data_as(_PD), y.ctypes.data_as(_PD),
+                              C.byref(nev)))
+    return x, y, nev.value
+
+
+def cheb_lan_pencil_csr(rp, ci, v, brp, bci, bv, solver, xi, eta, lmin, lmax, damping="sigma",
+                        res_tol=1e-8, est_count=20, seed=1234):
+    """The reference's B-weighted cheb_lan_nr/tr/cheb_si on (A, B), B a general sparse SPD CSR
+    (Cholesky-backed B-solves, eigensolvers.hpp:640-732)."""
+    h = lib().ref_cheb_lan_pencil_csr(len(rp) - 1, rp, ci, v, brp, bci, bv, SOLVER[solver], xi, eta,
+                                      lmin, lmax, DAMPING[damping], res_tol, est_count, seed)
+    if not h:
+        raise RefError(lib().ref_last_error().decode())
+    return _collect(h, False)["slices"][0]

@@ -855,6 +855,7 @@ int se_paired_cgs2(se_ctx* ctx, int n, int kq, const double* W, double* t, doubl
     try {
       SE_CUDA(cudaMemcpyAsync(dcm, W, sizeof(double) * (size_t)n * kq, cudaMemcpyHostToDevice, c.stream));
       SE_CUDA(cudaMemcpyAsync(dt, t, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      SE_CUDA(cudaMemsetAsync(dW, 0, sizeof(double) * (size_t)n * ldw, c.stream));
       k::rw_put_cols(c, n, dW, ldw, 0, kq, dcm, n, nullptr);
       Ctl z{};
       z.i = kq - 1;  // columns 0..i

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <limits>
+#include <map>
 #include <numeric>
 
 namespace se {
@@ -34,6 +35,9 @@ void rowbasis_reserve(Ctx& c, RowBasis& w, int n, int cols, bool keep) {
   if (w.p && w.n == n && w.cap >= cols) return;
   const int ld = k::rw_ldw(cols);
   double* p = dev_alloc<double>((size_t)n * ld);
+  // zero once: the CGS2 kernels read whole column pairs, so a never-written pad column must
+  // hold a finite value (it is multiplied by a zero coefficient)
+  SE_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)n * ld, c.stream));
   if (keep && w.p && w.cap > 0)  // re-stride the kept rows
     SE_CUDA(cudaMemcpy2DAsync(p, sizeof(double) * ld, w.p, sizeof(double) * w.ld,
                               sizeof(double) * w.ld, n, cudaMemcpyDeviceToDevice, c.stream));
@@ -68,9 +72,13 @@ struct Krylov {
   double* rbuf = nullptr;
   int* idx = nullptr;  // column indices for thick-restart copies
   int idx_cap = 0;
-  cudaGraphExec_t gexec = nullptr;
-  int gnodes = 0;
-  int gmode = -1;
+  // one captured step graph per (mode, CGS2 geometry class of the step's column count)
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    int nodes = 0;
+  };
+  std::map<std::pair<int, int>, StepGraph> graphs;
+  int host_i = 0;  // the column the next step filters (host mirror of ctl->i)
   int nlock = 0;
 
   double* mu_dev = nullptr;
@@ -90,7 +98,7 @@ struct Krylov {
   }
   ~Krylov() {
     cudaStreamSynchronize(c.stream);
-    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
     dev_free(W.p);
     devmat_free(L);
     dev_free(mu_dev);
@@ -102,12 +110,9 @@ struct Krylov {
   }
 
   void drop_graph() {
-    if (gexec) {
-      ctx_sync(c);
-      cudaGraphExecDestroy(gexec);
-    }
-    gexec = nullptr;
-    gmode = -1;
+    if (!graphs.empty()) ctx_sync(c);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
+    graphs.clear();
   }
 
   // Capacity for `wcols` basis columns and `lcols` locked columns; pointers baked into the step
@@ -179,6 +184,7 @@ struct Krylov {
     ctx_sync(c);
   }
   void begin(int i0) {  // new recurrence segment starting at column i0
+    host_i = i0;
     Ctl h = get();
     h.i = i0;
     h.halted = 0;
@@ -239,7 +245,7 @@ struct Krylov {
 
   // One Lanczos step.  mode 0: NR recurrence (eigensolvers.hpp:406-433 / lanczos.hpp:151-185);
   // mode 1: TR projection with h accumulation (eigensolvers.hpp:524-556 / lanczos.hpp:284-311).
-  void record_step(int mode) {
+  void record_step(int mode, int cls) {
     k::stamp(c, ctl, 0);
     record_filter();
     k::stamp(c, ctl, 1);
@@ -249,35 +255,49 @@ struct Krylov {
       k::rw_nr_sub_alpha(c, s, n, t, W.p, W.ld, ctl);
     }
     // CGS2 against W[:, 0..i] with three reads of W (TR: the T1 pass also takes ||t||)
-    k::rw_cgs2(c, rs, n, t, W.p, W.ld, ctl, mode == 1 ? hdiag : nullptr, coef, coef2, mode == 1);
+    k::rw_cgs2(c, rs, n, t, W.p, W.ld, ctl, mode == 1 ? hdiag : nullptr, coef, coef2, mode == 1,
+               cls);
     k::rw_normalize(c, s.cnt, n, t, W.p, W.ld, ctl, beta);
     k::stamp(c, ctl, 2);
   }
 
-  void run(int mode, int count) {
-    if (count <= 0) return;
-    if (!gexec || gmode != mode) {
-      drop_graph();
-      const long before = c.launches;
-      SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
-      try {
-        record_step(mode);
-      } catch (...) {
-        cudaGraph_t g;
-        cudaStreamEndCapture(c.stream, &g);
-        if (g) cudaGraphDestroy(g);
-        throw;
-      }
-      cudaGraph_t g;
-      SE_CUDA(cudaStreamEndCapture(c.stream, &g));
-      SE_CUDA(cudaGraphInstantiate(&gexec, g, cudaGraphInstantiateFlagUseNodePriority));
-      cudaGraphDestroy(g);
-      gnodes = (int)(c.launches - before);
-      c.launches = before;
-      gmode = mode;
+  StepGraph& graph(int mode, int cls) {
+    StepGraph& g = graphs[{mode, cls}];
+    if (g.exec) return g;
+    const long before = c.launches;
+    SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      record_step(mode, cls);
+    } catch (...) {
+      cudaGraph_t gr;
+      cudaStreamEndCapture(c.stream, &gr);
+      if (gr) cudaGraphDestroy(gr);
+      graphs.erase({mode, cls});
+      throw;
     }
-    for (int q = 0; q < count; ++q) SE_CUDA(cudaGraphLaunch(gexec, c.stream));
-    c.launches += (long)gnodes * count;
+    cudaGraph_t gr;
+    SE_CUDA(cudaStreamEndCapture(c.stream, &gr));
+    SE_CUDA(cudaGraphInstantiate(&g.exec, gr, cudaGraphInstantiateFlagUseNodePriority));
+    cudaGraphDestroy(gr);
+    g.nodes = (int)(c.launches - before);
+    c.launches = before;
+    return g;
+  }
+
+  // `count` Lanczos steps from host_i on: each replays the graph of its column count's CGS2
+  // geometry class (the step at column i orthogonalises against i + 1 columns; a halted
+  // recurrence makes the remaining replays no-ops)
+  void run(int mode, int count) {
+    for (int q = 0; q < count;) {
+      const int cls = k::rw_class(std::min(host_i + q + 1, W.cap));
+      int span = 1;
+      while (q + span < count && k::rw_class(std::min(host_i + q + span + 1, W.cap)) == cls) ++span;
+      StepGraph& g = graph(mode, cls);
+      for (int r = 0; r < span; ++r) SE_CUDA(cudaGraphLaunch(g.exec, c.stream));
+      c.launches += (long)g.nodes * span;
+      q += span;
+    }
+    host_i += count;
   }
 
   double dot(const double* x, const double* y) {
@@ -568,7 +588,9 @@ struct Slice {
     const Ctl hc = kr.get();
     r->orth_passes = hc.passes_total;
     r->orth_cols = hc.cols_total;
-    r->orth_bytes = 16.0 * A.n * (double)hc.cols_total + 24.0 * A.n * (double)hc.passes_total;
+    // bytes the CGS2 steps moved: every streamed basis column (8 n each: T1 + MID + N2 reads)
+    // plus the vector traffic (T1 reads t, MID and N2 read and write it: 8 + 16 + 16 n)
+    r->orth_bytes = 8.0 * A.n * (double)hc.reads_cols + 40.0 * A.n * (double)hc.passes_total;
     return r;
   }
 

@@ -24,7 +24,8 @@ struct Ctl {
   unsigned long long ts0, ts1;  // %globaltimer stamps (ns) for the Counters timers
   double t_mv_ns, t_orth_ns;    // accumulated filter / orthogonalisation device time
   long long passes_total;       // CGS passes executed (DGKS statistics)
-  long long cols_total;         // basis columns summed over those passes (bytes: 16 n per column)
+  long long cols_total;         // basis columns summed over those passes
+  long long reads_cols;         // basis columns streamed from HBM (row-major CGS2: T1 + MID + N2)
 };
 
 namespace k {
@@ -124,11 +125,9 @@ void gemvn_only(Ctx& c, const Scratch& s, int n, double* t, const double* Q, boo
                 const double* coef, int cap);
 // ---- row-major Krylov basis (rowgs.cu) --------------------------------------------------------
 // The Lanczos basis W is row-major, W[r * ldw + j] with ldw = rw_ldw(capacity) (even, so every row
-// is a 16-byte aligned run a TMA bulk copy can stage).  One CGS2 step = T1 (coef1 = W^T t), MID
+// is a 16-byte aligned run of column pairs).  One CGS2 step = T1 (coef1 = W^T t), MID
 // (t1 = t - W coef1, ||t1||, DGKS flag, coef2 = W^T t1 from the same staged rows) and N2 (t -= W
 // coef2, only when re-passed): three reads of W instead of four.
-constexpr size_t kRwMaxSmem = 227 * 1024;   // dynamic shared memory per CTA (sm_100a limit)
-constexpr size_t kRwSmemPerSm = 228 * 1024;
 struct RowScratch {
   double* part = nullptr;   // grid x ldw per-CTA coefficient partials
   double* npart = nullptr;  // grid per-CTA sums of squares
@@ -142,8 +141,11 @@ void rw_bind(RowScratch& s, double* buf);              // buf: rw_scratch_double
 // CGS2 of t against W[:, 0..ctl->i] (orth.hpp:63-80): coef1/coef2 (>= ldw doubles) receive the
 // two passes' coefficients, hdiag[i] += c (TR, eigensolvers.hpp:534) when non-null; want_before:
 // the T1 pass also sets before = after = ||t|| and resets the DGKS flags (TR's step).
+// cls: the geometry class (rw_class) of the largest column count the launches will see (-1:
+// the capacity's); the kernels handle any count up to it.
 void rw_cgs2(Ctx& c, const RowScratch& s, int n, double* t, const double* W, int ldw, Ctl* ctl,
-             double* hdiag, double* coef1, double* coef2, bool want_before);
+             double* hdiag, double* coef1, double* coef2, bool want_before, int cls = -1);
+int rw_class(int ncols);
 // dst = W[:, ctl->i + off] (contiguous copy of the step's source column)
 void rw_col_get(Ctx& c, int n, const double* W, int ldw, const Ctl* ctl, int off, double* dst);
 // beta = after; breakdown -> halted; else W[:, i+1] = t / beta, beta_arr[i] = beta, i++.

@@ -2,26 +2,25 @@
 // orth.hpp:19-80 cgs_pass / paired_cgs2, eigensolvers.hpp:406-433 / 524-556 for the step).
 //
 // Layout: the Lanczos basis W is stored ROW-major, W[r * ldw + j] (ldw = column capacity, even),
-// so one row of the active basis (columns 0..i) is a single contiguous run of 8 (i+1) bytes.
-// That makes every row block of W one TMA bulk copy (cp.async.bulk, 1-D) straight into shared
-// memory, and lets the middle of CGS2 use each staged row block twice:
+// so one row of the active basis (columns 0..i) is a single contiguous run of 8 (i+1) bytes and
+// a block of rows can be held by a CTA in registers.  That lets the middle of CGS2 use each row
+// block twice from ONE read:
 //
 //   T1  : coef1 = W^T t                    (and ||t|| for the TR step)          one read of W
-//   MID : t1 = t - W coef1, ||t1||, coef2 = W^T t1   (same staged rows)         one read of W
+//   MID : t1 = t - W coef1, ||t1||, coef2 = W^T t1   (same rows, registers)     one read of W
 //   N2  : t2 = t1 - W coef2, ||t2||        (only when the DGKS test asks, orth.hpp:76-78)
 //
-// i.e. three reads of W per re-passed CGS2 step instead of four, and two when no re-pass is
-// needed (coef2 is then simply discarded).  Each streaming kernel is persistent (a fixed grid,
-// row blocks dealt round-robin), stages R rows per block through an S-deep ring of bulk copies,
-// and gives every thread a fixed set of columns (j = tid + 256 q) whose coefficient and partial
-// sums live in registers.  All reductions have a fixed order (thread columns -> warp xor tree ->
-// warps in order; CTA partials in CTA order), so reruns are bitwise identical.
+// i.e. three reads of W per re-passed CGS2 step instead of the four of two column-major passes,
+// and two when no re-pass is needed (coef2 is then simply discarded).  A TMA-staged variant
+// (cp.async.bulk row copies into a shared-memory mbarrier ring) was measured first and lost to
+// the register-direct kernel at every basis width (profiles/r2_ncu_summary.md).
 //
 // The basis is written one column at a time (k_rw_normalize: W[:, i+1] = t / beta) and read one
 // column at a time by the filter (k_rw_col_get): strided 8-byte accesses, ~4 n sectors per step,
 // negligible next to the 8 n (i+1) bytes of each pass.
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -33,8 +32,7 @@ namespace {
 constexpr double kEta = 0.70710678118654752;  // DGKS threshold, orth.hpp:13
 constexpr int kRT = 256;                      // threads per streaming CTA
 constexpr int kRW = kRT / 32;
-constexpr int kRR = 2;                        // rows per staged block
-constexpr int kRS = 2;                        // ring stages
+constexpr int kRwPerSm = 2;                   // resident streaming CTAs per SM (persistent grid)
 constexpr int kFinCols = 32;                  // columns per finishing CTA (8 threads each)
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -46,151 +44,106 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void bar_init(unsigned long long* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void bar_arm(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred done;\n RW_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
-      " @!done bra RW_WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-// one contiguous global run -> shared memory, completion counted on `bar` (TMA bulk copy)
-__device__ __forceinline__ void row_copy(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
 enum RwPhase { kT = 0, kMid = 1, kN = 2 };
 
 // The streaming pass.  PH = kT: part[g][j] = sum over this CTA's rows of W[r, j] t[r];
 // npart[g] = sum t[r]^2.  PH = kMid: t[r] -= W[r, :] coef (written back), npart = sum t1^2,
 // part = W^T t1 partials.  PH = kN (only when ctl->repass): t[r] -= W[r, :] coef, npart.
-template <int PH, int QMAX>
-__global__ void __launch_bounds__(kRT) k_rw_stream(int n, const double* __restrict__ W, int ldw,
-                                                   double* __restrict__ t, const Ctl* ctl,
-                                                   const double* __restrict__ coef,
-                                                   double* __restrict__ part,
-                                                   double* __restrict__ npart) {
+//
+// Row blocks of R rows are dealt round-robin over a persistent grid (2 CTAs per SM).  Every
+// thread owns the column PAIRS j2 = tid + 256 q (q < QP) and loads them for the block's R rows
+// straight into registers -- R x QP independent 16-byte streaming loads in flight per thread,
+// ~100 KB per SM -- then uses the same registers for the row dots W[r, :] coef (MID / N) and for
+// the W^T x partial sums (T / MID): one read of the row block serves both halves of the fused
+// step.  Coefficients and partials live in registers; the row dots are reduced by the warp xor
+// tree and then over the warps in order, so the sums are deterministic.
+template <int PH, int QP, int R>
+__global__ void __launch_bounds__(kRT, 2) k_rw_stream(int n, const double* __restrict__ W, int ldw,
+                                                      double* __restrict__ t, const Ctl* ctl,
+                                                      const double* __restrict__ coef,
+                                                      double* __restrict__ part,
+                                                      double* __restrict__ npart, int) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (ctl->halted) return;
   if (PH == kN && !ctl->repass) return;
   const int ncols = ctl->i + 1;
-  const int nblk = (n + kRR - 1) / kRR;
-  const unsigned row_bytes = (unsigned)(((ncols + 1) & ~1) * (int)sizeof(double));
-  extern __shared__ __align__(128) double ring[];  // [kRS][kRR][ldw]
-  __shared__ __align__(8) unsigned long long full[kRS];
-  __shared__ double s_red[kRW][kRR];
-  __shared__ double s_x[kRR];
+  const int np = (ncols + 1) >> 1;
+  const int nblk = (n + R - 1) / R;
+  __shared__ double s_red[kRW][R];
+  __shared__ double s_x[R];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  double cr[QMAX], acc[QMAX];
+  double2 cr[QP], acc[QP];
 #pragma unroll
-  for (int q = 0; q < QMAX; ++q) {
-    const int j = tid + kRT * q;
-    cr[q] = (PH != kT && j < ncols) ? coef[j] : 0.0;
-    acc[q] = 0.0;
-  }
-  if (tid == 0) {
-    for (int s = 0; s < kRS; ++s) bar_init(&full[s]);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int s, int b) {  // thread 0: stage row block b into ring stage s
-    const int r0 = b * kRR, rows = min(kRR, n - r0);
-    bar_arm(&full[s], rows * row_bytes);
-    for (int r = 0; r < rows; ++r)
-      row_copy(ring + ((size_t)s * kRR + r) * ldw, W + (size_t)(r0 + r) * ldw, row_bytes, &full[s]);
-  };
-  if (tid == 0)
-    for (int s = 0; s < kRS; ++s) {
-      const int b = blockIdx.x + s * gridDim.x;
-      if (b < nblk) issue(s, b);
+  for (int q = 0; q < QP; ++q) {
+    const int j2 = tid + kRT * q;
+    cr[q] = make_double2(0.0, 0.0);
+    if (PH != kT && j2 < np) {
+      cr[q].x = coef[2 * j2];
+      cr[q].y = 2 * j2 + 1 < ncols ? coef[2 * j2 + 1] : 0.0;
     }
-  double nrm = 0.0;  // thread 0: this CTA's sum of squares, in block order
-  int it = 0;
-  for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
-    const int s = it % kRS;
-    const int r0 = b * kRR, rows = min(kRR, n - r0);
-    bar_wait(&full[s], (unsigned)((it / kRS) & 1));
-    const double* st = ring + (size_t)s * kRR * ldw;
-    double x[kRR];
+    acc[q] = make_double2(0.0, 0.0);
+  }
+  double nrm = 0.0;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int r0 = b * R, rows = min(R, n - r0);
+    double2 w[R][QP];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int j2 = tid + kRT * q;
+        w[r][q] = (r < rows && j2 < np)
+                      ? __ldcs(reinterpret_cast<const double2*>(W + (size_t)(r0 + r) * ldw) + j2)
+                      : make_double2(0.0, 0.0);
+      }
+    double x[R];
     if (PH == kT) {
 #pragma unroll
-      for (int r = 0; r < kRR; ++r) x[r] = r < rows ? t[r0 + r] : 0.0;
+      for (int r = 0; r < R; ++r) x[r] = r < rows ? t[r0 + r] : 0.0;
     } else {
-      // row dots W[r, :] coef over this thread's columns, then the block tree
-      double p[kRR];
+      double p[R];
 #pragma unroll
-      for (int r = 0; r < kRR; ++r) p[r] = 0.0;
+      for (int r = 0; r < R; ++r) {
+        p[r] = 0.0;
 #pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        const int j = tid + kRT * q;
-        if (j < ncols) {
-#pragma unroll
-          for (int r = 0; r < kRR; ++r) p[r] = add(p[r], mul(st[r * ldw + j], cr[q]));
-        }
+        for (int q = 0; q < QP; ++q) p[r] = fma(w[r][q].y, cr[q].y, fma(w[r][q].x, cr[q].x, p[r]));
+        p[r] = warp_sum(p[r]);
       }
-#pragma unroll
-      for (int r = 0; r < kRR; ++r) p[r] = warp_sum(p[r]);
       if (lane == 0)
 #pragma unroll
-        for (int r = 0; r < kRR; ++r) s_red[warp][r] = p[r];
+        for (int r = 0; r < R; ++r) s_red[warp][r] = p[r];
       __syncthreads();
       if (tid < rows) {
         double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < kRW; ++w) sum = add(sum, s_red[w][tid]);
+        for (int v = 0; v < kRW; ++v) sum = add(sum, s_red[v][tid]);
         const double xr = sub(t[r0 + tid], sum);
         t[r0 + tid] = xr;
         s_x[tid] = xr;
       }
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < kRR; ++r) x[r] = r < rows ? s_x[r] : 0.0;
+      for (int r = 0; r < R; ++r) x[r] = r < rows ? s_x[r] : 0.0;
     }
     if (tid == 0)
-      for (int r = 0; r < rows; ++r) nrm = add(nrm, mul(x[r], x[r]));
+      for (int r = 0; r < rows; ++r) nrm = fma(x[r], x[r], nrm);
     if (PH != kN) {
 #pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        const int j = tid + kRT * q;
-        if (j < ncols) {
+      for (int q = 0; q < QP; ++q)
 #pragma unroll
-          for (int r = 0; r < kRR; ++r)
-            if (r < rows) acc[q] = add(acc[q], mul(st[r * ldw + j], x[r]));
+        for (int r = 0; r < R; ++r) {
+          acc[q].x = fma(w[r][q].x, x[r], acc[q].x);
+          acc[q].y = fma(w[r][q].y, x[r], acc[q].y);
         }
-      }
-    }
-    __syncthreads();  // stage s fully consumed (and s_x / s_red free)
-    if (tid == 0) {
-      const int nb = b + kRS * gridDim.x;
-      if (nb < nblk) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue(s, nb);
-      }
     }
   }
   if (PH != kN) {
 #pragma unroll
-    for (int q = 0; q < QMAX; ++q) {
-      const int j = tid + kRT * q;
-      if (j < ncols) part[(size_t)blockIdx.x * ldw + j] = acc[q];
+    for (int q = 0; q < QP; ++q) {
+      const int j2 = tid + kRT * q;
+      if (2 * j2 < ncols) part[(size_t)blockIdx.x * ldw + 2 * j2] = acc[q].x;
+      if (2 * j2 + 1 < ncols) part[(size_t)blockIdx.x * ldw + 2 * j2 + 1] = acc[q].y;
     }
   }
   if (tid == 0) npart[blockIdx.x] = nrm;
@@ -237,6 +190,7 @@ __global__ void __launch_bounds__(kRT) k_rw_finish(int G, int ldw, const double*
       ctl->npass += 1;
       ctl->passes_total += 1;
       ctl->cols_total += ncols;
+      ctl->reads_cols += ncols;
     }
     return;
   }
@@ -253,6 +207,7 @@ __global__ void __launch_bounds__(kRT) k_rw_finish(int G, int ldw, const double*
     if (hdiag && j == icol && (PH == kT || repass)) hdiag[j] = add(hdiag[j], q);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->reads_cols += ncols;
     if (PH == kT) {
       if (want_before) {
         ctl->before = nrm;
@@ -454,38 +409,46 @@ void launch_pdl(const Ctx& c, K kern, dim3 grid, dim3 block, size_t smem, Args..
 
 int grid_small(const Ctx& c, int n) { return std::max(1, std::min(c.num_sms * 4, (n + kRT - 1) / kRT)); }
 
-size_t ring_bytes(int ldw) { return sizeof(double) * (size_t)kRS * kRR * ldw; }
+// Geometry per basis capacity (ldw): rows per block R and column pairs per thread QP, so a
+// thread keeps ~16 pairs (R x QP) in flight whatever the width.
+struct Geometry {
+  int R = 1, QP = 1;
+};
+// Geometry classes by the active column count (padded to even): class g serves ncols <=
+// kClassLim[g] with R rows per block and QP column pairs per thread, so a thread keeps ~8-16
+// pairs in flight whatever the width.  The Lanczos step graph is captured once per class.
+constexpr int kNumClasses = 11;
+constexpr int kClassLim[kNumClasses] = {416, 512, 832, 1024, 1664, 2048, 3072, 3328, 4096, 6144, 8192};
+constexpr int kClassR[kNumClasses] = {16, 8, 8, 4, 4, 2, 2, 2, 1, 1, 1};
+constexpr int kClassQP[kNumClasses] = {1, 1, 2, 2, 4, 4, 6, 8, 8, 12, 16};
 
-// register columns per thread for a capacity (template instance)
+Geometry geometry_of_class(int g) { return {kClassR[g], kClassQP[g]}; }
+
+template <int PH, int QP, int R>
+void stream_one(Ctx& c, const RowScratch& s, int n, const double* W, int ldw, double* t,
+                const Ctl* ctl, const double* coef) {
+  launch_pdl(c, k_rw_stream<PH, QP, R>, dim3(s.grid), dim3(kRT), 0, n, W, ldw, t, ctl, coef,
+             s.part, s.npart, 0);
+  ++c.launches;
+}
+
 template <int PH>
 void stream_launch(Ctx& c, const RowScratch& s, int n, const double* W, int ldw, double* t,
-                   const Ctl* ctl, const double* coef) {
-  const size_t smem = ring_bytes(ldw);
-  const dim3 grid(s.grid), block(kRT);
-  const int q = (ldw + kRT - 1) / kRT;
-#define SE_RW_CASE(QM)                                                                             \
-  if (q <= QM) {                                                                                   \
-    static std::atomic<unsigned long long> attr_set{0};  /* one bit per device */              \
-    const unsigned long long bit = 1ull << (c.device & 63);                                        \
-    if (!(attr_set.load() & bit)) {                                                                \
-      SE_CUDA(cudaFuncSetAttribute(k_rw_stream<PH, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   (int)kRwMaxSmem));                                               \
-      attr_set.fetch_or(bit);                                                                      \
-    }                                                                                              \
-    launch_pdl(c, k_rw_stream<PH, QM>, grid, block, smem, n, W, ldw, t, ctl, coef, s.part, s.npart); \
-    ++c.launches;                                                                                  \
-    return;                                                                                        \
+                   const Ctl* ctl, const double* coef, int cls) {
+  const Geometry g = geometry_of_class(cls);
+  switch (g.QP * 100 + g.R) {
+    case 116: return stream_one<PH, 1, 16>(c, s, n, W, ldw, t, ctl, coef);
+    case 108: return stream_one<PH, 1, 8>(c, s, n, W, ldw, t, ctl, coef);
+    case 208: return stream_one<PH, 2, 8>(c, s, n, W, ldw, t, ctl, coef);
+    case 204: return stream_one<PH, 2, 4>(c, s, n, W, ldw, t, ctl, coef);
+    case 404: return stream_one<PH, 4, 4>(c, s, n, W, ldw, t, ctl, coef);
+    case 402: return stream_one<PH, 4, 2>(c, s, n, W, ldw, t, ctl, coef);
+    case 602: return stream_one<PH, 6, 2>(c, s, n, W, ldw, t, ctl, coef);
+    case 802: return stream_one<PH, 8, 2>(c, s, n, W, ldw, t, ctl, coef);
+    case 801: return stream_one<PH, 8, 1>(c, s, n, W, ldw, t, ctl, coef);
+    case 1201: return stream_one<PH, 12, 1>(c, s, n, W, ldw, t, ctl, coef);
+    default: return stream_one<PH, 16, 1>(c, s, n, W, ldw, t, ctl, coef);
   }
-  SE_RW_CASE(2)
-  SE_RW_CASE(4)
-  SE_RW_CASE(8)
-  SE_RW_CASE(12)
-  SE_RW_CASE(16)
-  SE_RW_CASE(20)
-  SE_RW_CASE(24)
-  SE_RW_CASE(32)
-#undef SE_RW_CASE
-  fail(SE_EINVAL, "row-major Krylov basis: capacity beyond 8192 columns");
 }
 
 template <int PH>
@@ -503,10 +466,9 @@ int rw_ldw(int cols) { return std::max(2, (cols + 1) & ~1); }
 
 RowScratch rw_scratch(const Ctx& c, int ldw) {
   RowScratch s;
-  const size_t smem = ring_bytes(ldw);
-  if (smem > kRwMaxSmem) fail(SE_EINVAL, "row-major Krylov basis: capacity beyond 8192 columns");
-  const int per_sm = std::max(1, std::min(2, (int)(kRwSmemPerSm / (smem + 2048))));
-  s.grid = c.num_sms * per_sm;
+  if (ldw > kClassLim[kNumClasses - 1])
+    fail(SE_EINVAL, "row-major Krylov basis: capacity beyond 8192 columns");
+  s.grid = c.num_sms * kRwPerSm;
   s.ldw = ldw;
   return s;
 }
@@ -516,13 +478,21 @@ void rw_bind(RowScratch& s, double* buf) {
   s.npart = buf + (size_t)s.grid * s.ldw;
 }
 
+int rw_class(int ncols) {
+  const int pad = (ncols + 1) & ~1;
+  for (int g = 0; g < kNumClasses; ++g)
+    if (pad <= kClassLim[g]) return g;
+  fail(SE_EINVAL, "row-major Krylov basis: more than 8192 columns");
+}
+
 void rw_cgs2(Ctx& c, const RowScratch& s, int n, double* t, const double* W, int ldw, Ctl* ctl,
-             double* hdiag, double* coef1, double* coef2, bool want_before) {
-  stream_launch<kT>(c, s, n, W, ldw, t, ctl, nullptr);
+             double* hdiag, double* coef1, double* coef2, bool want_before, int cls) {
+  if (cls < 0) cls = rw_class(ldw);
+  stream_launch<kT>(c, s, n, W, ldw, t, ctl, nullptr, cls);
   finish_launch<kT>(c, s, ldw, ctl, coef1, hdiag, want_before ? 1 : 0);
-  stream_launch<kMid>(c, s, n, W, ldw, t, ctl, coef1);
+  stream_launch<kMid>(c, s, n, W, ldw, t, ctl, coef1, cls);
   finish_launch<kMid>(c, s, ldw, ctl, coef2, hdiag, 0);
-  stream_launch<kN>(c, s, n, W, ldw, t, ctl, coef2);
+  stream_launch<kN>(c, s, n, W, ldw, t, ctl, coef2, cls);
   finish_launch<kN>(c, s, ldw, ctl, nullptr, nullptr, 0);
 }
 

@@ -74,6 +74,11 @@ def test_cfg2_kpm_gaussian_moments_and_breakpoints(gpu_ctx, golden):
 
 
 @pytest.mark.slow
+def _golden(name):
+    import os
+    return dict(np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz")))
+
+
 def test_cfg2_full_pipeline_exact_counts(gpu_ctx):
     """BASELINE configs[1] end to end on one GPU: every slice returns exactly the analytic
     eigenvalues (counts identical, |dlambda| <= 1e-10 |lambda|)."""
@@ -93,6 +98,19 @@ def test_cfg2_full_pipeline_exact_counts(gpu_ctx):
         assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
         total += truth.size
     assert total == api.count_in_interval(ev, 0.6, 1.2) == 4120
+    # ... and the reference's own full cfg2 run (oracle/_ref, 8 slice threads, 2.2 h on the build
+    # container's CPU: tests/golden/cfg2_solve.npz from profiles/r2_cpu_reference_cfg2.json):
+    # identical breakpoints, per-slice counts, eigenvalues within 1e-10 relative, and the same
+    # filter degrees; iteration counts within one 30-step check cycle
+    g = _golden("cfg2_solve")
+    assert np.allclose(res.breakpoints, g["bp"], rtol=0, atol=1e-12)
+    for s in res.slices:
+        ref = g[f"slice{s.index}_vals"]
+        niter, _, degree, hit = g[f"slice{s.index}_meta"]
+        assert s.eigenvalues.size == ref.size, (s.index, s.eigenvalues.size, ref.size)
+        assert np.all(np.abs(s.eigenvalues - ref) <= 1e-10 * np.abs(ref))
+        assert s.degree == degree and not hit
+        assert abs(s.niter - niter) <= 30, (s.index, s.niter, niter)
 
 
 def test_kpm_dos_bitwise_rerun_and_validation(gpu_ctx):
