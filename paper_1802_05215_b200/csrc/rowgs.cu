@@ -70,8 +70,7 @@ __global__ void __launch_bounds__(kRT, 2) k_rw_stream(int n, const double* __res
   const int ncols = ctl->i + 1;
   const int np = (ncols + 1) >> 1;
   const int nblk = (n + R - 1) / R;
-  __shared__ double s_red[kRW][R];
-  __shared__ double s_x[R];
+  __shared__ double s_red[2][kRW][R];  // double-buffered: one barrier per row block
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double2 cr[QP], acc[QP];
 #pragma unroll
@@ -85,7 +84,8 @@ __global__ void __launch_bounds__(kRT, 2) k_rw_stream(int n, const double* __res
     acc[q] = make_double2(0.0, 0.0);
   }
   double nrm = 0.0;
-  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+  int it = 0;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
     const int r0 = b * R, rows = min(R, n - r0);
     double2 w[R][QP];
 #pragma unroll
@@ -97,34 +97,33 @@ __global__ void __launch_bounds__(kRT, 2) k_rw_stream(int n, const double* __res
                       ? __ldcs(reinterpret_cast<const double2*>(W + (size_t)(r0 + r) * ldw) + j2)
                       : make_double2(0.0, 0.0);
       }
+    // the block's t rows, read by every thread before anything is written back
     double x[R];
-    if (PH == kT) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[r] = r < rows ? t[r0 + r] : 0.0;
-    } else {
-      double p[R];
+    for (int r = 0; r < R; ++r) x[r] = r < rows ? t[r0 + r] : 0.0;
+    if (PH != kT) {
+      // row dots W[r, :] coef: own pairs, warp xor tree, then the warps in order (every thread
+      // forms the same sums from the shared partials)
+      double (*red)[R] = s_red[it & 1];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        p[r] = 0.0;
+        double p = 0.0;
 #pragma unroll
-        for (int q = 0; q < QP; ++q) p[r] = fma(w[r][q].y, cr[q].y, fma(w[r][q].x, cr[q].x, p[r]));
-        p[r] = warp_sum(p[r]);
+        for (int q = 0; q < QP; ++q) p = fma(w[r][q].y, cr[q].y, fma(w[r][q].x, cr[q].x, p));
+        p = warp_sum(p);
+        if (lane == 0) red[warp][r] = p;
       }
-      if (lane == 0)
-#pragma unroll
-        for (int r = 0; r < R; ++r) s_red[warp][r] = p[r];
       __syncthreads();
-      if (tid < rows) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
         double sum = 0.0;
 #pragma unroll
-        for (int v = 0; v < kRW; ++v) sum = add(sum, s_red[v][tid]);
-        const double xr = sub(t[r0 + tid], sum);
-        t[r0 + tid] = xr;
-        s_x[tid] = xr;
+        for (int v = 0; v < kRW; ++v) sum = add(sum, red[v][r]);
+        x[r] = r < rows ? sub(x[r], sum) : 0.0;
       }
-      __syncthreads();
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[r] = r < rows ? s_x[r] : 0.0;
+      for (int r = 0; r < R; ++r)
+        if (tid == r && r < rows) t[r0 + r] = x[r];
     }
     if (tid == 0)
       for (int r = 0; r < rows; ++r) nrm = fma(x[r], x[r], nrm);
@@ -147,6 +146,105 @@ __global__ void __launch_bounds__(kRT, 2) k_rw_stream(int n, const double* __res
     }
   }
   if (tid == 0) npart[blockIdx.x] = nrm;
+}
+
+// Narrow bases (<= 512 columns): a warp owns whole rows (lane = column pairs j2 = lane + 32 q),
+// so the row dots need only the warp's xor tree -- no CTA barrier in the loop -- and each warp
+// streams RW rows per iteration on its own.  Partial sums are per warp and combined over the
+// CTA's warps in order at the end, so the result is again deterministic.
+template <int PH, int Q, int RW>
+__global__ void __launch_bounds__(kRT, 2) k_rw_warp(int n, const double* __restrict__ W, int ldw,
+                                                    double* __restrict__ t, const Ctl* ctl,
+                                                    const double* __restrict__ coef,
+                                                    double* __restrict__ part,
+                                                    double* __restrict__ npart, int) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (ctl->halted) return;
+  if (PH == kN && !ctl->repass) return;
+  const int ncols = ctl->i + 1;
+  const int np = (ncols + 1) >> 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kRW + warp, nw = gridDim.x * kRW;  // global warp id / count
+  const int nblk = (n + RW - 1) / RW;
+  __shared__ double2 s_acc[kRW][Q * 32];
+  __shared__ double s_nrm[kRW];
+  double2 cr[Q], acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int j2 = lane + 32 * q;
+    cr[q] = make_double2(0.0, 0.0);
+    if (PH != kT && j2 < np) {
+      cr[q].x = coef[2 * j2];
+      cr[q].y = 2 * j2 + 1 < ncols ? coef[2 * j2 + 1] : 0.0;
+    }
+    acc[q] = make_double2(0.0, 0.0);
+  }
+  double nrm = 0.0;  // lane 0: this warp's sum of squares, in row order
+  for (int b = gw; b < nblk; b += nw) {
+    const int r0 = b * RW, rows = min(RW, n - r0);
+    double2 w[RW][Q];
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j2 = lane + 32 * q;
+        w[r][q] = (r < rows && j2 < np)
+                      ? __ldcs(reinterpret_cast<const double2*>(W + (size_t)(r0 + r) * ldw) + j2)
+                      : make_double2(0.0, 0.0);
+      }
+    double x[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) x[r] = r < rows ? t[r0 + r] : 0.0;
+    if (PH != kT) {
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        double p = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) p = fma(w[r][q].y, cr[q].y, fma(w[r][q].x, cr[q].x, p));
+        p = warp_sum(p);
+        x[r] = r < rows ? sub(x[r], p) : 0.0;
+      }
+      if (lane < rows) {
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+          if (lane == r) t[r0 + r] = x[r];
+      }
+    }
+    if (lane == 0)
+      for (int r = 0; r < rows; ++r) nrm = fma(x[r], x[r], nrm);
+    if (PH != kN) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+          acc[q].x = fma(w[r][q].x, x[r], acc[q].x);
+          acc[q].y = fma(w[r][q].y, x[r], acc[q].y);
+        }
+    }
+  }
+  // combine the CTA's warps in order
+  if (PH != kN)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) s_acc[warp][lane + 32 * q] = acc[q];
+  if (lane == 0) s_nrm[warp] = nrm;
+  __syncthreads();
+  if (PH != kN)
+    for (int j2 = threadIdx.x; j2 < np; j2 += kRT) {
+      double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int v = 0; v < kRW; ++v) {
+        a.x = add(a.x, s_acc[v][j2].x);
+        a.y = add(a.y, s_acc[v][j2].y);
+      }
+      if (2 * j2 < ncols) part[(size_t)blockIdx.x * ldw + 2 * j2] = a.x;
+      if (2 * j2 + 1 < ncols) part[(size_t)blockIdx.x * ldw + 2 * j2 + 1] = a.y;
+    }
+  if (threadIdx.x == 0) {
+    double q = 0.0;
+    for (int v = 0; v < kRW; ++v) q = add(q, s_nrm[v]);
+    npart[blockIdx.x] = q;
+  }
 }
 
 // sum of the G per-CTA squares, identical in every CTA (fixed thread assignment + tree)
@@ -417,10 +515,12 @@ struct Geometry {
 // Geometry classes by the active column count (padded to even): class g serves ncols <=
 // kClassLim[g] with R rows per block and QP column pairs per thread, so a thread keeps ~8-16
 // pairs in flight whatever the width.  The Lanczos step graph is captured once per class.
-constexpr int kNumClasses = 11;
-constexpr int kClassLim[kNumClasses] = {416, 512, 832, 1024, 1664, 2048, 3072, 3328, 4096, 6144, 8192};
-constexpr int kClassR[kNumClasses] = {16, 8, 8, 4, 4, 2, 2, 2, 1, 1, 1};
-constexpr int kClassQP[kNumClasses] = {1, 1, 2, 2, 4, 4, 6, 8, 8, 12, 16};
+constexpr int kNumClasses = 13;
+// classes 0-3: warp-per-row kernel (Q pairs per lane, RW rows per warp iteration); 4-: CTA rows
+constexpr int kClassLim[kNumClasses] = {64, 128, 256, 512, 832, 1024, 1664, 2048, 3072, 3328, 4096, 6144, 8192};
+constexpr int kClassR[kNumClasses] = {8, 8, 4, 1, 8, 4, 4, 2, 2, 2, 1, 1, 1};
+constexpr int kClassQP[kNumClasses] = {1, 2, 4, 8, 2, 2, 4, 4, 6, 8, 8, 12, 16};
+constexpr int kNumWarpClasses = 4;
 
 Geometry geometry_of_class(int g) { return {kClassR[g], kClassQP[g]}; }
 
@@ -432,13 +532,26 @@ void stream_one(Ctx& c, const RowScratch& s, int n, const double* W, int ldw, do
   ++c.launches;
 }
 
+template <int PH, int Q, int RW>
+void warp_one(Ctx& c, const RowScratch& s, int n, const double* W, int ldw, double* t,
+              const Ctl* ctl, const double* coef) {
+  launch_pdl(c, k_rw_warp<PH, Q, RW>, dim3(s.grid), dim3(kRT), 0, n, W, ldw, t, ctl, coef, s.part,
+             s.npart, 0);
+  ++c.launches;
+}
+
 template <int PH>
 void stream_launch(Ctx& c, const RowScratch& s, int n, const double* W, int ldw, double* t,
                    const Ctl* ctl, const double* coef, int cls) {
+  switch (cls) {
+    case 0: return warp_one<PH, 1, 8>(c, s, n, W, ldw, t, ctl, coef);
+    case 1: return warp_one<PH, 2, 8>(c, s, n, W, ldw, t, ctl, coef);
+    case 2: return warp_one<PH, 4, 4>(c, s, n, W, ldw, t, ctl, coef);
+    case 3: return warp_one<PH, 8, 1>(c, s, n, W, ldw, t, ctl, coef);
+    default: break;
+  }
   const Geometry g = geometry_of_class(cls);
   switch (g.QP * 100 + g.R) {
-    case 116: return stream_one<PH, 1, 16>(c, s, n, W, ldw, t, ctl, coef);
-    case 108: return stream_one<PH, 1, 8>(c, s, n, W, ldw, t, ctl, coef);
     case 208: return stream_one<PH, 2, 8>(c, s, n, W, ldw, t, ctl, coef);
     case 204: return stream_one<PH, 2, 4>(c, s, n, W, ldw, t, ctl, coef);
     case 404: return stream_one<PH, 4, 4>(c, s, n, W, ldw, t, ctl, coef);
