@@ -98,6 +98,10 @@ SE_API int se_device_memory(int device, size_t* free_bytes, size_t* total_bytes)
 
 /* ---- contexts ----------------------------------------------------------------------------- */
 SE_API int se_ctx_create(int device, se_ctx** out);
+/* Device bytes the Ritz-candidate evaluation of the drivers may hold at once (default 8 GB):
+ * larger candidate sets (eigensolvers.hpp:275-318 over thousands of Ritz vectors at n ~ 2M)
+ * are evaluated in column chunks and the thick-restart vectors recomputed once. */
+SE_API int se_ctx_set_candidate_budget(se_ctx* ctx, size_t bytes);
 SE_API int se_ctx_destroy(se_ctx* ctx);
 SE_API int se_ctx_synchronize(se_ctx* ctx);
 /* Number of this library's kernels launched on ctx so far (bench evidence). */

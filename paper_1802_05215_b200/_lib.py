@@ -52,6 +52,7 @@ _PL = C.POINTER(C.c_long)
 SIGNATURES = {
     "se_device_count": [_PI],
     "se_ctx_create": [C.c_int, C.POINTER(_VP)],
+    "se_ctx_set_candidate_budget": [_VP, C.c_size_t],
     "se_ctx_destroy": [_VP],
     "se_ctx_synchronize": [_VP],
     "se_ctx_kernel_launches": [_VP, _PL],

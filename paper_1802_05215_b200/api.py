@@ -48,6 +48,11 @@ class Context:
     def synchronize(self):
         call("se_ctx_synchronize", self.handle)
 
+    def set_candidate_budget(self, nbytes: int):
+        """Device bytes the drivers' Ritz-candidate evaluation may hold at once (default 8 GB);
+        larger candidate sets are evaluated in column chunks."""
+        call("se_ctx_set_candidate_budget", self.handle, int(nbytes))
+
     def kernel_launches(self) -> int:
         v = C.c_long()
         call("se_ctx_kernel_launches", self.handle, C.byref(v))

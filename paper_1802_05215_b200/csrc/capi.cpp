@@ -130,6 +130,13 @@ int se_device_count(int* count) {
 }
 
 // ---- contexts ------------------------------------------------------------------------------
+int se_ctx_set_candidate_budget(se_ctx* ctx, size_t bytes) {
+  return guard([&] {
+    if (bytes < 1) fail(SE_EINVAL, "se_ctx_set_candidate_budget: zero budget");
+    C(ctx).cand_budget = bytes;
+  });
+}
+
 int se_ctx_create(int device, se_ctx** out) {
   return guard([&] {
     *out = nullptr;

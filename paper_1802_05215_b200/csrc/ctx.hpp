@@ -22,6 +22,9 @@ struct Ctx {
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t solver = nullptr;
   long launches = 0;  // this library's kernel launches issued on `stream`
+  // device bytes the Ritz-candidate evaluation (U = W Y and A U) may hold at once; larger
+  // candidate sets are evaluated in column chunks (se_ctx_set_candidate_budget)
+  size_t cand_budget = (size_t)8 << 30;
 
   // Filter-kernel timing (bench roofline): events bracket each filter application.
   bool time_filter = false;

@@ -20,6 +20,10 @@ double now_s() {
 }
 
 int grow(int want) { return std::max(want, 16) + std::max(want, 16) / 2; }
+// Allocations above this size grow to the exact request instead of 1.5x (n ~ 2M: 16 MB a
+// column, so a 1.5x basis, locked set or candidate block would not fit next to the others).
+constexpr size_t kBigAlloc = (size_t)4 << 30;
+int grow_for(int n, int want) { return (size_t)n * want * 8 > kBigAlloc ? want : grow(want); }
 
 // ---- the Krylov basis: row-major (rowgs.cu) ----------------------------------------------------
 // W[r * ld + j], ld = rw_ldw(cap): each row of the active basis is one contiguous run, which is
@@ -115,16 +119,25 @@ struct Krylov {
     graphs.clear();
   }
 
+  // Locked-set capacity of exactly `cols` columns (large problems size it from the DOS estimate
+  // up front instead of growing by 1.5x).
+  void reserve_locked(int cols) {
+    if (cols <= L.cap) return;
+    devmat_reserve(c, L, n, cols, true);
+    drop_graph();
+    ensure(W.cap, cols);
+  }
+
   // Capacity for `wcols` basis columns and `lcols` locked columns; pointers baked into the step
   // graph change only here (then the graph is re-captured).
   void ensure(int wcols, int lcols) {
     bool dirty = false;
     if (wcols > W.cap) {
-      rowbasis_reserve(c, W, n, grow(wcols), true);
+      rowbasis_reserve(c, W, n, grow_for(n, wcols), true);
       dirty = true;
     }
     if (lcols > L.cap) {
-      devmat_reserve(c, L, n, grow(lcols), true);
+      devmat_reserve(c, L, n, grow_for(n, lcols), true);
       dirty = true;
     }
     if (W.ld > arr_cap) {
@@ -379,6 +392,13 @@ struct DevEig {
 };
 
 // ---- candidate evaluation (eigensolvers.hpp:275-318) --------------------------------------------
+// Candidate (Ritz vector) columns evaluated per chunk: U and A U for a chunk take at most the
+// context's candidate budget (8 GB by default).
+inline int cand_chunk(const Ctx& c, int n, int ncand) {
+  const size_t cols = c.cand_budget / (16 * (size_t)std::max(n, 1));
+  return std::max(1, (int)std::min<size_t>((size_t)ncand, std::max<size_t>(cols, 1)));
+}
+
 struct CandBuf {
   Ctx& c;
   DevMat U, AU;
@@ -399,8 +419,9 @@ struct CandBuf {
     const int n = A.n;
     // geometric growth: every reallocation is a cudaFree, which waits for the whole device
     // (the other slices' queued work included)
-    if (nc > U.cap || U.n != n) devmat_reserve(c, U, n, grow(nc), false);
-    if (nc > AU.cap || AU.n != n) devmat_reserve(c, AU, n, grow(nc), false);
+    const int want = (size_t)n * nc * 8 > kBigAlloc ? nc : grow(nc);
+    if (nc > U.cap || U.n != n) devmat_reserve(c, U, n, want, false);
+    if (nc > AU.cap || AU.n != n) devmat_reserve(c, AU, n, want, false);
     if (nc > stats_cap) {
       dev_free(stats);
       stats_cap = grow(nc);
@@ -485,7 +506,10 @@ struct Slice {
     HiPrio hp(c);
     k::tridiag_eigs_above(c, m, d.data(), e.data(), bar, chk_work, vals);
   }
-  ~Slice() { dev_free(chk_work); }
+  ~Slice() {
+    dev_free(chk_work);
+    devmat_free(trbuf);
+  }
   double stagnation_tol(double tnew) const {
     return cfg.tau1 > 0.0 ? cfg.tau1 : std::max(1e-12, 1e-10 * std::abs(tnew));
   }
@@ -516,6 +540,8 @@ struct Slice {
   }
 
   void lock(const double* u_raw, double uu, double lam, double res) {
+    if (kr.nlock + 1 > kr.L.cap && (size_t)A.n * (kr.nlock + 1) * 8 > kBigAlloc)
+      kr.reserve_locked(kr.nlock + 1 + std::max(64, kr.nlock / 8));  // +12.5%, not +50%
     kr.ensure(kr.W.cap, kr.nlock + 1);
     k::scale_copy(c, A.n, 1.0 / std::sqrt(uu), u_raw, kr.L.col(kr.nlock));
     ++kr.nlock;
@@ -592,6 +618,30 @@ struct Slice {
     // plus the vector traffic (T1 reads t, MID and N2 read and write it: 8 + 16 + 16 n)
     r->orth_bytes = 8.0 * A.n * (double)hc.reads_cols + 40.0 * A.n * (double)hc.passes_total;
     return r;
+  }
+
+  // Kept Ritz vectors of a thick restart recomputed into trbuf: trbuf[:, q] = W Y[:, j0 + cols[q]]
+  // (row-major W), for when the candidates were evaluated in chunks.
+  DevMat trbuf;
+  void stage_ritz(const double* W, int ldw, int steps, const double* Y, int j0,
+                  const std::vector<int>& cols) {
+    HiPrio hp(c);
+    const int n = A.n, k = (int)cols.size();
+    if (k > trbuf.cap || trbuf.n != n) devmat_reserve(c, trbuf, n, k, false);
+    Vec ysel((size_t)steps * k);
+    for (int q = 0; q < k; ++q) {
+      d2h(c, ysel.data() + (size_t)q * steps, Y + (size_t)(j0 + cols[q]) * steps, sizeof(double) * steps);
+    }
+    ctx_sync(c);
+    double* dy = dev_alloc<double>(ysel.size());
+    h2d(c, dy, ysel.data(), sizeof(double) * ysel.size());
+    const double one = 1.0, zero = 0.0;
+    const cublasStatus_t st = cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, n, k, steps, &one, W,
+                                          ldw, dy, steps, &zero, trbuf.p, n);
+    ctx_sync(c);
+    dev_free(dy);
+    if (st != CUBLAS_STATUS_SUCCESS) fail(SE_ECUDA, "cublasDgemm (thick-restart vectors) failed");
+    ++c.launches;
   }
 
   // Candidate rows ylast for thick restart: Y[steps-1, j] for the candidate columns.
@@ -780,11 +830,6 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
     int j0 = steps;
     while (j0 > 0 && vals[j0 - 1] >= s.bar_eff()) --j0;
     const int ncand = steps - j0;
-    Vec st;
-    tq = now_s();
-    if (ncand > 0) s.cand.eval(s.A, kr.W.p, steps, Y + (size_t)j0 * steps, steps, ncand, st, kr.W.ld);
-    s.prof[2] += now_s() - tq;
-    s.cnt.n_A_matvec += ncand;
     const Vec ylast = s.last_row(Y, steps, j0, ncand);
     struct TrC {
       double theta, ylast;
@@ -792,15 +837,27 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
     };
     std::vector<TrC> trset;
     int found = 0;
-    for (int q = ncand - 1; q >= 0; --q) {
-      const double lam = st[3 * q], res = st[3 * q + 1], uu = st[3 * q + 2];
-      if (!(uu > 0.0) || !s.in_slice(lam)) continue;
-      ++found;
-      if (s.converged(lam, res))
-        s.lock(s.cand.U.col(q), uu, lam, res);
-      else
-        trset.push_back({vals[j0 + q], ylast[q], q});
+    // candidates top-down (eigensolvers.hpp:582-591), evaluated in column chunks so that U and
+    // A U never hold more than ~8 GB (n ~ 2M); converged pairs lock as they are met
+    const int chunk = cand_chunk(s.c, n, ncand);
+    tq = now_s();
+    for (int hi = ncand; hi > 0; hi -= chunk) {
+      const int lo = std::max(0, hi - chunk);
+      Vec st;
+      s.cand.eval(s.A, kr.W.p, steps, Y + (size_t)(j0 + lo) * steps, steps, hi - lo, st, kr.W.ld);
+      for (int q = hi - 1; q >= lo; --q) {
+        const int u = q - lo;
+        const double lam = st[3 * u], res = st[3 * u + 1], uu = st[3 * u + 2];
+        if (!(uu > 0.0) || !s.in_slice(lam)) continue;
+        ++found;
+        if (s.converged(lam, res))
+          s.lock(s.cand.U.col(u), uu, lam, res);
+        else
+          trset.push_back({vals[j0 + q], ylast[q], q});
+      }
     }
+    s.prof[2] += now_s() - tq;
+    s.cnt.n_A_matvec += ncand;
     if (found == 0) {
       if (++empty_cycles >= 2) break;
     } else {
@@ -816,15 +873,23 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
     tr_s.clear();
     if (!broke) {
       const int lnew = (int)trset.size();
-      // the last Lanczos vector moves to column lnew, the kept Ritz vectors fill 0..lnew-1
-      k::rw_col_move(s.c, n, kr.W.p, kr.W.ld, steps, lnew);
       std::vector<int> cols;
       for (int q = 0; q < lnew; ++q) {
         tr_theta.push_back(trset[q].theta);
         tr_s.push_back(trailing * trset[q].ylast);
         cols.push_back(trset[q].col);
       }
-      kr.put_cols(cols, s.cand.U.p);
+      // the kept Ritz vectors: straight from U when every candidate fit in one chunk, else
+      // recomputed as W Y_kept into a staging block (the basis is still being read until then)
+      const double* src = s.cand.U.p;
+      if (chunk < ncand && lnew > 0) {
+        s.stage_ritz(kr.W.p, kr.W.ld, steps, Y, j0, cols);
+        src = s.trbuf.p;
+        for (int q = 0; q < lnew; ++q) cols[q] = q;
+      }
+      // the last Lanczos vector moves to column lnew, the kept Ritz vectors fill 0..lnew-1
+      k::rw_col_move(s.c, n, kr.W.p, kr.W.ld, steps, lnew);
+      kr.put_cols(cols, src);
     }
   }
   s.cnt.n_A_matvec += (long)s.op.k * its;

@@ -253,6 +253,25 @@ def window_estimate(n: int, mem_bytes: Optional[float], jobs: int, cap: float = 
     return max(est, MIN_WINDOW_EST)
 
 
+def capped_basis(n: int, mem_bytes: Optional[float], jobs: int, est: float) -> int:
+    """For a slice too large for the reference's m = 4 est but whose locked set still fits:
+    the basis width m (<= 5,000: "explicit m <= 5,000") that fits next to
+    the locked set (~1.15 est columns), the thick-restart staging block (m / 2) and the
+    chunked candidate buffers (8 GB), in 85% of the device memory per concurrent slice.
+    0 when even that does not fit (the slice is then solved as DOS-mass windows): a slice
+    solved in one window keeps the filter of the whole slice, while w windows need w times the
+    filter degree (each window is w times narrower)."""
+    if not mem_bytes:
+        return 0
+    col = 8.0 * n
+    room = 0.85 * mem_bytes / max(jobs, 1) - col * 1.15 * est - 8e9
+    m = int(min(5000, 4 * math.ceil(est), room / (1.5 * col)))
+    return m if m >= max(MIN_BASIS, 0.4 * est) else 0
+
+
+MIN_BASIS = 400
+
+
 def concurrent_jobs(n: int, mem_bytes: Optional[float], nslices: int, requested: int) -> int:
     """Slices solved at once on one GPU: all of them unless their windows would shrink below
     ~4x MIN_WINDOW_EST (narrow windows need high filter degrees); then as many as fit."""
@@ -330,12 +349,12 @@ class GpuBackend:
     def curve(self, zeta, lmin, lmax, npts):
         return api.kpm_curve(zeta, self.n, api.SpectralBounds(lmin, lmax), npts)
 
-    def solve_slice(self, plan: Plan, lmin, lmax, lo, hi, est):
+    def solve_slice(self, plan: Plan, lmin, lmax, lo, hi, est, m: int = 0):
         ctx = self._ctx()
         A = api.DeviceCsr(self.A.handle, ctx)  # se_csr is shareable across contexts on a device
         try:
             f = api.find_pol(lo, hi, api.SpectralBounds(lmin, lmax), api.PolyOpts(damping=plan.damping))
-            cfg = api.SolverConfig(m=plan.solver_m, res_tol=plan.tol, seed=plan.seed,
+            cfg = api.SolverConfig(m=m or plan.solver_m, res_tol=plan.tol, seed=plan.seed,
                                    est_count=max(1, int(math.ceil(est))))
             if plan.solver == "si":  # filtered subspace iteration (eigensolvers.hpp:760-940)
                 r = api.cheb_si(A, None, f, lo, hi, cfg.est_count, cfg, want_vectors=plan.want_vectors)
@@ -404,7 +423,11 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
         ts = time.perf_counter()
         out.t_start = ts - t2
         try:
-            wbp = window_breakpoints(curve, out.lo, out.hi, out.est, max_west)
+            m_cap = 0
+            if out.est > max_west and plan.window_est <= 0:
+                m_cap = capped_basis(backend.n, mem, jobs, out.est)
+            wbp = (np.array([out.lo, out.hi]) if m_cap else
+                   window_breakpoints(curve, out.lo, out.hi, out.est, max_west))
             nw = len(wbp) - 1
             vals, ress, vecs = [], [], []
             for w in range(nw):
@@ -412,7 +435,8 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
                 wlo, whi = float(wbp[w]), float(wbp[w + 1])
                 west = out.est if nw == 1 else api.dos_count(
                     curve, max(wlo, curve.xdos[0]), min(whi, curve.xdos[-1]))
-                k, r = backend.solve_slice(plan, lmin, lmax, wlo, whi, west)
+                k, r = backend.solve_slice(plan, lmin, lmax, wlo, whi, west,
+                                           **({"m": m_cap} if m_cap else {}))
                 # window seams follow the slice-seam rule (sliceeig_main.cpp:422-442)
                 wk = trim_to_slice(r.eigenvalues, r.residuals, w, nw, wlo, whi, delta)
                 vals.append(np.asarray(r.eigenvalues)[wk])

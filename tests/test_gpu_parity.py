@@ -514,3 +514,28 @@ def test_pipeline_solvers_match_reference_cli(gpu_ctx, golden, solver):
             assert np.all(s.residuals <= 1e-8 * np.maximum(1.0, np.abs(s.eigenvalues)))
         if solver != "si":  # Lanczos iteration counts within one stagnation-check cycle
             assert abs(s.niter - niter) <= 30, (s.index, s.niter, niter)
+
+
+def test_tr_chunked_candidates_and_staged_restart(gpu_ctx):
+    """Large-slice memory plan (cfg4/cfg5 sizes): with the candidate budget forced down to 24
+    Ritz vectors, run_tr evaluates the candidates in chunks (locking as it goes) and recomputes
+    the thick-restart vectors into a staging block.  Same slice as with one chunk: exactly the
+    analytic eigenvalues, residuals within tol."""
+    api = _api()
+    a = api.gen_laplacian([40, 40, 40])
+    ev = api.laplacian_analytic_eigs([40, 40, 40])
+    lo, hi = 0.9, 1.05
+    truth = ev[(ev >= lo) & (ev <= hi)]
+    f = api.find_pol(lo, hi, api.SpectralBounds(0.0, 12.0))
+    cfg = api.SolverConfig(est_count=int(truth.size), res_tol=1e-8)
+    ctx = api.default_context(0)
+    ref = api.cheb_lan_tr(a, None, f, lo, hi, cfg)
+    try:
+        ctx.set_candidate_budget(24 * 16 * a.n)
+        r = api.cheb_lan_tr(a, None, f, lo, hi, cfg)
+    finally:
+        ctx.set_candidate_budget(8 << 30)
+    for res in (ref, r):
+        assert res.eigenvalues.size == truth.size, (res.eigenvalues.size, truth.size)
+        assert np.all(np.abs(res.eigenvalues - truth) <= 1e-10 * np.abs(truth))
+        assert np.all(res.residuals <= 1e-8 * np.maximum(1.0, np.abs(res.eigenvalues)))
