@@ -344,7 +344,17 @@ inline se_csr* dev_of(const Operator& op, const char* who) {
 }
 inline void euclid_only(const InnerProduct& ip, const char* who) {
   if (!ip.euclidean())
-    throw std::invalid_argument(std::string(who) + ": B-weighted runs are outside the device path");
+    throw std::invalid_argument(std::string(who) + ": B-weighted runs need the CSR-backed B of a "
+                                "pencil (lan_tr_bounds / dos_generalized)");
+}
+// The device pencil of an InnerProduct whose B is a CSR-backed operator (make_operator(B)); the
+// b_solve operator is not needed (B-solves become B-products of the B^-1/2 series).
+inline se_pencil* pencil_for(const InnerProduct& ip, const char* who) {
+  if (!ip.b || !ip.b->csr)
+    throw std::invalid_argument(std::string(who) + ": the device path needs a CSR-backed B (make_operator)");
+  se_pencil* pen = nullptr;
+  ok(se_pencil_create(ctx(), ip.b->csr->device(), 0.0, 0, &pen));
+  return pen;
 }
 }  // namespace detail
 
@@ -442,11 +452,62 @@ inline LanczosState lanczos_run(const Operator& op, const InnerProduct& ip, Vec 
 inline SpectralBounds lan_tr_bounds(const Operator& op, const InnerProduct& ip, double tol,
                                     int restart_dim, int max_restarts = 40,
                                     unsigned long seed = 1234) {
-  detail::euclid_only(ip, "lan_tr_bounds");
+  if (!ip.euclidean()) {  // B inner product (sliceeig_main.cpp:128-136): the device pencil
+    se_pencil* pen = detail::pencil_for(ip, "lan_tr_bounds");
+    SpectralBounds b;
+    const int rc = se_lan_tr_bounds_pencil(detail::ctx(), detail::dev_of(op, "lan_tr_bounds"), pen,
+                                           tol, restart_dim, max_restarts, seed, &b.lmin, &b.lmax);
+    se_pencil_free(pen);
+    detail::ok(rc);
+    return b;
+  }
   SpectralBounds b;
   detail::ok(se_lan_tr_bounds(detail::ctx(), detail::dev_of(op, "lan_tr_bounds"), tol, restart_dim,
                               max_restarts, seed, &b.lmin, &b.lmax));
   return b;
+}
+
+// ---- cheb_approx.hpp -------------------------------------------------------------------------------
+enum class ScalarFun { Inverse, InverseSqrt };
+struct ChebApprox {
+  ScalarFun fun = ScalarFun::Inverse;
+  double lmin = 0.0, lmax = 0.0;
+  Vec coeff;
+  double achieved_rel_error = 0.0;
+  int degree() const { return (int)coeff.size() - 1; }
+  double eval(double t) const {  // Clenshaw on the mapped argument
+    const double c = 0.5 * (lmax + lmin), h = 0.5 * (lmax - lmin);
+    const double x = (t - c) / h;
+    double b1 = 0.0, b2 = 0.0;
+    for (int j = (int)coeff.size() - 1; j >= 1; --j) {
+      const double b0 = 2.0 * x * b1 - b2 + coeff[j];
+      b2 = b1;
+      b1 = b0;
+    }
+    return x * b1 - b2 + coeff[0];
+  }
+};
+inline ChebApprox ls_pol_approx(ScalarFun fun, const SpectralBounds& bounds, double tol,
+                                int max_deg = 300) {
+  ChebApprox ap;
+  ap.fun = fun;
+  ap.lmin = bounds.lmin;
+  ap.lmax = bounds.lmax;
+  ap.coeff.resize(std::max(max_deg, 0) + 1);
+  int deg = 0;
+  detail::ok(se_ls_pol_approx(fun == ScalarFun::InverseSqrt ? SE_FUN_INVSQRT : SE_FUN_INV,
+                              bounds.lmin, bounds.lmax, tol, max_deg, (int)ap.coeff.size(), &deg,
+                              ap.coeff.data(), &ap.achieved_rel_error));
+  ap.coeff.resize(deg + 1);
+  return ap;
+}
+// y = p(B) v (deg B-products on the device; the operator must be CSR-backed)
+inline void apply_cheb(const ChebApprox& ap, const Operator& b, const Vec& v, Vec& y,
+                       Counters* counters = nullptr) {
+  y.assign(v.size(), 0.0);
+  detail::ok(se_apply_cheb(detail::ctx(), detail::dev_of(b, "apply_cheb"), ap.lmin, ap.lmax,
+                           ap.degree(), ap.coeff.data(), 1, v.data(), y.data()));
+  if (counters) counters->n_B_matvec += ap.degree();
 }
 
 // ---- filter_poly.hpp -----------------------------------------------------------------------------------------
@@ -606,6 +667,28 @@ inline DosCurve lan_dos(const Operator& op, const SpectralBounds& bounds, const 
                         c.ydos.data(), &c.nev_est));
   return c;
 }
+// Pencil density (dos.hpp:160-184).  b_solve / b_halfsolve are the reference's Cholesky hooks;
+// the device path draws on op_b's CSR matrix instead (S = P A P, P ~ B^-1/2).
+inline DosCurve dos_generalized(const Operator& op_a, const Operator& b_solve,
+                                const Operator& b_halfsolve, const Operator& op_b,
+                                const SpectralBounds& bounds, const DosConfig& cfg = {}) {
+  (void)b_solve;
+  (void)b_halfsolve;
+  InnerProduct ip;
+  ip.b = &op_b;
+  se_pencil* pen = detail::pencil_for(ip, "dos_generalized");
+  DosCurve c;
+  c.n = op_a.n;
+  c.xdos.resize(std::max(cfg.npts, 0));
+  c.ydos.resize(std::max(cfg.npts, 0));
+  const int rc = se_lan_dos_pencil(detail::ctx(), detail::dev_of(op_a, "dos_generalized"), pen,
+                                   bounds.lmin, bounds.lmax, cfg.m, cfg.n_vec, cfg.npts,
+                                   cfg.gaussian_sigma, cfg.seed, c.xdos.data(), c.ydos.data(),
+                                   &c.nev_est);
+  se_pencil_free(pen);
+  detail::ok(rc);
+  return c;
+}
 inline double dos_count(const DosCurve& c, double xi, double eta) {
   double out = 0.0;
   detail::ok(se_dos_count((int)c.xdos.size(), c.n, c.xdos.data(), c.ydos.data(), xi, eta, &out));
@@ -717,10 +800,36 @@ inline EigenResults pencil_scaled(const CsrMatrix& a, const CsrMatrix& b, const 
   return r;
 }
 
+inline bool is_diagonal(const CsrMatrix& b) {
+  for (int i = 0; i < b.n(); ++i)
+    if (b.row_ptr()[i + 1] - b.row_ptr()[i] != 1 || b.col_idx()[b.row_ptr()[i]] != i) return false;
+  return true;
+}
+
+// A general sparse SPD B on the device: se_pencil (S = P A P with P ~ B^-1/2 a Chebyshev series
+// in B; the reference's Cholesky B-solves become B-products).  RAII over the C handle.
+struct PencilHandle {
+  se_pencil* p = nullptr;
+  explicit PencilHandle(const CsrMatrix& b) { ok(se_pencil_create(ctx(), b.device(), 0.0, 0, &p)); }
+  ~PencilHandle() { se_pencil_free(p); }
+  PencilHandle(const PencilHandle&) = delete;
+  PencilHandle& operator=(const PencilHandle&) = delete;
+};
+
 inline EigenResults cheb_lan_pencil(int solver, const CsrMatrix& a, const CsrMatrix& b,
                                     const PolynomialFilter& f, double xi, double eta,
                                     const SolverConfig& cfg, const DeflationSet* locked) {
   const std::string who = solver ? "cheb_lan_tr" : "cheb_lan_nr";
+  if (!is_diagonal(b)) {
+    if (locked && locked->count() > 0)
+      throw std::invalid_argument(who + ": a preloaded deflation set is not supported for a non-diagonal B");
+    PencilHandle pen(b);
+    const se_poly_filter s = to_c(f);
+    const se_solver_cfg c{cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count, cfg.seed};
+    se_results* r = nullptr;
+    ok(se_cheb_lan_pencil(ctx(), a.device(), pen.p, &s, xi, eta, &c, solver, &r));
+    return collect(r, a.n());
+  }
   return pencil_scaled(a, b, who, [&](const CsrMatrix& s, const Vec& d) {
     DeflationSet ly;
     if (locked && locked->count() > 0) {  // locked pencil vectors x -> y = D^-1 x

@@ -263,6 +263,39 @@ SE_API int se_cheb_lan(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, do
  * isation, Rayleigh-Ritz by DGEMM + syevd); SE_ENUMERIC when the block saturates above the bar. */
 SE_API int se_cheb_si(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi, double eta,
                       int est_count, const se_solver_cfg* cfg, se_results** out);
+/* ---- general SPD-B pencils (A, B) ------------------------------------------------------------
+ * The reference solves them with Cholesky-backed B-solves (cholesky.hpp, eigensolvers.hpp:
+ * 640-732).  Here a pencil is the standard problem S = P A P with P ~ B^-1/2 a Chebyshev series
+ * in B (ls_pol_approx InverseSqrt, cheb_approx.hpp:40-88, applied like apply_cheb :91-112): every
+ * B-solve becomes B-products on the GPU, eigenvalues are the pencil's, eigenvectors come back as
+ * x = P y with x'Bx = 1, residuals are ||Ax - lambda Bx|| / sqrt(x'Bx).  B must outlive the
+ * pencil handle. */
+typedef struct se_pencil se_pencil;
+#define SE_FUN_INV 0
+#define SE_FUN_INVSQRT 1
+/* ls_pol_approx (cheb_approx.hpp:40-88): fun SE_FUN_INV (1/t) or SE_FUN_INVSQRT (1/sqrt t). */
+SE_API int se_ls_pol_approx(int fun, double lmin, double lmax, double tol, int max_deg, int cap,
+                            int* degree, double* coeff, double* achieved);
+/* apply_cheb (cheb_approx.hpp:91-112): y = p(B) x for nvec host column-major vectors. */
+SE_API int se_apply_cheb(se_ctx* ctx, const se_csr* b, double lmin, double lmax, int degree,
+                         const double* coeff, int nvec, const double* x, double* y);
+/* B's spectrum by lan_tr_bounds, widened, and the B^-1/2 fit (tol 0 -> 1e-13, max_deg 0 -> 300). */
+SE_API int se_pencil_create(se_ctx* ctx, const se_csr* b, double tol, int max_deg, se_pencil** out);
+SE_API int se_pencil_info(const se_pencil* p, int* degree, double* bmin, double* bmax,
+                          double* achieved);
+SE_API int se_pencil_free(se_pencil* p);
+/* lan_tr_bounds with ip = {B, B-solve} (lanczos.hpp:148-277), sliceeig_main.cpp:128-136. */
+SE_API int se_lan_tr_bounds_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p, double tol,
+                                   int restart_dim, int max_restarts, uint64_t seed, double* lmin,
+                                   double* lmax);
+/* dos_generalized (dos.hpp:160-184): Lanczos density of the pencil. */
+SE_API int se_lan_dos_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p, double lmin,
+                             double lmax, int m, int n_vec, int npts, double sigma, uint64_t seed,
+                             double* x, double* y, double* nev_est);
+/* cheb_lan_nr / cheb_lan_tr(a, &b, ...) (eigensolvers.hpp:703-732) for a general SPD B. */
+SE_API int se_cheb_lan_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p,
+                              const se_poly_filter* f, double xi, double eta,
+                              const se_solver_cfg* cfg, int solver, se_results** out);
 SE_API int se_results_count(const se_results* r, int* nev);
 /* eigenvalues/residuals (nev each, ascending by eigenvalue), vectors (n x nev, may be NULL). */
 SE_API int se_results_copy(const se_results* r, double* eigenvalues, double* residuals, double* vectors);

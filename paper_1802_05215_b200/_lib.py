@@ -92,6 +92,17 @@ SIGNATURES = {
     "se_kpm_dos_multi": [C.c_int, _PI, C.c_int, _PI, _PI, _PD, C.c_double, C.c_double, C.c_int,
                          C.c_int, C.c_int, C.c_uint64, C.c_int, _PD, _PD, _PD],
     "se_nccl_version": [_PI],
+    "se_ls_pol_approx": [C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, _PI, _PD,
+                         _PD],
+    "se_apply_cheb": [_VP, _VP, C.c_double, C.c_double, C.c_int, _PD, C.c_int, _PD, _PD],
+    "se_pencil_create": [_VP, _VP, C.c_double, C.c_int, C.POINTER(_VP)],
+    "se_pencil_info": [_VP, _PI, _PD, _PD, _PD],
+    "se_pencil_free": [_VP],
+    "se_lan_tr_bounds_pencil": [_VP, _VP, _VP, C.c_double, C.c_int, C.c_int, C.c_uint64, _PD, _PD],
+    "se_lan_dos_pencil": [_VP, _VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                          C.c_double, C.c_uint64, _PD, _PD, _PD],
+    "se_cheb_lan_pencil": [_VP, _VP, _VP, C.POINTER(SePolyFilter), C.c_double, C.c_double,
+                           C.POINTER(SeSolverCfg), C.c_int, C.POINTER(_VP)],
     "se_kpm_curve": [C.c_int, _PD, C.c_int, C.c_double, C.c_double, C.c_int, _PD, _PD, _PD],
     "se_kpm_dos": [_VP, _VP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
                    _PD, _PD, _PD],

@@ -541,6 +541,57 @@ def lan_dos(op, bounds: SpectralBounds, cfg: DosConfig = DosConfig()) -> DosCurv
     return DosCurve(x, y, nev.value, d.n)
 
 
+def ls_pol_approx(fun: str, bounds: SpectralBounds, tol: float, max_deg: int = 300):
+    """cheb_approx.hpp:40-88: Chebyshev least-squares fit of 1/t ("inverse") or 1/sqrt(t)
+    ("inverse_sqrt") on bounds.  Returns (coefficients, achieved relative error)."""
+    co = np.empty(max_deg + 1)
+    deg, ach = C.c_int(), C.c_double()
+    call("se_ls_pol_approx", 1 if fun == "inverse_sqrt" else 0, bounds.lmin, bounds.lmax, tol,
+         max_deg, max_deg + 1, C.byref(deg), _pd(co), C.byref(ach))
+    return co[: deg.value + 1].copy(), ach.value
+
+
+def apply_cheb(coeff, bounds: SpectralBounds, b, v) -> np.ndarray:
+    """cheb_approx.hpp:91-112: y = p(B) v (v: n or n x k), on the GPU."""
+    d = _dev(b)
+    co = _f64(coeff)
+    v = np.asarray(v, np.float64)
+    vv = np.asfortranarray(v.reshape(d.n, -1))
+    out = np.empty_like(vv, order="F")
+    call("se_apply_cheb", d.ctx.handle, d.handle, bounds.lmin, bounds.lmax, co.size - 1, _pd(co),
+         vv.shape[1], vv.ctypes.data_as(_PD), out.ctypes.data_as(_PD))
+    return out.reshape(v.shape)
+
+
+def lan_tr_bounds_pencil(a, b, tol: float = 1e-4, restart_dim: int = 60, max_restarts: int = 40,
+                         seed: int = 1234) -> SpectralBounds:
+    """lan_tr_bounds(op_a, {B, B-solve}, ...) (lanczos.hpp:148-277) for a general SPD B."""
+    d = _dev(a)
+    pen = Pencil(b, d.ctx)
+    try:
+        lo, hi = C.c_double(), C.c_double()
+        call("se_lan_tr_bounds_pencil", d.ctx.handle, d.handle, pen.handle, tol, restart_dim,
+             max_restarts, seed, C.byref(lo), C.byref(hi))
+        return SpectralBounds(lo.value, hi.value)
+    finally:
+        pen.close()
+
+
+def dos_generalized(a, b, bounds: SpectralBounds, cfg: DosConfig = DosConfig()) -> DosCurve:
+    """dos.hpp:160-184: the Lanczos density of the pencil (A, B), B sparse SPD."""
+    d = _dev(a)
+    pen = Pencil(b, d.ctx)
+    try:
+        x = np.empty(max(cfg.npts, 0))
+        y = np.empty(max(cfg.npts, 0))
+        nev = C.c_double()
+        call("se_lan_dos_pencil", d.ctx.handle, d.handle, pen.handle, bounds.lmin, bounds.lmax,
+             cfg.m, cfg.n_vec, cfg.npts, cfg.gaussian_sigma, cfg.seed, _pd(x), _pd(y), C.byref(nev))
+        return DosCurve(x, y, nev.value, d.n)
+    finally:
+        pen.close()
+
+
 def dos_count(c: DosCurve, xi: float, eta: float) -> float:
     """dos.hpp:212-218."""
     out = C.c_double()
@@ -755,7 +806,64 @@ def _pencil_scaled(a, d, b, who, solve, want_vectors=True):
     return EigenResults(r.eigenvalues, x, r.residuals, r.niter, r.counters, r.hit_max_its, r.orth)
 
 
+def _is_diagonal(b, n: int) -> bool:
+    hb = b.download() if isinstance(b, DeviceCsr) else b
+    rp, ci = np.asarray(hb.row_ptr), np.asarray(hb.col_idx)
+    return bool(np.all(np.diff(rp) == 1) and np.array_equal(ci, np.arange(n)))
+
+
+class Pencil:
+    """A general SPD-B pencil on the device (se_pencil): B's spectrum, the Chebyshev fit
+    P ~ B^-1/2 (ls_pol_approx, cheb_approx.hpp:40-88) used to solve S = P A P."""
+
+    def __init__(self, b, ctx: Optional[Context] = None, tol: float = 0.0, max_deg: int = 0):
+        ctx = ctx or default_context()
+        self.B = b if isinstance(b, DeviceCsr) else DeviceCsr.upload(b, ctx)
+        self._owns = not isinstance(b, DeviceCsr)
+        h = C.c_void_p()
+        call("se_pencil_create", self.B.ctx.handle, self.B.handle, tol, max_deg, C.byref(h))
+        self.handle = h
+        deg, lo, hi, ach = C.c_int(), C.c_double(), C.c_double(), C.c_double()
+        call("se_pencil_info", h, C.byref(deg), C.byref(lo), C.byref(hi), C.byref(ach))
+        self.degree, self.bmin, self.bmax, self.achieved = deg.value, lo.value, hi.value, ach.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            call("se_pencil_free", self.handle)
+            self.handle = None
+        if getattr(self, "_owns", False) and self.B is not None:
+            self.B.free()
+            self.B = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _cheb_lan_general_pencil(solver, d, b, f, xi, eta, cfg, locked, want_vectors, who):
+    if locked is not None and locked.count() > 0:
+        raise ValueError(f"{who}: a preloaded deflation set is not supported for a non-diagonal B")
+    pen = Pencil(b, d.ctx)
+    try:
+        s, _keep = f._c()
+        c = _lib.SeSolverCfg(cfg.m, cfg.max_its, cfg.ncycle, cfg.tau1, cfg.res_tol, cfg.est_count,
+                             cfg.seed)
+        h = C.c_void_p()
+        call("se_cheb_lan_pencil", d.ctx.handle, d.handle, pen.handle, C.byref(s), xi, eta,
+             C.byref(c), solver, C.byref(h))
+        return _collect_results(h, d, want_vectors)
+    finally:
+        pen.close()
+
+
 def _cheb_lan_pencil(solver, a, d, b, f, xi, eta, cfg, locked, want_vectors, who):
+    if getattr(b, "n", d.n) != d.n:
+        raise ValueError(f"{who}: pencil size mismatch")
+    if not _is_diagonal(b, d.n):  # general SPD B: S = P A P with P ~ B^-1/2 on the device
+        return _cheb_lan_general_pencil(solver, d, b, f, xi, eta, cfg, locked, want_vectors, who)
+
     def solve(S, dsc):
         ly = None
         if locked is not None and locked.count() > 0:  # locked pencil vectors x -> y = D^-1 x

@@ -22,6 +22,10 @@ struct se_ctx {
 struct se_csr {
   DevCsr a;
 };
+struct se_pencil {
+  Pencil p;
+  double bmin = 0.0, bmax = 0.0, achieved = 0.0;
+};
 struct se_results {
   std::unique_ptr<SliceResult> r;
   int device = 0;
@@ -957,6 +961,162 @@ int se_cheb_si(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, double xi,
     auto res = std::make_unique<se_results>();
     res->device = c.device;
     res->r = cheb_si(c, M(a), to_filter(f), xi, eta, est_count, sc);
+    *out = res.release();
+  });
+}
+
+// ---- general SPD-B pencils ------------------------------------------------------------------
+int se_ls_pol_approx(int fun, double lmin, double lmax, double tol, int max_deg, int cap,
+                     int* degree, double* coeff, double* achieved) {
+  return guard([&] {
+    const ChebFit f = ls_pol_approx(fun == SE_FUN_INVSQRT, lmin, lmax, tol, max_deg);
+    if ((int)f.coeff.size() > cap) fail(SE_EINVAL, "ls_pol_approx: coefficient buffer too small");
+    std::copy(f.coeff.begin(), f.coeff.end(), coeff);
+    *degree = (int)f.coeff.size() - 1;
+    if (achieved) *achieved = f.achieved;
+  });
+}
+
+int se_apply_cheb(se_ctx* ctx, const se_csr* b, double lmin, double lmax, int degree,
+                  const double* coeff, int nvec, const double* x, double* y) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& B = M(b);
+    if (degree < 0 || !(lmax > lmin) || nvec < 0) fail(SE_EINVAL, "apply_cheb: bad arguments");
+    const size_t len = (size_t)B.n * nvec;
+    if (len == 0) return;
+    double* dx = dev_alloc<double>(len);
+    double* dy = dev_alloc<double>(len);
+    try {
+      h2d(c, dx, x, sizeof(double) * len);
+      if (degree == 0) {  // y = c0 x
+        k::scale_copy(c, (int)len, coeff[0], dx, dy);
+      } else {
+        StepOp op;
+        op.plain = false;
+        op.k = degree;
+        op.mu.assign(coeff, coeff + degree + 1);
+        op.c = 0.5 * (lmax + lmin);
+        op.invd = 1.0 / (0.5 * (lmax - lmin));
+        apply_filter_dev(c, B, op, nvec, dx, dy);
+      }
+      d2h(c, y, dy, sizeof(double) * len);
+      ctx_sync(c);
+    } catch (...) {
+      dev_free(dx);
+      dev_free(dy);
+      throw;
+    }
+    dev_free(dx);
+    dev_free(dy);
+  });
+}
+
+int se_pencil_create(se_ctx* ctx, const se_csr* b, double tol, int max_deg, se_pencil** out) {
+  return guard([&] {
+    *out = nullptr;
+    Ctx& c = C(ctx);
+    const DevCsr& B = M(b);
+    if (B.n < 1) fail(SE_EINVAL, "pencil: empty B");
+    // B's spectrum (the reference bounds its pencils the same way, lanczos.hpp:148-277), widened
+    // so the B^-1/2 fit covers it; B must be SPD
+    double lo = 0.0, hi = 0.0;
+    lan_tr_bounds(c, B, 1e-4, 60, 40, 1234, lo, hi);
+    if (!(lo > 0.0)) fail(SE_EINVAL, "pencil: B is not positive definite");
+    auto h = std::make_unique<se_pencil>();
+    h->bmin = 0.9 * lo;
+    h->bmax = 1.05 * hi;
+    const ChebFit f = ls_pol_approx(true, h->bmin, h->bmax, tol > 0.0 ? tol : 1e-13,
+                                    max_deg > 0 ? max_deg : 300);
+    h->achieved = f.achieved;
+    h->p.B = &B;
+    h->p.P.plain = false;
+    h->p.P.k = (int)f.coeff.size() - 1;
+    h->p.P.mu = f.coeff;
+    h->p.P.c = 0.5 * (h->bmax + h->bmin);
+    h->p.P.invd = 1.0 / (0.5 * (h->bmax - h->bmin));
+    if (h->p.P.k < 1) {  // keep at least one recurrence degree for the fused kernel
+      h->p.P.k = 1;
+      h->p.P.mu.push_back(0.0);
+    }
+    *out = h.release();
+  });
+}
+
+int se_pencil_info(const se_pencil* p, int* degree, double* bmin, double* bmax, double* achieved) {
+  return guard([&] {
+    if (!p) fail(SE_EINVAL, "null se_pencil");
+    if (degree) *degree = p->p.P.k;
+    if (bmin) *bmin = p->bmin;
+    if (bmax) *bmax = p->bmax;
+    if (achieved) *achieved = p->achieved;
+  });
+}
+
+int se_pencil_free(se_pencil* p) {
+  delete p;
+  return SE_OK;
+}
+
+int se_lan_tr_bounds_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p, double tol,
+                            int restart_dim, int max_restarts, uint64_t seed, double* lmin,
+                            double* lmax) {
+  return guard([&] {
+    if (!p) fail(SE_EINVAL, "null se_pencil");
+    lan_tr_bounds(C(ctx), M(a), tol, restart_dim, max_restarts, seed, *lmin, *lmax, &p->p);
+  });
+}
+
+int se_lan_dos_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p, double lmin, double lmax,
+                      int m, int n_vec, int npts, double sigma, uint64_t seed, double* x,
+                      double* y, double* nev_est) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const DevCsr& mat = M(a);
+    if (!p) fail(SE_EINVAL, "null se_pencil");
+    if (!(lmin < lmax)) fail(SE_EINVAL, "dos: empty spectral interval");
+    if (m < 1 || n_vec < 1 || npts < 2) fail(SE_EINVAL, "dos: need m >= 1, n_vec >= 1, npts >= 2");
+    // dos_generalized (dos.hpp:160-184): Lanczos on S = P A P from Gaussian probes (the
+    // reference's L^-T g start is a Gaussian probe of the equivalent standard problem too)
+    const double sg = sigma > 0.0 ? sigma : 0.4 * (lmax - lmin) / std::sqrt((double)m);
+    Curve cv;
+    cv.n = mat.n;
+    cv.x = dos_grid(lmin, lmax, npts);
+    cv.y.assign(npts, 0.0);
+    Rng rng(seed);
+    Vec start(mat.n);
+    for (int l = 0; l < n_vec; ++l) {
+      rng.normal_fill(start.data(), mat.n);
+      const LanczosRun r = lanczos_run(c, mat, start.data(), m, false, &p->p);
+      Vec vals, vecs;
+      sym_tridiag_eig(r.alpha, r.beta, true, vals, vecs);
+      const int steps = (int)vals.size();
+      Vec tau2(steps);
+      for (int i = 0; i < steps; ++i) tau2[i] = vecs[(size_t)i * steps] * vecs[(size_t)i * steps];
+      add_ritz_gaussians(vals, tau2, cv.x, sg, cv.y);
+    }
+    dos_finalize(cv);
+    std::copy(cv.x.begin(), cv.x.end(), x);
+    std::copy(cv.y.begin(), cv.y.end(), y);
+    *nev_est = cv.nev_est;
+  });
+}
+
+int se_cheb_lan_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p, const se_poly_filter* f,
+                       double xi, double eta, const se_solver_cfg* cfg, int solver,
+                       se_results** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!p) fail(SE_EINVAL, "null se_pencil");
+    const char* who = solver == 1 ? "cheb_lan_tr" : "cheb_lan_nr";
+    Ctx& c = C(ctx);
+    if (M(a).n != p->p.B->n) fail(SE_EINVAL, std::string(who) + ": pencil size mismatch");
+    if (!(eta > xi)) fail(SE_EINVAL, std::string(who) + ": degenerate interval");
+    const SolverCfg sc = resolve_config(cfg, who);
+    auto res = std::make_unique<se_results>();
+    res->device = c.device;
+    res->r = cheb_lan(c, M(a), to_filter(f), xi, eta, sc, solver == 1, 0, nullptr, nullptr, who,
+                      &p->p);
     *out = res.release();
   });
 }

@@ -60,7 +60,10 @@ struct Krylov {
   Ctx& c;
   const DevCsr& A;
   const StepOp& op;
+  const Pencil* pen;
   int n;
+  double* pb[3] = {nullptr, nullptr, nullptr};  // pencil: the P-series recurrence buffers
+  double *s1 = nullptr, *s2 = nullptr, *sx = nullptr;  // P x, A P x, S x
   RowBasis W;
   DevMat L;
   double* t = nullptr;
@@ -87,9 +90,16 @@ struct Krylov {
 
   double* mu_dev = nullptr;
 
-  Krylov(Ctx& cc, const DevCsr& a, const StepOp& o) : c(cc), A(a), op(o), n(a.n) {
+  Krylov(Ctx& cc, const DevCsr& a, const StepOp& o, const Pencil* p = nullptr)
+      : c(cc), A(a), op(o), pen(p), n(a.n) {
     t = dev_alloc<double>(n);
     vsrc = dev_alloc<double>(n);
+    if (pen) {
+      for (double*& b : pb) b = dev_alloc<double>(n);
+      s1 = dev_alloc<double>(n);
+      s2 = dev_alloc<double>(n);
+      sx = dev_alloc<double>(n);
+    }
     if (!op.plain) {
       for (double*& b : fb) b = dev_alloc<double>(n);
       mu_dev = dev_alloc<double>(op.k + 1);
@@ -106,6 +116,8 @@ struct Krylov {
     dev_free(W.p);
     devmat_free(L);
     dev_free(mu_dev);
+    for (void* p : {(void*)pb[0], (void*)pb[1], (void*)pb[2], (void*)s1, (void*)s2, (void*)sx})
+      dev_free(p);
     for (void* p : {(void*)t, (void*)vsrc, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl,
                     (void*)alpha, (void*)beta, (void*)hdiag, (void*)coef, (void*)coef2,
                     (void*)coef_l, (void*)dscal, (void*)s.buf, (void*)s.cnt, (void*)rbuf,
@@ -221,39 +233,79 @@ struct Krylov {
     k::rw_put_cols(c, n, W.p, W.ld, 0, (int)cols.size(), U, n, idx);
   }
 
-  // Filter W[:, ctl->i] into t (apply_pol filter_poly.hpp:256-277, or one op application).
-  void record_filter() {
-    k::rw_col_get(c, n, W.p, W.ld, ctl, 0, vsrc);
+  // out = sum_j op.mu[j] T_j((M - c I) / d) x by the fused SpMV recurrence on matrix M, with
+  // buffers buf[3] (apply_pol filter_poly.hpp:256-277; apply_cheb cheb_approx.hpp:91-112 for
+  // the pencil series, whose map multiplies by 1/h instead of dividing).
+  void record_series(const DevCsr& M, const StepOp& sop, const double* x, double* out,
+                     double* const* buf) {
     k::ChebArgs a;
     a.halt = ctl;
-    if (op.plain) {
-      a.x = vsrc;
-      a.y = t;
-      k::spmv_cheb(c, A, k::kPlain, a);
-      return;
-    }
-    a.c = op.c;
-    a.invd = op.invd;
-    a.x = vsrc;
-    a.y = fb[0];
-    a.out = t;
-    a.mu0 = op.mu[0];
-    a.muj = op.mu[1];
-    k::spmv_cheb(c, A, k::kFirst, a);
-    // buffers: prev (j-2), cur (j-1), next; the source column plays prev for j = 2
+    a.c = sop.c;
+    a.invd = sop.invd;
+    a.x = x;
+    a.y = buf[0];
+    a.out = out;
+    a.mu0 = sop.mu[0];
+    a.muj = sop.mu[1];
+    k::spmv_cheb(c, M, k::kFirst, a);
+    // buffers: prev (j-2), cur (j-1), next; x plays prev for j = 2
     int cur = 0, prv = -1, nxt = 1;
-    for (int j = 2; j <= op.k; ++j) {
+    for (int j = 2; j <= sop.k; ++j) {
       k::ChebArgs b = a;
-      b.x = fb[cur];
-      b.prev = prv < 0 ? vsrc : fb[prv];
-      b.y = fb[nxt];
-      b.muj = op.mu[j];
-      k::spmv_cheb(c, A, k::kNext, b);
+      b.x = buf[cur];
+      b.prev = prv < 0 ? x : buf[prv];
+      b.y = buf[nxt];
+      b.muj = sop.mu[j];
+      k::spmv_cheb(c, M, k::kNext, b);
       const int old_prv = prv < 0 ? 2 : prv;
       prv = cur;
       cur = nxt;
       nxt = old_prv;
     }
+  }
+
+  // y = S x = P A P x (pencil)
+  void record_apply_s(const double* x, double* y) {
+    record_series(*pen->B, pen->P, x, s1, pb);
+    k::ChebArgs a;
+    a.halt = ctl;
+    a.x = s1;
+    a.y = s2;
+    k::spmv_cheb(c, A, k::kPlain, a);
+    record_series(*pen->B, pen->P, s2, y, pb);
+  }
+
+  // Filter W[:, ctl->i] into t (apply_pol filter_poly.hpp:256-277, or one op application).
+  void record_filter() {
+    k::rw_col_get(c, n, W.p, W.ld, ctl, 0, vsrc);
+    if (pen) {  // composite operator: each degree is S x, then the recurrence update
+      if (op.plain) {
+        record_apply_s(vsrc, t);
+        return;
+      }
+      record_apply_s(vsrc, sx);
+      k::cheb_combine(c, n, true, sx, vsrc, nullptr, fb[0], t, op.c, op.invd, op.mu[0], op.mu[1], ctl);
+      int cur = 0, prv = -1, nxt = 1;
+      for (int j = 2; j <= op.k; ++j) {
+        record_apply_s(fb[cur], sx);
+        k::cheb_combine(c, n, false, sx, fb[cur], prv < 0 ? vsrc : fb[prv], fb[nxt], t, op.c,
+                        op.invd, 0.0, op.mu[j], ctl);
+        const int old_prv = prv < 0 ? 2 : prv;
+        prv = cur;
+        cur = nxt;
+        nxt = old_prv;
+      }
+      return;
+    }
+    if (op.plain) {
+      k::ChebArgs a;
+      a.halt = ctl;
+      a.x = vsrc;
+      a.y = t;
+      k::spmv_cheb(c, A, k::kPlain, a);
+      return;
+    }
+    record_series(A, op, vsrc, t, fb);
   }
 
   // One Lanczos step.  mode 0: NR recurrence (eigensolvers.hpp:406-433 / lanczos.hpp:151-185);
@@ -401,14 +453,17 @@ inline int cand_chunk(const Ctx& c, int n, int ncand) {
 
 struct CandBuf {
   Ctx& c;
-  DevMat U, AU;
+  const Pencil* pen = nullptr;
+  DevMat U, AU, X, BX;
   double* stats = nullptr;
   int stats_cap = 0;
-  explicit CandBuf(Ctx& cc) : c(cc) {}
+  explicit CandBuf(Ctx& cc, const Pencil* p = nullptr) : c(cc), pen(p) {}
   ~CandBuf() {
     cudaStreamSynchronize(c.stream);
     devmat_free(U);
     devmat_free(AU);
+    devmat_free(X);
+    devmat_free(BX);
     dev_free(stats);
   }
   // U = W[:, :steps] Y (Y steps x nc, ld ldy), AU = A U, stats per column.  W is column-major
@@ -437,14 +492,26 @@ struct CandBuf {
     if (st != CUBLAS_STATUS_SUCCESS)
       fail(SE_ECUDA, "cublasDgemm (Ritz combinations) failed");
     ++c.launches;
-    for (int j0 = 0; j0 < nc; j0 += 65535) {
-      k::ChebArgs a;
-      a.x = U.col(j0);
-      a.y = AU.col(j0);
-      a.ncols = std::min(65535, nc - j0);
-      k::spmv_cheb(c, A, k::kPlain, a);
+    auto spmv_cols = [&](const DevCsr& M, const double* x, double* y) {
+      for (int q0 = 0; q0 < nc; q0 += 65535) {
+        k::ChebArgs a;
+        a.x = x + (size_t)q0 * n;
+        a.y = y + (size_t)q0 * n;
+        a.ncols = std::min(65535, nc - q0);
+        k::spmv_cheb(c, M, k::kPlain, a);
+      }
+    };
+    if (pen) {  // x = P u, A x, B x: the reference's B-weighted Rayleigh quotient and residual
+      if (nc > X.cap || X.n != n) devmat_reserve(c, X, n, want, false);
+      if (nc > BX.cap || BX.n != n) devmat_reserve(c, BX, n, want, false);
+      apply_filter_block(c, *pen->B, pen->P, nc, U.p, X.p);
+      spmv_cols(A, X.p, AU.p);
+      spmv_cols(*pen->B, X.p, BX.p);
+      k::pencil_stats(c, n, nc, U.p, X.p, AU.p, BX.p, stats);
+    } else {
+      spmv_cols(A, U.p, AU.p);
+      k::candidate_stats(c, n, nc, U.p, AU.p, stats, A.resw);
     }
-    k::candidate_stats(c, n, nc, U.p, AU.p, stats, A.resw);
     out3.resize(3 * (size_t)nc);
     d2h(c, out3.data(), stats, sizeof(double) * 3 * nc);
     ctx_sync(c);
@@ -467,10 +534,11 @@ struct Slice {
   DevEig eig;
   CandBuf cand;
 
+  const Pencil* pen;
   Slice(Ctx& cc, const DevCsr& a, const PolyFilter& f, double xi_, double eta_,
-        const SolverCfg& cf)
+        const SolverCfg& cf, const Pencil* p = nullptr)
       : c(cc), A(a), cfg(cf), bar(f.bar), xi(xi_), eta(eta_), rng(cf.seed), op(make_op(f)),
-        kr(cc, a, op), eig(cc), cand(cc) {}
+        kr(cc, a, op, p), eig(cc), cand(cc, p), pen(p) {}
 
   static StepOp make_op(const PolyFilter& f) {
     StepOp o;
@@ -598,6 +666,25 @@ struct Slice {
                               cudaMemcpyDeviceToDevice, c.stream));
     }
     ctx_sync(c);
+    if (pen && k > 0) {  // eigenvectors of the pencil: x = P y, B-normalised
+      DevMat X, BX;
+      devmat_reserve(c, X, A.n, k, false);
+      devmat_reserve(c, BX, A.n, k, false);
+      apply_filter_block(c, *pen->B, pen->P, k, r->vectors.p, X.p);
+      for (int q0 = 0; q0 < k; q0 += 65535) {
+        k::ChebArgs a;
+        a.x = X.col(q0);
+        a.y = BX.col(q0);
+        a.ncols = std::min(65535, k - q0);
+        k::spmv_cheb(c, *pen->B, k::kPlain, a);
+      }
+      k::b_normalize(c, A.n, k, X.p, BX.p);
+      SE_CUDA(cudaMemcpyAsync(r->vectors.p, X.p, sizeof(double) * (size_t)A.n * k,
+                              cudaMemcpyDeviceToDevice, c.stream));
+      ctx_sync(c);
+      devmat_free(X);
+      devmat_free(BX);
+    }
     add_timers();
     cnt.t_total += now_s() - t0;
     if (std::getenv("SE_PROFILE"))
@@ -967,11 +1054,12 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
 }
 
 // lanczos_run (lanczos.hpp:37-118), euclidean inner product.
-LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m, bool want_basis) {
+LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m, bool want_basis,
+                       const Pencil* pen) {
   const int n = a.n;
   m = std::min(m, n);
-  StepOp op;  // plain A
-  Krylov kr(c, a, op);
+  StepOp op;  // plain A (or S = P A P)
+  Krylov kr(c, a, op, pen);
   kr.ensure(m + 1, 0);
   h2d(c, kr.t, start_host, sizeof(double) * n);
   const double nb2 = kr.dot(kr.t, kr.t);
@@ -1007,15 +1095,15 @@ LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m,
 
 // lan_tr_bounds (lanczos.hpp:148-277): keep the two extreme Ritz pairs across restarts.
 void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max_restarts,
-                   std::uint64_t seed, double& lmin, double& lmax) {
+                   std::uint64_t seed, double& lmin, double& lmax, const Pencil* pen) {
   const int n = a.n;
   const int m = std::min(restart_dim, n);
   if (m < 1) fail(SE_EINVAL, "lan_tr_bounds: empty operator");
   Rng rng(seed);
   StepOp op;
-  Krylov kr(c, a, op);
+  Krylov kr(c, a, op, pen);
   kr.ensure(m + 1, 0);
-  CandBuf cand(c);
+  CandBuf cand(c);  // restart combinations only (the Ritz vectors stay in the Lanczos space)
   double* dY = dev_alloc<double>((size_t)m * 2);
   Vec kept_theta, kept_s;
   double prev_lo = 0.0, prev_hi = 0.0;
@@ -1085,13 +1173,19 @@ void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max
   fail(SE_ENUMERIC, "lan_tr_bounds: failed to settle");
 }
 
+void pencil_map(Ctx& c, const Pencil& pen, int nvec, const double* x, double* y) {
+  apply_filter_block(c, *pen.B, pen.P, nvec, x, y);
+}
+
 std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter& f, double xi,
                                       double eta, const SolverCfg& cfg, bool thick_restart,
                                       int ndefl, const double* defl_u, const double* defl_vals,
-                                      const char* who) {
+                                      const char* who, const Pencil* pen) {
   if (!(eta > xi)) fail(SE_EINVAL, std::string(who) + ": degenerate interval");
   if (f.k < 1 || (int)f.mu.size() != f.k + 1) fail(SE_EINVAL, std::string(who) + ": malformed filter");
-  Slice s(c, a, f, xi, eta, cfg);
+  if (pen && ndefl > 0)
+    fail(SE_EINVAL, std::string(who) + ": a preloaded deflation set is not supported for B-pencils");
+  Slice s(c, a, f, xi, eta, cfg, pen);
   s.preload(ndefl, defl_u, defl_vals, who);
   return thick_restart ? run_tr(s) : run_nr(s);
 }

@@ -30,6 +30,17 @@ struct SolverCfg {  // SolverConfig after resolve_config (eigensolvers.hpp:142-1
 };
 SolverCfg resolve_config(const se_solver_cfg* in, const char* who);
 
+// A generalized pencil (A, B), B sparse SPD, solved as the standard problem S = P A P with
+// P ~ B^(-1/2): a Chebyshev least-squares series in B (ls_pol_approx, cheb_approx.hpp:40-88)
+// applied by the same fused SpMV recurrence as the filter (apply_cheb, :91-112).  The spectrum
+// of S is the pencil's; eigenvectors map back as x = P y (B-normalised), and candidate
+// residuals are the reference's ||A x - lambda B x|| / sqrt(x' B x) (eigensolvers.hpp:289-316).
+// Every B-solve of the reference's Cholesky path (cholesky.hpp) becomes B-products on the GPU.
+struct Pencil {
+  const DevCsr* B = nullptr;
+  StepOp P;  // plain = false, k = series degree, mu = coefficients, c / invd = the fit interval map
+};
+
 struct SliceResult {
   Vec eigenvalues, residuals;
   DevMat vectors;  // n x nev on the device (column i pairs with eigenvalues[i])
@@ -60,16 +71,19 @@ struct LanczosRun {
   Vec next_w;
   Vec basis;  // n x steps (optional)
 };
-LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m, bool want_basis);
+LanczosRun lanczos_run(Ctx& c, const DevCsr& a, const double* start_host, int m, bool want_basis,
+                       const Pencil* pen = nullptr);
 void lan_tr_bounds(Ctx& c, const DevCsr& a, double tol, int restart_dim, int max_restarts,
-                   std::uint64_t seed, double& lmin, double& lmax);
+                   std::uint64_t seed, double& lmin, double& lmax, const Pencil* pen = nullptr);
 
 // Polynomial filtered Lanczos slice drivers (run_nr eigensolvers.hpp:385-472 and run_tr
 // :481-628, wired as cheb_lan_nr/tr :703-732).  defl_u: host n x ndefl preloaded locked set.
 std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter& f, double xi,
                                       double eta, const SolverCfg& cfg, bool thick_restart,
                                       int ndefl, const double* defl_u, const double* defl_vals,
-                                      const char* who);
+                                      const char* who, const Pencil* pen = nullptr);
+// y = P x for nvec column-major vectors (the pencil's B^(-1/2) series; apply_cheb).
+void pencil_map(Ctx& c, const Pencil& pen, int nvec, const double* x, double* y);
 
 // Filtered subspace iteration (cheb_si, eigensolvers.hpp:760-940) on a block of
 // ceil(1.3 est_count) + 8 vectors; standard problems.

@@ -601,3 +601,53 @@ void arrow_to_tridiag(const Vec& theta, const Vec& s, double alpha_l, Vec& diag,
 }
 
 }  // namespace se
+
+namespace se {
+
+// Chebyshev least squares for B^-1 / B^-1/2 (cheb_approx.hpp:40-88): the normal equations of a
+// Chebyshev-weighted fit on Chebyshev nodes are diagonal, so each coefficient is a cosine sum.
+ChebFit ls_pol_approx(bool inverse_sqrt, double lmin, double lmax, double tol, int max_deg) {
+  if (lmin <= 0.0) fail(SE_EINVAL, "ls_pol_approx: interval must be positive (B must be SPD)");
+  if (lmax <= lmin) fail(SE_EINVAL, "ls_pol_approx: empty interval");
+  if (max_deg < 1) fail(SE_EINVAL, "ls_pol_approx: max_deg must be positive");
+  const double pi = 3.14159265358979323846;
+  const double mid = 0.5 * (lmax + lmin), half = 0.5 * (lmax - lmin);
+  auto fun = [&](double t) { return inverse_sqrt ? 1.0 / std::sqrt(t) : 1.0 / t; };
+  const int nodes = 4 * max_deg;
+  Vec node(nodes), fval(nodes);
+  for (int i = 0; i < nodes; ++i) {
+    node[i] = std::cos(pi * (i + 0.5) / nodes);
+    fval[i] = fun(mid + half * node[i]);
+  }
+  Vec coef(max_deg + 1);
+  for (int j = 0; j <= max_deg; ++j) {
+    double acc = 0.0;
+    for (int i = 0; i < nodes; ++i) acc += fval[i] * std::cos(j * std::acos(node[i]));
+    coef[j] = (j == 0 ? 1.0 : 2.0) * acc / nodes;
+  }
+  // Clenshaw evaluation of a truncation on the mapped argument
+  auto series = [&](int deg, double t) {
+    const double x = (t - mid) / half;
+    double b1 = 0.0, b2 = 0.0;
+    for (int j = deg; j >= 1; --j) {
+      const double b0 = 2.0 * x * b1 - b2 + coef[j];
+      b2 = b1;
+      b1 = b0;
+    }
+    return x * b1 - b2 + coef[0];
+  };
+  const int grid = 2000;
+  double worst = 0.0;
+  for (int deg = 1; deg <= max_deg; ++deg) {
+    worst = 0.0;
+    for (int i = 0; i <= grid; ++i) {
+      const double t = lmin + (lmax - lmin) * i / grid;
+      worst = std::max(worst, std::abs(series(deg, t) - fun(t)) / std::abs(fun(t)));
+    }
+    if (worst <= tol) return {Vec(coef.begin(), coef.begin() + deg + 1), worst};
+  }
+  fail(SE_ENUMERIC, "ls_pol_approx: tolerance not reached; best relative error " +
+                        std::to_string(worst) + " at degree " + std::to_string(max_deg));
+}
+
+}  // namespace se

@@ -94,6 +94,17 @@ double dos_cumulative(const Curve& c, double t);
 double dos_count(const Curve& c, double xi, double eta);
 void slice_spectrum(const Curve& c, double xi, double eta, int ns, Vec& bp, Vec& est);
 
+// ---- cheb_approx.hpp:40-88 -----------------------------------------------------------------
+// Chebyshev least-squares fit of 1/t (inverse_sqrt = false) or 1/sqrt(t) on [lmin, lmax] (> 0):
+// discrete cosine sums on 4 max_deg Chebyshev nodes, truncated at the smallest degree whose
+// relative error on a 2,001-point grid is <= tol.  Throws SE_EINVAL for a non-positive or
+// empty interval and SE_ENUMERIC when max_deg does not reach tol.
+struct ChebFit {
+  Vec coeff;  // degree = size - 1
+  double achieved = 0.0;
+};
+ChebFit ls_pol_approx(bool inverse_sqrt, double lmin, double lmax, double tol, int max_deg);
+
 // ---- tridiag_eig.hpp / dense_eig.hpp --------------------------------------------------------
 // Symmetric tridiagonal eigenproblem (implicit QL, Wilkinson shift); Z (m x m col-major) optional.
 void tridiag_ql(Vec& d, Vec& e, double* z, int ldz, int zrows);

@@ -171,6 +171,15 @@ void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W,
 // out3[3j..] = (lambda, residual, uu).  U is left unscaled (raw W y, kept for thick restart).
 void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3,
                      const double* w = nullptr);
+// Chebyshev filter degree on a precomputed product sx = S x (pencils; filter_poly.hpp:261-276).
+void cheb_combine(Ctx& c, int n, bool first, const double* sx, const double* x, const double* prev,
+                  double* y, double* out, double cc, double invd, double mu0, double muj,
+                  const Ctl* halt);
+// Pencil candidate statistics: out3[3j..] = (x.Ax / x.Bx, ||Ax - lambda Bx|| / sqrt(x.Bx), u.u).
+void pencil_stats(Ctx& c, int n, int nc, const double* U, const double* X, const double* AX,
+                  const double* BX, double* out3);
+// X[:, j] /= sqrt(X[:, j] . BX[:, j]).
+void b_normalize(Ctx& c, int n, int nc, double* X, const double* BX);
 void dot_dev(Ctx& c, const Scratch& s, int n, const double* x, const double* y, double* result_dev);
 void scale(Ctx& c, int n, double a, double* x);
 // dst = a * src (n doubles).

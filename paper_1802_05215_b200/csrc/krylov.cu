@@ -370,6 +370,84 @@ __global__ void __launch_bounds__(kThreads) k_candidate_stats(int n, double* __r
   }
 }
 
+// One Chebyshev degree of the filter on a precomputed operator product sx = S x (pencils, where
+// S = P A P is a composition and cannot be fused into the SpMV): the same update as the fused
+// kernel (filter_poly.hpp:261-276): t = (sx - c x) / d; first: y = t, out = mu0 x + mu1 t;
+// next: y = 2 t - prev, out += mu_j y.
+__global__ void k_cheb_combine(int n, int first, const double* __restrict__ sx,
+                               const double* __restrict__ x, const double* __restrict__ prev,
+                               double* __restrict__ y, double* __restrict__ out, double c,
+                               double invd, double mu0, double muj, const Ctl* halt) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (halt && halt->halted) return;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const double xr = x[r];
+    const double t = mul(sub(sx[r], mul(c, xr)), invd);
+    if (first) {
+      y[r] = t;
+      out[r] = add(add(0.0, mul(mu0, xr)), mul(muj, t));
+    } else {
+      const double tj = sub(mul(2.0, t), prev[r]);
+      y[r] = tj;
+      out[r] = add(out[r], mul(muj, tj));
+    }
+  }
+}
+
+// Pencil candidate statistics, one CTA per column (eigensolvers.hpp:289-316 with b != nullptr):
+// x = P u, ax = A x, bx = B x:  lambda = x.ax / x.bx, res = ||ax - lambda bx|| / sqrt(x.bx),
+// out3 = (lambda, res, u.u).
+__global__ void __launch_bounds__(kThreads) k_pencil_stats(int n, const double* __restrict__ U,
+                                                           const double* __restrict__ X,
+                                                           const double* __restrict__ AX,
+                                                           const double* __restrict__ BX,
+                                                           double* out3) {
+  const size_t off = (size_t)blockIdx.x * n;
+  const double *u = U + off, *x = X + off, *ax = AX + off, *bx = BX + off;
+  double suu = 0.0, sxa = 0.0, sxb = 0.0;
+  for (int r = threadIdx.x; r < n; r += kThreads) {
+    suu = add(suu, mul(u[r], u[r]));
+    sxa = add(sxa, mul(x[r], ax[r]));
+    sxb = add(sxb, mul(x[r], bx[r]));
+  }
+  __shared__ double s_uu, s_xb, s_lam;
+  double v = block_sum(suu);
+  if (threadIdx.x == 0) s_uu = v;
+  __syncthreads();
+  v = block_sum(sxb);
+  if (threadIdx.x == 0) s_xb = v;
+  __syncthreads();
+  v = block_sum(sxa);
+  if (threadIdx.x == 0) s_lam = s_xb > 0.0 ? v / s_xb : 0.0;
+  __syncthreads();
+  const double lam = s_lam;
+  double srr = 0.0;
+  for (int r = threadIdx.x; r < n; r += kThreads) {
+    const double q = add(ax[r], mul(-lam, bx[r]));
+    srr = add(srr, mul(q, q));
+  }
+  v = block_sum(srr);
+  if (threadIdx.x == 0) {
+    out3[3 * blockIdx.x + 0] = lam;
+    out3[3 * blockIdx.x + 1] = s_xb > 0.0 ? sqrt(v) / sqrt(s_xb) : 0.0;
+    out3[3 * blockIdx.x + 2] = s_uu;
+  }
+}
+
+// x_j *= 1 / sqrt(x_j . bx_j) per column (B-normalisation of returned pencil eigenvectors)
+__global__ void __launch_bounds__(kThreads) k_b_normalize(int n, double* __restrict__ X,
+                                                          const double* __restrict__ BX) {
+  const size_t off = (size_t)blockIdx.x * n;
+  double s = 0.0;
+  for (int r = threadIdx.x; r < n; r += kThreads) s = add(s, mul(X[off + r], BX[off + r]));
+  __shared__ double s_scale;
+  const double v = block_sum(s);
+  if (threadIdx.x == 0) s_scale = v > 0.0 ? 1.0 / sqrt(v) : 0.0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < n; r += kThreads) X[off + r] = mul(s_scale, X[off + r]);
+}
+
 __global__ void k_dot(int n, const double* __restrict__ x, const double* __restrict__ y,
                       double* result, double* partial, unsigned* cnt) {
   double s = 0.0;
@@ -562,6 +640,29 @@ void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W,
   const int g = grid_for(c, n);
   need(s, 0, kSlotMisc + 1);
   launch_pdl(c, k_normalize, dim3(g), dim3(kThreads), 0, n, t, W, ctl, beta_arr, s.cnt + kSlotNorm);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+void cheb_combine(Ctx& c, int n, bool first, const double* sx, const double* x, const double* prev,
+                  double* y, double* out, double cc, double invd, double mu0, double muj,
+                  const Ctl* halt) {
+  launch_pdl(c, k_cheb_combine, dim3(grid_for(c, n)), dim3(kThreads), 0, n, first ? 1 : 0, sx, x,
+             prev, y, out, cc, invd, mu0, muj, halt);
+  ++c.launches;
+}
+
+void pencil_stats(Ctx& c, int n, int nc, const double* U, const double* X, const double* AX,
+                  const double* BX, double* out3) {
+  if (nc <= 0) return;
+  k_pencil_stats<<<nc, kThreads, 0, c.stream>>>(n, U, X, AX, BX, out3);
+  ++c.launches;
+  SE_CUDA(cudaGetLastError());
+}
+
+void b_normalize(Ctx& c, int n, int nc, double* X, const double* BX) {
+  if (nc <= 0) return;
+  k_b_normalize<<<nc, kThreads, 0, c.stream>>>(n, X, BX);
   ++c.launches;
   SE_CUDA(cudaGetLastError());
 }

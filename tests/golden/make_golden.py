@@ -224,6 +224,54 @@ def landos():
     save("landos", **out)
 
 
+def kron_mass(nx):
+    """B = M1 (x) M1, M1 = tridiag(1, 4, 1) / 6 (1-D linear-element mass matrix): a 9-point SPD
+    matrix whose eigenvectors are those of the 2-D Laplacian (sine products), so the pencil
+    (Laplacian, B) has the closed-form spectrum (t_i + t_j) / (m_i m_j)."""
+    m1 = np.diag(np.full(nx, 4.0 / 6.0)) + np.diag(np.full(nx - 1, 1.0 / 6.0), 1) + \
+        np.diag(np.full(nx - 1, 1.0 / 6.0), -1)
+    Bd = np.kron(m1, m1)
+    rows, cols = np.nonzero(Bd)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    rp = np.zeros(nx * nx + 1, np.int32)
+    np.add.at(rp, rows + 1, 1)
+    return np.cumsum(rp).astype(np.int32), cols.astype(np.int32), Bd[rows, cols].astype(np.float64)
+
+
+def pencil_general():
+    """The reference's B-weighted drivers (Cholesky B-solves) on a non-diagonal SPD B."""
+    nx = 30
+    rp, ci, v = reflib.laplacian([nx, nx])
+    brp, bci, bv = kron_mass(nx)
+    th = np.arange(1, nx + 1) * np.pi / (nx + 1)
+    t = 2.0 - 2.0 * np.cos(th)
+    m = (4.0 + 2.0 * np.cos(th)) / 6.0
+    ev = np.sort(((t[:, None] + t[None, :]) / (m[:, None] * m[None, :])).ravel())
+    lo, hi = reflib.pencil_bounds(rp, ci, v, brp, bci, bv, seed=1234)
+    x, y, nev = reflib.pencil_dos(rp, ci, v, brp, bci, bv, lo, hi, m=60, n_vec=40, npts=300, seed=1234)
+    out = dict(brp=brp, bci=bci, bv=bv, analytic=ev, bounds=[lo, hi], dos_x=x, dos_y=y, dos_nev=nev)
+    for q, (xi, eta) in enumerate([(2.0, 3.0), (10.0, 11.5)]):
+        est = int(((ev >= xi) & (ev <= eta)).sum())
+        for solver in ("tr", "nr"):
+            r = reflib.cheb_lan_pencil_csr(rp, ci, v, brp, bci, bv, solver, xi, eta, lo, hi,
+                                           est_count=est, seed=1234)
+            out[f"{solver}{q}_vals"] = r["eigenvalues"]
+            out[f"{solver}{q}_res"] = r["residuals"]
+            out[f"{solver}{q}_meta"] = [r["niter"], r["n_A_matvec"], r["degree"],
+                                        int(r["hit_max_its"]), xi, eta, est]
+    # ls_pol_approx KATs (test_operators.cpp:162-225 shapes)
+    for q, (fun, a, b, tol) in enumerate([("inverse", 1.0, 2.0, 1e-8), ("inverse_sqrt", 0.5, 2.0, 1e-9),
+                                          ("inverse", 1.0 / 3.0 - 1e-3, 1.0 + 1e-3, 1e-12),
+                                          ("inverse_sqrt", 0.1, 1.05, 1e-13)]):
+        co, ach = reflib.ls_pol_approx(fun, a, b, tol)
+        out[f"lsq{q}_coeff"] = co
+        out[f"lsq{q}_meta"] = [1.0 if fun == "inverse_sqrt" else 0.0, a, b, tol, ach]
+        xv = np.cos(np.arange(brp.size - 1) * 0.37)
+        out[f"lsq{q}_apply"] = reflib.apply_cheb(brp, bci, bv, fun, a, b, co, xv)
+    save("pencil_general", **out)
+
+
 def cli():
     """`sliceeig solve --dims 30,30 --interval 0.4,0.6 --slices 4 [--solver tr]` with the CLI
     defaults (KPM deg 60 x 40 Rademacher probes, sigma damping, tol 1e-8, seed 1234): the
@@ -254,7 +302,7 @@ def cli():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-solve", action="store_true")
-    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli,pencil,landos")
+    ap.add_argument("--only", default="kats,cfg1,cfg2,cfg4p,cfg5p,cli,pencil,landos,pencil_general")
     a = ap.parse_args()
     only = a.only.split(",")
     if "kats" in only:
@@ -273,3 +321,5 @@ if __name__ == "__main__":
         pencil()
     if "landos" in only:
         landos()
+    if "pencil_general" in only:
+        pencil_general()

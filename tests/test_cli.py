@@ -219,3 +219,36 @@ def test_filter_dump_curve(tmp_path):
 def test_solve_errors(tmp_path):
     assert run(f"solve --dims 6,6 --interval 50,60 --out {tmp_path}")[0] != 0  # outside spectrum
     assert run(f"solve --dims 6,6 --interval 0.4,0.6 --filter rat --out {tmp_path}")[0] != 0
+
+
+def _write_mtx(path, rp, ci, v):
+    """Symmetric MatrixMarket (lower triangle), as the reference's write_matrix_market."""
+    n = len(rp) - 1
+    ent = [(i + 1, int(ci[p]) + 1, float(v[p])) for i in range(n) for p in range(rp[i], rp[i + 1])
+           if ci[p] <= i]
+    with open(path, "w") as f:
+        f.write(f"%%MatrixMarket matrix coordinate real symmetric\n{n} {n} {len(ent)}\n")
+        for i, j, x in ent:
+            f.write(f"{i} {j} {x:.17g}\n")
+
+
+@pytest.mark.gpu
+def test_solve_generalized_pencil(tmp_path, golden):
+    """test_cli.cpp:226-241: `solve --matrix a.mtx --bmatrix b.mtx --method lanczos`, here with a
+    non-diagonal SPD B (the linear-element mass matrix of tests/golden/pencil_general.npz): the
+    pencil's closed-form eigenvalues in the interval, slices seam-trimmed, exit status 0; KPM
+    refuses a pencil as the reference does."""
+    g = golden("pencil_general")
+    a = api.gen_laplacian([30, 30])
+    _write_mtx(tmp_path / "a.mtx", a.row_ptr, a.col_idx, a.vals)
+    _write_mtx(tmp_path / "b.mtx", g["brp"], g["bci"], g["bv"])
+    rep = ok_json(f"solve --matrix {tmp_path}/a.mtx --bmatrix {tmp_path}/b.mtx --method lanczos "
+                  f"--interval 2.0,3.0 --slices 2 --solver tr --out {tmp_path}")
+    ev = g["analytic"]
+    truth = ev[(ev >= 2.0) & (ev <= 3.0)]
+    got = union(rep)
+    assert got.size == truth.size and np.all(np.abs(got - truth) <= 1e-10 * truth)
+    assert rep["converged"] is True
+    rc, _, err = run(f"solve --matrix {tmp_path}/a.mtx --bmatrix {tmp_path}/b.mtx --method kpm "
+                     f"--interval 2.0,3.0 --out {tmp_path}")
+    assert rc == 1 and "pencil" in err

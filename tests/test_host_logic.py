@@ -159,3 +159,20 @@ def test_csr_from_triplets_semantics():
         api.CsrMatrix.from_triplets(2, [0], [2], [1.0])
     with pytest.raises(ValueError):
         api.CsrMatrix.from_triplets(-1, [], [], [])
+
+
+@pytest.mark.parametrize("q", [0, 1, 2, 3])
+def test_ls_pol_approx_matches_reference(golden, q):
+    """ls_pol_approx (cheb_approx.hpp:40-88, host): degree and coefficients of the reference's
+    fits (tests/golden/pencil_general.npz)."""
+    g = golden("pencil_general")
+    fun, a, b, tol, ach = g[f"lsq{q}_meta"]
+    co, got = api.ls_pol_approx("inverse_sqrt" if fun else "inverse", api.SpectralBounds(a, b), tol)
+    ref = g[f"lsq{q}_coeff"]
+    assert co.size == ref.size
+    assert np.max(np.abs(co - ref)) <= 1e-14 * np.max(np.abs(ref))
+    assert got <= tol and abs(got - ach) <= 1e-3 * tol
+    with pytest.raises(ValueError):
+        api.ls_pol_approx("inverse", api.SpectralBounds(-0.5, 2.0), 1e-8)
+    with pytest.raises(RuntimeError):
+        api.ls_pol_approx("inverse", api.SpectralBounds(1e-4, 1.0), 1e-14, 6)

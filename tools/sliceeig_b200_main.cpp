@@ -7,7 +7,8 @@
 // Exit status is 0 only when every requested slice converged.
 //
 // In scope: polynomial filters with the nr / tr / si drivers, KPM or Lanczos densities, standard
-// problems.  Rational filters and B-pencils are reported as errors (nonzero exit), as the
+// problems and generalized pencils (--bmatrix: a sparse SPD B, solved on the device as
+// S = P A P with P ~ B^-1/2).  Rational filters are reported as errors (nonzero exit), as the
 // reference does for invalid combinations.  B200 extension: --gpus N spreads the slice pool over
 // N GPUs of the node (worker thread w on GPU w mod N) and splits the KPM probes over them with one
 // NCCL all-reduce of the moments (kpm_dos_devices).
@@ -21,6 +22,7 @@
 #include <fstream>
 #include <iostream>
 #include <map>
+#include <optional>
 #include <set>
 #include <sstream>
 #include <string>
@@ -178,27 +180,50 @@ Manifest parse(const std::string& cmd, const std::vector<std::string>& args) {
 }
 
 // ---- shared pipeline stages (sliceeig_main.cpp:112-195) ---------------------------------------
-CsrMatrix load_problem(const Manifest& m) {
+// The problem of a run: A, and B for a generalized pencil (--bmatrix, sliceeig_main.cpp:112-125).
+struct Problem {
+  CsrMatrix a;
+  std::optional<CsrMatrix> b;
+  const CsrMatrix* bp() const { return b ? &*b : nullptr; }
+};
+
+Problem load_problem(const Manifest& m) {
   if (m.matrix_path.empty() == m.dims.empty())
     throw UsageError("input: exactly one of --matrix and --dims is required");
-  if (!m.bmatrix_path.empty())
-    throw std::invalid_argument("generalized pencils (--bmatrix) are outside the B200 build");
-  return m.dims.empty() ? read_matrix_market(m.matrix_path) : gen_laplacian(m.dims);
+  Problem p;
+  p.a = m.dims.empty() ? read_matrix_market(m.matrix_path) : gen_laplacian(m.dims);
+  if (!m.bmatrix_path.empty()) {
+    p.b = read_matrix_market(m.bmatrix_path);
+    if (p.b->n() != p.a.n()) throw std::invalid_argument("A and B sizes differ");
+  }
+  return p;
 }
 
-SpectralBounds estimate_bounds(const CsrMatrix& a, unsigned long seed) {
-  return lan_tr_bounds(make_operator(a), InnerProduct{}, 1e-4, 60, 40, seed);
+// Bounds in the problem's inner product (sliceeig_main.cpp:128-136); for a pencil the device
+// path uses B's CSR matrix instead of a Cholesky solve.
+SpectralBounds estimate_bounds(const Problem& p, unsigned long seed) {
+  const Operator opa = make_operator(p.a);
+  if (!p.b) return lan_tr_bounds(opa, InnerProduct{}, 1e-4, 60, 40, seed);
+  const Operator opb = make_operator(*p.b);
+  InnerProduct ip;
+  ip.b = &opb;
+  return lan_tr_bounds(opa, ip, 1e-4, 60, 40, seed);
 }
 
-DosCurve estimate_dos(const CsrMatrix& a, const SpectralBounds& b, const Manifest& m) {
+DosCurve estimate_dos(const Problem& p, const SpectralBounds& b, const Manifest& m) {
   DosConfig cfg;
   cfg.method = m.method == "kpm" ? DosMethod::Kpm : DosMethod::Lanczos;
   cfg.m = m.dos_deg;
   cfg.n_vec = m.dos_vecs;
   cfg.npts = m.dos_npts;
   cfg.seed = m.seed;
-  const Operator op = make_operator(a);
-  return cfg.method == DosMethod::Kpm ? kpm_dos(op, b, cfg) : lan_dos(op, b, cfg);
+  const Operator op = make_operator(p.a);
+  if (!p.b) return cfg.method == DosMethod::Kpm ? kpm_dos(op, b, cfg) : lan_dos(op, b, cfg);
+  if (cfg.method == DosMethod::Kpm)
+    throw std::invalid_argument("kpm density estimation handles standard problems only; "
+                                "use --method lanczos for a pencil");
+  const Operator opb = make_operator(*p.b);
+  return dos_generalized(op, opb, opb, opb, b, cfg);
 }
 
 void write_text(const fs::path& path, const std::string& body) {
@@ -263,7 +288,7 @@ int cmd_gen(const Manifest& m) {
 }
 
 int cmd_bounds(const Manifest& m) {
-  const CsrMatrix a = load_problem(m);
+  const Problem a = load_problem(m);
   const SpectralBounds b = estimate_bounds(a, m.seed);
   Json r = Json::object();
   r["schema"] = 1;
@@ -276,7 +301,7 @@ int cmd_bounds(const Manifest& m) {
 }
 
 int cmd_dos(const Manifest& m) {
-  const CsrMatrix a = load_problem(m);
+  const Problem a = load_problem(m);
   const SpectralBounds b = estimate_bounds(a, m.seed);
   const DosCurve curve = estimate_dos(a, b, m);
   double nev = curve.nev_est;
@@ -315,7 +340,7 @@ SliceSet slice_clipped(const DosCurve& curve, double xi, double eta, int ns) {
 
 int cmd_slice(const Manifest& m) {
   m.require_interval();
-  const CsrMatrix a = load_problem(m);
+  const Problem a = load_problem(m);
   const SpectralBounds b = estimate_bounds(a, m.seed);
   const DosCurve curve = estimate_dos(a, b, m);
   const SliceSet s = slice_clipped(curve, m.interval[0], m.interval[1], m.slices);
@@ -350,7 +375,7 @@ int cmd_slice(const Manifest& m) {
 int cmd_filter_dump(const Manifest& m) {
   m.require_interval();
   require_poly(m);
-  const CsrMatrix a = load_problem(m);
+  const Problem a = load_problem(m);
   const SpectralBounds b = estimate_bounds(a, m.seed);
   const double lo = m.interval[0], hi = m.interval[1];
   PolyOpts po;
@@ -430,25 +455,25 @@ EigenResults select_pairs(const EigenResults& r, const std::vector<int>& pick) {
   return out;
 }
 
-using SliceDriver = EigenResults (*)(const CsrMatrix&, const PolynomialFilter&, const SliceJob&,
+using SliceDriver = EigenResults (*)(const Problem&, const PolynomialFilter&, const SliceJob&,
                                      const SolverConfig&);
 SliceDriver driver_for(const std::string& solver) {
   if (solver == "tr")
-    return [](const CsrMatrix& a, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
-      return cheb_lan_tr(a, nullptr, f, j.lo, j.hi, c);
+    return [](const Problem& p, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
+      return cheb_lan_tr(p.a, p.bp(), f, j.lo, j.hi, c);
     };
   if (solver == "si")
-    return [](const CsrMatrix& a, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
-      return cheb_si(a, nullptr, f, j.lo, j.hi, c.est_count, c);
+    return [](const Problem& p, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
+      return cheb_si(p.a, p.bp(), f, j.lo, j.hi, c.est_count, c);
     };
-  return [](const CsrMatrix& a, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
-    return cheb_lan_nr(a, nullptr, f, j.lo, j.hi, c);
+  return [](const Problem& p, const PolynomialFilter& f, const SliceJob& j, const SolverConfig& c) {
+    return cheb_lan_nr(p.a, p.bp(), f, j.lo, j.hi, c);
   };
 }
 
 class SlicePool {
  public:
-  SlicePool(const CsrMatrix& a, const SpectralBounds& b, const Manifest& m, SeamOwner seams)
+  SlicePool(const Problem& a, const SpectralBounds& b, const Manifest& m, SeamOwner seams)
       : a_(a), bounds_(b), m_(m), seams_(seams), drive_(driver_for(m.solver)) {}
 
   std::vector<SliceRun> run(const std::vector<SliceJob>& jobs, int workers) {
@@ -496,7 +521,7 @@ class SlicePool {
     return mine.size() == r.eigenvalues.size() ? std::move(r) : select_pairs(r, mine);
   }
 
-  const CsrMatrix& a_;
+  const Problem& a_;
   const SpectralBounds& bounds_;
   const Manifest& m_;
   SeamOwner seams_;
@@ -606,8 +631,8 @@ std::string pairs_csv(const std::vector<SliceRun>& runs) {
 
 // The density for solve: with --gpus N > 1 and KPM the probes are split over the GPUs and the
 // moments combined by one NCCL all-reduce (bit-identical to the single-GPU curve).
-DosCurve solve_dos(const CsrMatrix& a, const SpectralBounds& b, const Manifest& m) {
-  if (m.gpus <= 1 || m.method != "kpm") return estimate_dos(a, b, m);
+DosCurve solve_dos(const Problem& a, const SpectralBounds& b, const Manifest& m) {
+  if (m.gpus <= 1 || m.method != "kpm" || a.b) return estimate_dos(a, b, m);
   DosConfig cfg;
   cfg.m = m.dos_deg;
   cfg.n_vec = m.dos_vecs;
@@ -615,7 +640,7 @@ DosCurve solve_dos(const CsrMatrix& a, const SpectralBounds& b, const Manifest& 
   cfg.seed = m.seed;
   std::vector<int> devices(m.gpus);
   for (int g = 0; g < m.gpus; ++g) devices[g] = g;
-  return kpm_dos_devices(a, b, cfg, devices);
+  return kpm_dos_devices(a.a, b, cfg, devices);
 }
 
 int cmd_solve(const Manifest& m) {
@@ -623,7 +648,7 @@ int cmd_solve(const Manifest& m) {
   m.require_interval();
   require_poly(m);
   const double xi = m.interval[0], eta = m.interval[1];
-  const CsrMatrix a = load_problem(m);
+  const Problem a = load_problem(m);
   const double t_load = since(t0);
   auto tb = std::chrono::steady_clock::now();
   const SpectralBounds bounds = estimate_bounds(a, m.seed);
