@@ -299,6 +299,9 @@ SE_API int se_cheb_lan_pencil(se_ctx* ctx, const se_csr* a, const se_pencil* p,
 SE_API int se_results_count(const se_results* r, int* nev);
 /* eigenvalues/residuals (nev each, ascending by eigenvalue), vectors (n x nev, may be NULL). */
 SE_API int se_results_copy(const se_results* r, double* eigenvalues, double* residuals, double* vectors);
+/* One eigenvector (n doubles; EigenResults.vectors column `index`, eigensolvers.hpp:75-82):
+   lets a caller walk a result too large for one host block. */
+SE_API int se_results_vector(const se_results* r, int index, double* vector);
 SE_API int se_results_info(const se_results* r, long* niter, int* hit_max_its, se_counters* counters);
 /* Reorthogonalisation accounting of a slice solve (extension, measurement only): projection
    passes over the Krylov basis, basis columns summed over them, algorithmic HBM bytes. */

@@ -124,6 +124,7 @@ SIGNATURES = {
                     C.POINTER(SeSolverCfg), C.c_int, C.c_int, _PD, _PD, C.c_int, C.POINTER(_VP)],
     "se_results_count": [_VP, _PI],
     "se_results_copy": [_VP, _PD, _PD, _PD],
+    "se_results_vector": [_VP, C.c_int, _PD],
     "se_results_info": [_VP, _PL, _PI, C.POINTER(SeCounters)],
     "se_results_free": [_VP],
     "se_rayleigh_residual": [_VP, _VP, _PD, _PD, _PD],

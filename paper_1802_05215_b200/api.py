@@ -733,6 +733,8 @@ class EigenResults:
     counters: Counters
     hit_max_its: bool
     orth: OrthStats = field(default_factory=OrthStats)
+    sample_index: Optional[np.ndarray] = None    # with want_vectors=False and SAMPLE_VECTORS > 0
+    sample_vectors: Optional[np.ndarray] = None  # (n, len(sample_index))
 
 
 def _host_buffer(shape):
@@ -880,7 +882,14 @@ def _d_matvec(d: "DeviceCsr", x) -> np.ndarray:
     return y
 
 
+# With want_vectors=False a driver still returns this many evenly spaced eigenvectors
+# (EigenResults.sample_index / sample_vectors) for spot checks of results too large to download
+# whole (SURVEY.md §8c, cfg4/cfg5 at full size).  0: none.
+SAMPLE_VECTORS = 0
+
+
 def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
+    sample_idx, sample_vecs = None, None
     try:
         nev = C.c_int()
         call("se_results_count", h, C.byref(nev))
@@ -890,6 +899,11 @@ def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
         vecs = _host_buffer((k, d.n)) if (want_vectors and k) else None
         call("se_results_copy", h, _pd(vals) if k else None, _pd(res) if k else None,
              _pd(vecs) if vecs is not None else None)
+        if not want_vectors and SAMPLE_VECTORS > 0 and k:
+            sample_idx = np.unique(np.linspace(0, k - 1, min(k, SAMPLE_VECTORS)).astype(np.int64))
+            sample_vecs = np.empty((sample_idx.size, d.n))
+            for q, j in enumerate(sample_idx):
+                call("se_results_vector", h, int(j), _pd(sample_vecs[q]))
         niter, hit = C.c_long(), C.c_int()
         cn = _lib.SeCounters()
         call("se_results_info", h, C.byref(niter), C.byref(hit), C.byref(cn))
@@ -901,7 +915,8 @@ def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
                         cn.t_orth, cn.t_sv, cn.t_total)
     return EigenResults(vals, vecs.T if vecs is not None else (np.zeros((d.n, 0)) if want_vectors else None),
                         res, niter.value, counters, bool(hit.value),
-                        OrthStats(op.value, oc.value, ob.value))
+                        OrthStats(op.value, oc.value, ob.value), sample_idx,
+                        sample_vecs.T if sample_vecs is not None else None)
 
 
 def cheb_si(a, b, f: PolynomialFilter, xi: float, eta: float, est_count: int,

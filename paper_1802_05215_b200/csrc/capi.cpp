@@ -1142,6 +1142,18 @@ int se_results_copy(const se_results* r, double* eigenvalues, double* residuals,
   });
 }
 
+int se_results_vector(const se_results* r, int index, double* vector) {
+  return guard([&] {
+    if (!r || !vector) fail(SE_EINVAL, "se_results_vector: null argument");
+    const SliceResult& s = *r->r;
+    if (index < 0 || index >= (int)s.eigenvalues.size())
+      fail(SE_ERANGE, "se_results_vector: eigenpair index out of range");
+    SE_CUDA(cudaSetDevice(r->device));
+    SE_CUDA(cudaMemcpy(vector, s.vectors.col(index), sizeof(double) * (size_t)s.n,
+                       cudaMemcpyDeviceToHost));
+  });
+}
+
 int se_results_info(const se_results* r, long* niter, int* hit_max_its, se_counters* counters) {
   return guard([&] {
     if (!r) fail(SE_EINVAL, "null results");

@@ -125,6 +125,14 @@ struct Krylov {
       dev_free(p);
   }
 
+  // End of the recurrence: the step graphs and the basis are released (the locked set stays).
+  void release_basis() {
+    drop_graph();
+    ctx_sync(c);
+    dev_free(W.p);
+    W = RowBasis{};
+  }
+
   void drop_graph() {
     if (!graphs.empty()) ctx_sync(c);
     for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
@@ -466,6 +474,13 @@ struct CandBuf {
     devmat_free(BX);
     dev_free(stats);
   }
+  void release() {
+    cudaStreamSynchronize(c.stream);
+    devmat_free(U);
+    devmat_free(AU);
+    devmat_free(X);
+    devmat_free(BX);
+  }
   // U = W[:, :steps] Y (Y steps x nc, ld ldy), AU = A U, stats per column.  W is column-major
   // (ld n) when w_row_ld == 0, else the row-major Krylov basis with row stride w_row_ld.
   void eval(const DevCsr& A, const double* W, int steps, const double* Y, int ldy, int nc,
@@ -657,15 +672,46 @@ struct Slice {
     std::sort(idx.begin(), idx.end(),
               [&](int i, int j) { return lock_val[preloaded + i] < lock_val[preloaded + j]; });
     r->n = A.n;
-    if (k > 0) devmat_reserve(c, r->vectors, A.n, k, false);
     for (int q = 0; q < k; ++q) {
-      const int src = preloaded + idx[q];
-      r->eigenvalues.push_back(lock_val[src]);
-      r->residuals.push_back(lock_res[src]);
-      SE_CUDA(cudaMemcpyAsync(r->vectors.col(q), kr.L.col(src), sizeof(double) * A.n,
-                              cudaMemcpyDeviceToDevice, c.stream));
+      r->eigenvalues.push_back(lock_val[preloaded + idx[q]]);
+      r->residuals.push_back(lock_res[preloaded + idx[q]]);
     }
-    ctx_sync(c);
+    // the recurrence is over: its basis, candidate and restart blocks go before the result is
+    // formed (at n ~ 2M the locked set alone is 80+ GB and must not meet a second copy of itself)
+    kr.release_basis();
+    cand.release();
+    devmat_free(trbuf);
+    if (preloaded == 0 && k > 0) {
+      // the locked set becomes the result: columns permuted in place into ascending order
+      // (cycle by cycle through one staging column), then the buffer changes owner
+      std::vector<char> done(k, 0);
+      const size_t colb = sizeof(double) * (size_t)A.n;
+      for (int s0 = 0; s0 < k; ++s0) {
+        if (done[s0] || idx[s0] == s0) {
+          done[s0] = 1;
+          continue;
+        }
+        SE_CUDA(cudaMemcpyAsync(kr.t, kr.L.col(s0), colb, cudaMemcpyDeviceToDevice, c.stream));
+        int j = s0;
+        while (idx[j] != s0) {
+          SE_CUDA(cudaMemcpyAsync(kr.L.col(j), kr.L.col(idx[j]), colb, cudaMemcpyDeviceToDevice,
+                                  c.stream));
+          done[j] = 1;
+          j = idx[j];
+        }
+        SE_CUDA(cudaMemcpyAsync(kr.L.col(j), kr.t, colb, cudaMemcpyDeviceToDevice, c.stream));
+        done[j] = 1;
+      }
+      ctx_sync(c);
+      r->vectors = kr.L;
+      kr.L = DevMat{};
+    } else {
+      if (k > 0) devmat_reserve(c, r->vectors, A.n, k, false);
+      for (int q = 0; q < k; ++q)
+        SE_CUDA(cudaMemcpyAsync(r->vectors.col(q), kr.L.col(preloaded + idx[q]),
+                                sizeof(double) * A.n, cudaMemcpyDeviceToDevice, c.stream));
+      ctx_sync(c);
+    }
     if (pen && k > 0) {  // eigenvectors of the pencil: x = P y, B-normalised
       DevMat X, BX;
       devmat_reserve(c, X, A.n, k, false);
@@ -1187,6 +1233,10 @@ std::unique_ptr<SliceResult> cheb_lan(Ctx& c, const DevCsr& a, const PolyFilter&
     fail(SE_EINVAL, std::string(who) + ": a preloaded deflation set is not supported for B-pencils");
   Slice s(c, a, f, xi, eta, cfg, pen);
   s.preload(ndefl, defl_u, defl_vals, who);
+  // a large locked set is reserved once from the estimate (+15% for the DOS estimate's error):
+  // regrowing an 80 GB block needs the old and the new copy at once
+  const int lock_est = ndefl + cfg.est_count + cfg.est_count * 3 / 20 + 64;
+  if ((size_t)a.n * lock_est * 8 > kBigAlloc) s.kr.reserve_locked(lock_est);
   return thick_restart ? run_tr(s) : run_nr(s);
 }
 

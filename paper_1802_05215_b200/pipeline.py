@@ -373,7 +373,8 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
 
     sink(slice_index, window_index, window, eigenvalues, residuals, vectors): optional consumer
     called on the owning rank as each solve window finishes (seam-trimmed; vectors (n, k) on the
-    host when plan.want_vectors).  With a sink the eigenvectors are streamed to it -- e.g. written
+    host when plan.want_vectors, else None -- or, with api.SAMPLE_VECTORS set, the pair
+    (positions, (n, s) sample vectors) for spot checks of a result too large to download).  With a sink the eigenvectors are streamed to it -- e.g. written
     out like the CLI's vectors_<i>.bin -- instead of being accumulated, so neither device nor host
     memory has to hold a whole large slice.  A sink returning True stops that slice after the
     current window (a bounded partial solve)."""
@@ -458,6 +459,13 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
                     out.orth_bytes += orth.bytes
                 out.windows.append(Window(wlo, whi, float(west), k, int(wk.size), r.niter,
                                           time.perf_counter() - tw, r.hit_max_its))
+                if wv is None and getattr(r, "sample_vectors", None) is not None:
+                    # want_vectors=False with api.SAMPLE_VECTORS: the spot-check sample, as
+                    # (positions into this window's kept eigenvalues, (n, s) vectors)
+                    pos = {int(j): q for q, j in enumerate(wk)}
+                    sel = [q for q, j in enumerate(r.sample_index) if int(j) in pos]
+                    wv = (np.array([pos[int(r.sample_index[q])] for q in sel], np.int64),
+                          r.sample_vectors[:, sel])
                 del r
                 stop = sink is not None and sink(i, w, out.windows[-1], vals[-1], ress[-1], wv)
                 del wv

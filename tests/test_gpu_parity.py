@@ -434,12 +434,26 @@ def test_diagonal_pencil_matches_reference(gpu_ctx, golden, solver):
         assert abs(lam - r.eigenvalues[j]) <= 1e-10 * abs(lam) and res <= 1e-8
 
 
-def test_non_diagonal_pencil_rejected(gpu_ctx):
+def test_non_diagonal_pencil_solved(gpu_ctx):
+    """A non-diagonal SPD B (round 1 rejected it) goes through the Chebyshev B^-1/2 series
+    (cheb_approx.hpp:40-112): counts and eigenvalues against a dense generalized eigensolve."""
+    import scipy.linalg
     api = _api()
     A = api.gen_laplacian([6, 6])
-    with pytest.raises(ValueError):
-        api.cheb_lan_tr(A, api.CsrMatrix.tridiag_toeplitz(36, 0.1, 2.0),
-                        api.find_pol(0.5, 0.8, api.SpectralBounds(0.0, 8.0)), 0.5, 0.8)
+    B = api.CsrMatrix.tridiag_toeplitz(36, 0.1, 2.0)
+    r = api.cheb_lan_tr(A, B, api.find_pol(0.6, 1.6, api.SpectralBounds(0.0, 8.0)), 0.6, 1.6)
+
+    def dense(M):
+        D = np.zeros((M.n, M.n))
+        for i in range(M.n):
+            for p in range(M.row_ptr[i], M.row_ptr[i + 1]):
+                D[i, M.col_idx[p]] = M.vals[p]
+        return D
+    ev = scipy.linalg.eigh(dense(A), dense(B), eigvals_only=True)
+    truth = ev[(ev >= 0.6) & (ev <= 1.6)]
+    assert r.eigenvalues.size == truth.size and truth.size > 0
+    assert np.all(np.abs(r.eigenvalues - truth) <= 1e-10 * np.abs(truth))
+    assert np.all(r.residuals <= 1e-8 * np.maximum(1.0, np.abs(r.eigenvalues)))
 
 
 @pytest.mark.parametrize("m,first,count", [(300, 16, 2), (40, 32, 16)])
