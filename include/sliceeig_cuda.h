@@ -166,6 +166,12 @@ SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
 /* A full CGS2 step with the re-pass forced: mode 0 = two column-major passes (4 reads of W),
  * mode 2 = the product path on the row-major basis, T1 + fused MID + N2 (3 reads); mode -1 =
  * one column-major pass. */
+/* mult_cols (vecops.hpp:81-89) / the Rayleigh-Ritz contractions (eigensolvers.hpp:275-283,
+ * 838-871) on the fp64 tensor cores: out (m x n, column-major, ldc) = A B, B[k + col ldb],
+ * A[row lda + k] (a_kcontig) or A[row + k lda]; host buffers.  With a or b NULL the operands are
+ * synthetic and nothing is copied back (timing); reps > 0: mean device ms of `reps` runs -> *ms. */
+SE_API int se_mult_cols(se_ctx* ctx, int m, int n, int k, const double* a, long lda, int a_kcontig,
+                        const double* b, long ldb, double* out, long ldc, int reps, double* ms);
 SE_API int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms);
 
 /* Production timing of kdeg degrees of the multi-vector filter (nv <= 8 recurrences sharing one

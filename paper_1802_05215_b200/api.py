@@ -888,6 +888,32 @@ def _d_matvec(d: "DeviceCsr", x) -> np.ndarray:
 SAMPLE_VECTORS = 0
 
 
+def mult_cols(a: np.ndarray, b: np.ndarray, a_rowmajor: bool = True, ctx=None) -> np.ndarray:
+    """out = A @ B on the GPU's fp64 tensor cores (mult_cols vecops.hpp:81-89; the Ritz
+    combination U = W Y of eigensolvers.hpp:275-283).  a: (m, k) C-contiguous (the row-major
+    Krylov-basis layout) or, with a_rowmajor=False, F-contiguous; b: (k, n), returned (m, n)."""
+    ctx = ctx or default_context(0)
+    a = np.asarray(a, np.float64)
+    m, k = a.shape
+    a = np.ascontiguousarray(a) if a_rowmajor else np.asfortranarray(a)
+    bf = np.asfortranarray(np.asarray(b, np.float64))
+    n = bf.shape[1]
+    out = np.empty((m, n), order="F")
+    call("se_mult_cols", ctx.handle, m, n, k, a.ctypes.data_as(_PD), k if a_rowmajor else m,
+         int(a_rowmajor), bf.ctypes.data_as(_PD), k, out.ctypes.data_as(_PD), m, 0, None)
+    return out
+
+
+def mult_cols_bench(m: int, n: int, k: int, a_rowmajor: bool = True, reps: int = 5, ctx=None) -> float:
+    """Mean device milliseconds of one (m x k)(k x n) Ritz contraction on synthetic operands."""
+    ctx = ctx or default_context(0)
+    ms = C.c_double()
+    dummy = np.zeros(1)
+    call("se_mult_cols", ctx.handle, m, n, k, None, k + (k & 1) if a_rowmajor else m, int(a_rowmajor),
+         None, k, dummy.ctypes.data_as(_PD), m, reps, C.byref(ms))
+    return ms.value
+
+
 def _collect_results(h, d, want_vectors: bool) -> "EigenResults":
     sample_idx, sample_vecs = None, None
     try:

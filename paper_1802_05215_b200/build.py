@@ -4,7 +4,7 @@
 
 Every translation unit in csrc/ is compiled by nvcc with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` (host code through the host compiler),
-then linked into ``paper_1802_05215_b200/libsliceeig_cuda.so`` against cuBLAS / cuSOLVER / cudart.
+then linked into ``paper_1802_05215_b200/libsliceeig_cuda.so`` against cuSOLVER / cudart.
 Object files go to ``paper_1802_05215_b200/_build`` (git-ignored); the .so travels with the repo
 snapshot to the GPU box.
 """
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if (force or not os.path.exists(LIB)
             or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, f"-L{os.path.join(CUDA, 'lib64')}",
-               "-lcublas", "-lcusolver", "-lcudart",
+               "-lcusolver", "-lcudart",
                "-Xlinker", f"-rpath={os.path.join(CUDA, 'lib64')}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -493,6 +493,49 @@ int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms) {
   });
 }
 
+int se_mult_cols(se_ctx* ctx, int m, int n, int k, const double* a, long lda, int a_kcontig,
+                 const double* b, long ldb, double* out, long ldc, int reps, double* ms) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (m < 0 || n < 0 || k < 0 || !out) fail(SE_EINVAL, "mult_cols: bad shape");
+    const size_t na = a_kcontig ? (size_t)(m - 1) * lda + k : (size_t)(k - 1) * lda + m;
+    const size_t nb = (size_t)(n - 1) * ldb + k, nc = (size_t)(n - 1) * ldc + m;
+    double* da = dev_alloc<double>(std::max<size_t>(na, 1));
+    double* db = dev_alloc<double>(std::max<size_t>(nb, 1));
+    double* dc = dev_alloc<double>(std::max<size_t>(nc, 1));
+    if (a) {
+      SE_CUDA(cudaMemcpyAsync(da, a, sizeof(double) * na, cudaMemcpyHostToDevice, c.stream));
+    } else {  // timing only: synthetic operands
+      SE_CUDA(cudaMemsetAsync(da, 0x3c, sizeof(double) * na, c.stream));
+    }
+    if (b)
+      SE_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * nb, cudaMemcpyHostToDevice, c.stream));
+    else
+      SE_CUDA(cudaMemsetAsync(db, 0x3c, sizeof(double) * nb, c.stream));
+    SE_CUDA(cudaMemsetAsync(dc, 0, sizeof(double) * nc, c.stream));
+    k::ritz_gemm(c, m, n, k, da, lda, a_kcontig != 0, db, ldb, dc, ldc);
+    if (reps > 0 && ms) {
+      cudaEvent_t e0, e1;
+      SE_CUDA(cudaEventCreate(&e0));
+      SE_CUDA(cudaEventCreate(&e1));
+      SE_CUDA(cudaEventRecord(e0, c.stream));
+      for (int r = 0; r < reps; ++r) k::ritz_gemm(c, m, n, k, da, lda, a_kcontig != 0, db, ldb, dc, ldc);
+      SE_CUDA(cudaEventRecord(e1, c.stream));
+      SE_CUDA(cudaEventSynchronize(e1));
+      float t = 0.f;
+      SE_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      *ms = t / reps;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    if (a && b) SE_CUDA(cudaMemcpyAsync(out, dc, sizeof(double) * nc, cudaMemcpyDeviceToHost, c.stream));
+    ctx_sync(c);
+    dev_free(da);
+    dev_free(db);
+    dev_free(dc);
+  });
+}
+
 int se_cheb_apply(se_ctx* ctx, const se_csr* a, const se_poly_filter* f, int nvec, const double* v,
                   double* out, long* n_matvec) {
   return guard([&] {

@@ -162,8 +162,6 @@ Ctx* ctx_create(int device) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
-  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(SE_ECUDA, "cublasCreate failed");
-  cublasSetStream(c->blas, c->hstream);
   if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(SE_ECUDA, "cusolverDnCreate failed");
   cusolverDnSetStream(c->solver, c->hstream);
   SE_CUDA(cudaEventCreateWithFlags(&c->evsync, cudaEventBlockingSync | cudaEventDisableTiming));
@@ -180,7 +178,6 @@ void ctx_destroy(Ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->bulk);
   cudaStreamSynchronize(c->hstream);
-  if (c->blas) cublasDestroy(c->blas);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->evsync) cudaEventDestroy(c->evsync);

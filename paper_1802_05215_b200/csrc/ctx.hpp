@@ -2,7 +2,6 @@
 // single-threaded host code; this owns what a B200 slice worker needs).
 #pragma once
 
-#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <atomic>
@@ -19,7 +18,6 @@ struct Ctx {
   cudaStream_t stream = nullptr;   // current launch stream (bulk Lanczos work: low priority)
   cudaStream_t bulk = nullptr;     // the low-priority stream
   cudaStream_t hstream = nullptr;  // high priority: latency-bound host-driven phases
-  cublasHandle_t blas = nullptr;
   cusolverDnHandle_t solver = nullptr;
   long launches = 0;  // this library's kernel launches issued on `stream`
   // device bytes the Ritz-candidate evaluation (U = W Y and A U) may hold at once; larger

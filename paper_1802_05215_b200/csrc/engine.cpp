@@ -497,16 +497,12 @@ struct CandBuf {
       stats_cap = grow(nc);
       stats = dev_alloc<double>(3 * (size_t)stats_cap);
     }
-    const double one = 1.0, zero = 0.0;
-    // row-major W is the column-major (steps x n, ld w_row_ld) matrix W^T: U = (W^T)^T Y
-    const cublasStatus_t st =
-        w_row_ld ? cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, n, nc, steps, &one, W, w_row_ld, Y,
-                               ldy, &zero, U.p, n)
-                 : cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, nc, steps, &one, W, n, Y, ldy,
-                               &zero, U.p, n);
-    if (st != CUBLAS_STATUS_SUCCESS)
-      fail(SE_ECUDA, "cublasDgemm (Ritz combinations) failed");
-    ++c.launches;
+    // U = W Y on the fp64 tensor cores (ritz_gemm.cu): W row-major (row stride w_row_ld) or
+    // column-major (ld n)
+    if (w_row_ld)
+      k::ritz_gemm(c, n, nc, steps, W, w_row_ld, true, Y, ldy, U.p, n);
+    else
+      k::ritz_gemm(c, n, nc, steps, W, n, false, Y, ldy, U.p, n);
     auto spmv_cols = [&](const DevCsr& M, const double* x, double* y) {
       for (int q0 = 0; q0 < nc; q0 += 65535) {
         k::ChebArgs a;
@@ -639,10 +635,7 @@ struct Slice {
     HiPrio hp(c);
     h2d(c, kr.L.p, u, sizeof(double) * (size_t)n * ndefl);
     double* G = dev_alloc<double>((size_t)ndefl * ndefl);
-    const double one = 1.0, zero = 0.0;
-    cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, ndefl, ndefl, n, &one, kr.L.p, n, kr.L.p, n,
-                &zero, G, ndefl);
-    ++c.launches;
+    k::ritz_gemm(c, ndefl, ndefl, n, kr.L.p, n, true, kr.L.p, n, G, ndefl);  // L^T L
     Vec g((size_t)ndefl * ndefl);
     d2h(c, g.data(), G, sizeof(double) * g.size());
     ctx_sync(c);
@@ -768,13 +761,9 @@ struct Slice {
     ctx_sync(c);
     double* dy = dev_alloc<double>(ysel.size());
     h2d(c, dy, ysel.data(), sizeof(double) * ysel.size());
-    const double one = 1.0, zero = 0.0;
-    const cublasStatus_t st = cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, n, k, steps, &one, W,
-                                          ldw, dy, steps, &zero, trbuf.p, n);
+    k::ritz_gemm(c, n, k, steps, W, ldw, true, dy, steps, trbuf.p, n);
     ctx_sync(c);
     dev_free(dy);
-    if (st != CUBLAS_STATUS_SUCCESS) fail(SE_ECUDA, "cublasDgemm (thick-restart vectors) failed");
-    ++c.launches;
   }
 
   // Candidate rows ylast for thick restart: Y[steps-1, j] for the candidate columns.
@@ -1412,23 +1401,14 @@ std::unique_ptr<SliceResult> cheb_si(Ctx& c, const DevCsr& a, const PolyFilter& 
         k::spmv_cheb(c, a, k::kPlain, pa);
       }
       cnt.n_A_matvec += q;
-      const double one = 1.0, zero = 0.0;
       double* dG = dev_alloc<double>((size_t)q * q);
-      if (cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, q, q, n, &one, T.p, n, AY.p, n, &zero, dG, q) !=
-          CUBLAS_STATUS_SUCCESS) {
-        dev_free(dG);
-        fail(SE_ECUDA, "cublasDgemm (Rayleigh-Ritz gram) failed");
-      }
-      ++c.launches;
+      k::ritz_gemm(c, q, q, n, T.p, n, true, AY.p, n, dG, q);  // gram = T^T (A T)
       d2h(c, G.data(), dG, sizeof(double) * (size_t)q * q);
       dev_free(dG);
       for (int j = 0; j < q; ++j)
         for (int i = j + 1; i < q; ++i) G[(size_t)j * q + i] = G[(size_t)i * q + j];  // lower := upper
       const double* V = eig.solve(q, G, lam);
-      if (cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, q, q, &one, T.p, n, V, q, &zero, Y.p, n) !=
-          CUBLAS_STATUS_SUCCESS)
-        fail(SE_ECUDA, "cublasDgemm (Ritz block) failed");
-      ++c.launches;
+      k::ritz_gemm(c, n, q, q, T.p, n, false, V, q, Y.p, n);  // Y = T V
       cnt.t_mv += secs(tm);
       // candidate pass (eigensolvers.hpp:857-896): Ritz values inside the slack-widened slice
       std::vector<int> sel;

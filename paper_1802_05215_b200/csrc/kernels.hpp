@@ -167,6 +167,13 @@ void project_out(Ctx& c, const Scratch& s, int n, int kq, const double* Q, doubl
 // beta = after; breakdown -> halted; else W[:, i+1] = t * (1/beta), beta_arr[i] = beta, i++.
 void normalize_next(Ctx& c, const Scratch& s, int n, const double* t, double* W, Ctl* ctl,
                     double* beta_arr);
+// Dense fp64 contraction on the tensor cores (DMMA), C (M x N, column-major, ldc) = A B with
+// B[k + col ldb] and A[row lda + k] (a_kcontig: the row-major Krylov basis, or X^T of a
+// column-major X with lda = its leading dimension) or A[row + k lda] (a column-major block).
+// Rayleigh-Ritz combinations U = W Y (eigensolvers.hpp:275-283), thick-restart vectors, the
+// subspace-iteration Gram / rotation products and the deflation-set Gram (ritz_gemm.cu).
+void ritz_gemm(Ctx& c, int M, int N, int K, const double* A, long lda, bool a_kcontig,
+               const double* B, long ldb, double* C, long ldc);
 // Candidate statistics (eigensolvers.hpp:289-316) per column of U (n x nc) and AU:
 // out3[3j..] = (lambda, residual, uu).  U is left unscaled (raw W y, kept for thick restart).
 void candidate_stats(Ctx& c, int n, int nc, double* U, const double* AU, double* out3,
