@@ -166,6 +166,12 @@ SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
 /* A full CGS2 step with the re-pass forced: mode 0 = two column-major passes (4 reads of W),
  * mode 2 = the product path on the row-major basis, T1 + fused MID + N2 (3 reads); mode -1 =
  * one column-major pass. */
+/* The resident filter (all degrees of apply_pol, filter_poly.hpp:256-277, in one cooperative
+ * launch with the matrix held in shared memory; matrices up to ~300k rows / 2.3M entries).
+ * se_resident_filter(0) switches it off process-wide (A/B measurements; results are bit-identical
+ * either way); se_csr_resident_tiles: row tiles of the matrix' plan, 0 when it does not apply. */
+SE_API int se_resident_filter(int enable);
+SE_API int se_csr_resident_tiles(const se_csr* a, int* tiles);
 /* mult_cols (vecops.hpp:81-89) / the Rayleigh-Ritz contractions (eigensolvers.hpp:275-283,
  * 838-871) on the fp64 tensor cores: out (m x n, column-major, ldc) = A B, B[k + col ldb],
  * A[row lda + k] (a_kcontig) or A[row + k lda]; host buffers.  With a or b NULL the operands are

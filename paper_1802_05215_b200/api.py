@@ -888,6 +888,19 @@ def _d_matvec(d: "DeviceCsr", x) -> np.ndarray:
 SAMPLE_VECTORS = 0
 
 
+def set_resident_filter(on: bool) -> None:
+    """Process-wide switch of the resident (one launch for all degrees) filter; results are
+    bit-identical either way.  Default on."""
+    call("se_resident_filter", int(bool(on)))
+
+
+def resident_tiles(d) -> int:
+    """Row tiles of the matrix' resident-filter plan (0: the per-degree kernels run)."""
+    t = C.c_int()
+    call("se_csr_resident_tiles", _dev(d).handle, C.byref(t))
+    return t.value
+
+
 def mult_cols(a: np.ndarray, b: np.ndarray, a_rowmajor: bool = True, ctx=None) -> np.ndarray:
     """out = A @ B on the GPU's fp64 tensor cores (mult_cols vecops.hpp:81-89; the Ritz
     combination U = W Y of eigensolvers.hpp:275-283).  a: (m, k) C-contiguous (the row-major

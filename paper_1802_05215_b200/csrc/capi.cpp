@@ -414,6 +414,7 @@ int se_csr_free(se_csr* a) {
     cudaSetDevice(a->a.device);
     dev_free_shared(a->a.rp);
     dev_free_shared(a->a.resw);
+    k::resident_free(a->a);
     a->a.free_entries();
     if (a->a.ell_c) {
       dev_free_shared(a->a.ell_c);
@@ -490,6 +491,17 @@ int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int re
 int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms) {
   return guard([&] {
     cgs2_bench(C(ctx), n, k, reps, mode, *ms);
+  });
+}
+
+int se_resident_filter(int enable) {
+  return guard([&] { k::resident_enable(enable != 0); });
+}
+
+int se_csr_resident_tiles(const se_csr* a, int* tiles) {
+  return guard([&] {
+    if (!a || !tiles) fail(SE_EINVAL, "se_csr_resident_tiles: null argument");
+    *tiles = k::resident_tiles(M(a));
   });
 }
 

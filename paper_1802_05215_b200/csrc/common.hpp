@@ -33,6 +33,10 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 // col = row, val = 0) that the block KPM kernel reads instead of the CSR arrays.
 constexpr int kEllW = 8;
 
+namespace k {
+struct ResidentPlan;  // resident.cu: row tiles + neighbour lists of the one-launch filter
+}
+
 struct DevCsr {
   int device = 0;
   int n = 0;
@@ -47,6 +51,9 @@ struct DevCsr {
   // Set on D A D of a diagonal-B pencil with w = D^-1, which makes the residual the reference's
   // ||A x - lambda B x|| / sqrt(x' B x) for x = D u (eigensolvers.hpp:289-316)
   double* resw = nullptr;
+  // plan of the resident (one launch for all degrees) filter; null when the matrix does not fit
+  // in the GPU's aggregate shared memory
+  k::ResidentPlan* resident = nullptr;
   // vals and col_idx live in ONE allocation (vals first, col_idx right after) so a single L2
   // access-policy window covers the whole matrix stream of the filter SpMV
   void alloc_entries(long count);

@@ -89,6 +89,7 @@ struct Krylov {
   int nlock = 0;
 
   double* mu_dev = nullptr;
+  long long* res_flags = nullptr;  // resident filter: one degree counter per row tile
 
   Krylov(Ctx& cc, const DevCsr& a, const StepOp& o, const Pencil* p = nullptr)
       : c(cc), A(a), op(o), pen(p), n(a.n) {
@@ -104,6 +105,10 @@ struct Krylov {
       for (double*& b : fb) b = dev_alloc<double>(n);
       mu_dev = dev_alloc<double>(op.k + 1);
       h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
+      if (!pen && k::resident_tiles(A) > 0) {  // the whole filter in one launch (resident.cu)
+        res_flags = dev_alloc<long long>(k::resident_tiles(A));
+        SE_CUDA(cudaMemsetAsync(res_flags, 0, sizeof(long long) * k::resident_tiles(A), c.stream));
+      }
     }
     ctl = dev_alloc<Ctl>(1);
     dscal = dev_alloc<double>(4);
@@ -116,6 +121,7 @@ struct Krylov {
     dev_free(W.p);
     devmat_free(L);
     dev_free(mu_dev);
+    dev_free(res_flags);
     for (void* p : {(void*)pb[0], (void*)pb[1], (void*)pb[2], (void*)s1, (void*)s2, (void*)sx})
       dev_free(p);
     for (void* p : {(void*)t, (void*)vsrc, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl,
@@ -313,7 +319,10 @@ struct Krylov {
       k::spmv_cheb(c, A, k::kPlain, a);
       return;
     }
-    record_series(A, op, vsrc, t, fb);
+    if (res_flags)
+      k::cheb_resident(c, A, op.k, mu_dev, op.c, op.invd, vsrc, t, fb, res_flags, ctl);
+    else
+      record_series(A, op, vsrc, t, fb);
   }
 
   // One Lanczos step.  mode 0: NR recurrence (eigensolvers.hpp:406-433 / lanczos.hpp:151-185);
@@ -1053,10 +1062,23 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
   if (op.k < 1) fail(SE_EINVAL, "apply_pol: filter degree must be >= 1");
   double* fb[3];
   for (double*& b : fb) b = dev_alloc<double>(n);
+  const int tiles = k::resident_tiles(a);
+  double* mu_dev = nullptr;
+  long long* flags = nullptr;
+  if (tiles > 0) {
+    mu_dev = dev_alloc<double>(op.k + 1);
+    h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
+    flags = dev_alloc<long long>(tiles);
+    SE_CUDA(cudaMemsetAsync(flags, 0, sizeof(long long) * tiles, c.stream));
+  }
   try {
     for (int col = 0; col < nvec; ++col) {
       const double* x = v + (size_t)col * n;
       double* o = out + (size_t)col * n;
+      if (tiles > 0) {
+        k::cheb_resident(c, a, op.k, mu_dev, op.c, op.invd, x, o, fb, flags, nullptr);
+        continue;
+      }
       k::ChebArgs a1;
       a1.c = op.c;
       a1.invd = op.invd;
@@ -1083,9 +1105,13 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
     ctx_sync(c);
   } catch (...) {
     for (double* b : fb) dev_free(b);
+    dev_free(mu_dev);
+    dev_free(flags);
     throw;
   }
   for (double* b : fb) dev_free(b);
+  dev_free(mu_dev);
+  dev_free(flags);
 }
 
 // lanczos_run (lanczos.hpp:37-118), euclidean inner product.
@@ -1495,34 +1521,46 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     const long before = c.launches;
     double* mu_dev = dev_alloc<double>(op.k + 1);
     h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
+    const int tiles = k::resident_tiles(a);
+    long long* flags = nullptr;
+    if (tiles > 0) {
+      flags = dev_alloc<long long>(tiles);
+      SE_CUDA(cudaMemsetAsync(flags, 0, sizeof(long long) * tiles, c.stream));
+      ctx_sync(c);
+    }
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
-    k::ChebArgs a1;
-    a1.c = op.c;
-    a1.invd = op.invd;
-    a1.x = v;
-    a1.y = fb[0];
-    a1.out = out;
-    a1.mu0 = op.mu[0];
-    a1.muj = op.mu[1];
-    k::spmv_cheb(c, a, k::kFirst, a1);
-    int cur = 0, prv = -1, nxt = 1;
-    for (int j = 2; j <= op.k; ++j) {
-      k::ChebArgs b = a1;
-      b.x = fb[cur];
-      b.prev = prv < 0 ? v : fb[prv];
-      b.y = fb[nxt];
-      b.muj = op.mu[j];
-      k::spmv_cheb(c, a, k::kNext, b);
-      const int old = prv < 0 ? 2 : prv;
-      prv = cur;
-      cur = nxt;
-      nxt = old;
+    if (tiles > 0) {  // as in production: the whole filter is one resident launch
+      k::cheb_resident(c, a, op.k, mu_dev, op.c, op.invd, v, out, fb, flags, nullptr);
+    } else {
+      k::ChebArgs a1;
+      a1.c = op.c;
+      a1.invd = op.invd;
+      a1.x = v;
+      a1.y = fb[0];
+      a1.out = out;
+      a1.mu0 = op.mu[0];
+      a1.muj = op.mu[1];
+      k::spmv_cheb(c, a, k::kFirst, a1);
+      int cur = 0, prv = -1, nxt = 1;
+      for (int j = 2; j <= op.k; ++j) {
+        k::ChebArgs b = a1;
+        b.x = fb[cur];
+        b.prev = prv < 0 ? v : fb[prv];
+        b.y = fb[nxt];
+        b.muj = op.mu[j];
+        k::spmv_cheb(c, a, k::kNext, b);
+        const int old = prv < 0 ? 2 : prv;
+        prv = cur;
+        cur = nxt;
+        nxt = old;
+      }
     }
     cudaGraph_t g;
     SE_CUDA(cudaStreamEndCapture(c.stream, &g));
     SE_CUDA(cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
-    const long per = c.launches - before;
+    // reported per filter degree either way (the resident launch covers op.k degrees)
+    const long per = tiles > 0 ? op.k : c.launches - before;
     SE_CUDA(cudaGraphLaunch(ge, c.stream));  // warm
     SE_CUDA(cudaEventRecord(c.ev0, c.stream));
     for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));
@@ -1534,6 +1572,7 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     launches = per * reps;
     c.launches += (c.launches - before) * (reps + 1);
     dev_free(mu_dev);
+    dev_free(flags);
   } catch (...) {
     if (ge) cudaGraphExecDestroy(ge);
     for (void* p : {(void*)v, (void*)out, (void*)fb[0], (void*)fb[1], (void*)fb[2]}) dev_free(p);

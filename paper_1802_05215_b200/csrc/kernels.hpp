@@ -67,6 +67,19 @@ void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args);
 
 
 
+// Resident filter (resident.cu): out = sum_j mu[j] T_j(Ahat) x, all kdeg degrees in one
+// cooperative launch with the matrix held in shared memory; available when a.resident != null.
+// buf: three n-vectors (tile exchange), flags: resident_tiles(a) zero-initialised counters that
+// belong to one caller (they advance monotonically across launches).
+void resident_build(Ctx& c, DevCsr& a);
+void resident_free(DevCsr& a);
+int resident_tiles(const DevCsr& a);
+void resident_enable(bool on);  // process-wide switch (A/B measurements); default on
+bool resident_enabled();
+void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, double cc, double invd,
+                   const double* x, double* out, double* const* buf, long long* flags,
+                   const Ctl* halt);
+
 // Block KPM step over b <= 16 row-major probe columns (dos.hpp:98-108):
 //   first: w1 = (A w0 - c w0)/d ; zeta[0], zeta[1] partials
 //   next : t  = 2 (A w1 - c w1)/d - w0 ; zeta[k] partial

@@ -829,6 +829,7 @@ void kpm_step(Ctx& c, const Scratch& s, const DevCsr& a, int b, int mode, const 
 }
 
 void build_ell(Ctx& c, DevCsr& a) {
+  if (!a.resident) resident_build(c, a);  // the pattern is in place: plan the resident filter
   if (a.n == 0 || a.max_row_nnz > kEllW) return;
   if (!a.ell_c) {
     a.ell_c = dev_alloc_shared<int>((size_t)a.n * kEllW);

@@ -332,6 +332,11 @@ class GpuBackend:
     def launches(self) -> int:
         return self.ctx.kernel_launches() + sum(c.kernel_launches() for c in self._thread_ctx.values())
 
+    def resident(self) -> bool:
+        """True when the filter runs as one resident cooperative launch per application
+        (resident.cu): such a launch holds every SM, so slices on this GPU run one at a time."""
+        return api.resident_tiles(self.A) > 0
+
     def memory(self) -> float:
         """Total device memory in bytes (sizes the memory plan's windows)."""
         return float(api.device_memory(self.device)[1])
@@ -417,6 +422,8 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
 
     mem = backend.memory() if hasattr(backend, "memory") else None
     jobs = concurrent_jobs(backend.n, mem, len(mine_idx), plan.jobs)
+    if plan.jobs <= 0 and plan.solver in ("tr", "nr") and getattr(backend, "resident", lambda: False)():
+        jobs = 1  # the resident filter owns the whole GPU while it runs; concurrency buys nothing
     max_west = window_estimate(backend.n, mem, min(jobs, max(1, len(mine_idx))), plan.window_est)
 
     def work(i):

@@ -244,3 +244,62 @@ def test_ritz_gemm_matches_numpy(gpu_ctx, m, n, k, rowmajor):
     ref = a @ b
     scale = np.abs(a) @ np.abs(b)
     assert np.all(np.abs(out - ref) <= 4e-16 * k * scale + 1e-300)
+
+
+@pytest.mark.parametrize("case,degree", [("lap3d", 0), ("lap2d", 0), ("irr8", 0), ("irr24", 0),
+                                         ("banded", 0), ("lap2d", 1), ("lap2d", 2), ("tiny", 0)])
+def test_resident_filter_bitwise(gpu_ctx, case, degree):
+    """The resident filter (resident.cu: every degree in one cooperative launch, matrix tiles in
+    shared memory, neighbour hand-off through L2) against the oracle's apply_pol and against the
+    per-degree kernels: bit-identical on stencils (neighbour tiles only), irregular matrices with
+    empty rows and a random banded matrix (every tile a neighbour), a one-tile matrix, and the
+    degree-1 / degree-2 edge cases."""
+    api = _api()
+    if case == "lap3d":
+        a, (lo, hi) = api.gen_laplacian([30, 28, 26]), (0.0, 12.0)
+    elif case == "lap2d":
+        a, (lo, hi) = api.gen_laplacian([130, 90]), (0.0, 8.0)
+    elif case == "tiny":
+        a, (lo, hi) = api.gen_laplacian([9, 7]), (0.0, 8.0)
+    elif case == "irr8":
+        a, (lo, hi) = _irregular(30011, 7, 8), (-4.0, 6.0)
+    elif case == "irr24":
+        a, (lo, hi) = _irregular(20001, 8, 24), (-6.0, 9.0)
+    else:
+        a, (lo, hi) = api.gen_random_sparse(40000, 3), (-12.0, 18.0)
+    f = api.find_pol(lo + 0.31 * (hi - lo), lo + 0.36 * (hi - lo), api.SpectralBounds(lo, hi))
+    if degree:  # truncate the series: degree 1 and 2 take the kernel's short paths
+        f = api.PolynomialFilter(k=degree, gamma=f.gamma, mu=f.mu[:degree + 1].copy(), c=f.c, d=f.d,
+                                 tau=f.tau, ta=f.ta, tb=f.tb, bar=f.bar, damping=f.damping,
+                                 cap_reached=f.cap_reached)
+    x = clib.rng_vectors(3, "normal", a.n)[0]
+    assert api.resident_tiles(a) > 0
+    out = api.apply_pol(f, a, x)
+    ref = clib.apply_pol(a.row_ptr, a.col_idx, a.vals, f.mu, f.c, f.d, x)
+    assert np.array_equal(out, ref), np.max(np.abs(out - ref))
+    api.set_resident_filter(False)
+    try:
+        assert api.resident_tiles(a) == 0
+        out2 = api.apply_pol(f, a, x)
+    finally:
+        api.set_resident_filter(True)
+    assert np.array_equal(out, out2)
+    # a second application on the same matrix (the tile counters keep advancing)
+    assert np.array_equal(api.apply_pol(f, a, x), ref)
+
+
+def test_resident_filter_in_the_slice_solve(gpu_ctx):
+    """cheb_lan_tr with the resident filter on and off: identical eigenvalues, residuals and
+    iteration counts (the filter output is bit-identical, so the whole recurrence is)."""
+    api = _api()
+    a = api.gen_laplacian([40, 40])
+    f = api.find_pol(0.5, 0.9, api.SpectralBounds(0.0, 8.0))
+    cfg = api.SolverConfig(est_count=60)
+    r1 = api.cheb_lan_tr(a, None, f, 0.5, 0.9, cfg)
+    api.set_resident_filter(False)
+    try:
+        r0 = api.cheb_lan_tr(a, None, f, 0.5, 0.9, cfg)
+    finally:
+        api.set_resident_filter(True)
+    assert r1.niter == r0.niter and np.array_equal(r1.eigenvalues, r0.eigenvalues)
+    assert np.array_equal(r1.residuals, r0.residuals)
