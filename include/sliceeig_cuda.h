@@ -183,6 +183,8 @@ SE_API int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* 
 /* Production timing of kdeg degrees of the multi-vector filter (nv <= 8 recurrences sharing one
  * staging of A per degree), graph-captured and replayed `reps` times.  Returns total ms. */
 SE_API int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int reps, double* ms);
+/* The same for the row-major block filter (8 vectors, padded-row matrices): kdeg degrees. */
+SE_API int se_block_filter_bench(se_ctx* ctx, const se_csr* a, int kdeg, int reps, double* ms);
 
 /* ---- filters (host, filter_poly.hpp) -------------------------------------------------------- */
 SE_API int se_damping_multipliers(int k, int damping, double* out);            /* :41-60   */

@@ -74,6 +74,7 @@ SIGNATURES = {
     "se_filter_bench": [_VP, _VP, C.POINTER(SePolyFilter), C.c_int, _PD, _PL, _PD],
     "se_cgs_bench": [_VP, C.c_int, C.c_int, C.c_int, _PD],
     "se_multi_filter_bench": [_VP, _VP, C.c_int, C.c_int, C.c_int, _PD],
+    "se_block_filter_bench": [_VP, _VP, C.c_int, C.c_int, _PD],
     "se_resident_filter": [C.c_int],
     "se_csr_resident_tiles": [_VP, _PI],
     "se_mult_cols": [_VP, C.c_int, C.c_int, C.c_int, _PD, C.c_long, C.c_int, _PD, C.c_long, _PD,

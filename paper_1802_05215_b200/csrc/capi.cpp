@@ -488,6 +488,10 @@ int se_multi_filter_bench(se_ctx* ctx, const se_csr* a, int nv, int kdeg, int re
   return guard([&] { multi_filter_bench(C(ctx), M(a), nv, kdeg, reps, *ms); });
 }
 
+int se_block_filter_bench(se_ctx* ctx, const se_csr* a, int kdeg, int reps, double* ms) {
+  return guard([&] { block_filter_bench(C(ctx), M(a), kdeg, reps, *ms); });
+}
+
 int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms) {
   return guard([&] {
     cgs2_bench(C(ctx), n, k, reps, mode, *ms);

@@ -89,7 +89,7 @@ struct Krylov {
   int nlock = 0;
 
   double* mu_dev = nullptr;
-  long long* res_flags = nullptr;  // resident filter: one degree counter per row tile
+  void* res_state = nullptr;  // resident filter: tile-exchange buffers + tag epoch
 
   Krylov(Ctx& cc, const DevCsr& a, const StepOp& o, const Pencil* p = nullptr)
       : c(cc), A(a), op(o), pen(p), n(a.n) {
@@ -106,8 +106,8 @@ struct Krylov {
       mu_dev = dev_alloc<double>(op.k + 1);
       h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
       if (!pen && k::resident_tiles(A) > 0) {  // the whole filter in one launch (resident.cu)
-        res_flags = dev_alloc<long long>(k::resident_tiles(A));
-        SE_CUDA(cudaMemsetAsync(res_flags, 0, sizeof(long long) * k::resident_tiles(A), c.stream));
+        res_state = dev_alloc<char>(k::resident_state_bytes(A));
+        SE_CUDA(cudaMemsetAsync(res_state, 0, k::resident_state_bytes(A), c.stream));
       }
     }
     ctl = dev_alloc<Ctl>(1);
@@ -121,7 +121,7 @@ struct Krylov {
     dev_free(W.p);
     devmat_free(L);
     dev_free(mu_dev);
-    dev_free(res_flags);
+    dev_free(res_state);
     for (void* p : {(void*)pb[0], (void*)pb[1], (void*)pb[2], (void*)s1, (void*)s2, (void*)sx})
       dev_free(p);
     for (void* p : {(void*)t, (void*)vsrc, (void*)fb[0], (void*)fb[1], (void*)fb[2], (void*)ctl,
@@ -319,8 +319,8 @@ struct Krylov {
       k::spmv_cheb(c, A, k::kPlain, a);
       return;
     }
-    if (res_flags)
-      k::cheb_resident(c, A, op.k, mu_dev, op.c, op.invd, vsrc, t, fb, res_flags, ctl);
+    if (res_state)
+      k::cheb_resident(c, A, op.k, mu_dev, op.c, op.invd, vsrc, t, res_state, ctl);
     else
       record_series(A, op, vsrc, t, fb);
   }
@@ -1064,19 +1064,19 @@ void apply_filter_dev(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, const
   for (double*& b : fb) b = dev_alloc<double>(n);
   const int tiles = k::resident_tiles(a);
   double* mu_dev = nullptr;
-  long long* flags = nullptr;
+  void* flags = nullptr;  // resident filter state
   if (tiles > 0) {
     mu_dev = dev_alloc<double>(op.k + 1);
     h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
-    flags = dev_alloc<long long>(tiles);
-    SE_CUDA(cudaMemsetAsync(flags, 0, sizeof(long long) * tiles, c.stream));
+    flags = dev_alloc<char>(k::resident_state_bytes(a));
+    SE_CUDA(cudaMemsetAsync(flags, 0, k::resident_state_bytes(a), c.stream));
   }
   try {
     for (int col = 0; col < nvec; ++col) {
       const double* x = v + (size_t)col * n;
       double* o = out + (size_t)col * n;
       if (tiles > 0) {
-        k::cheb_resident(c, a, op.k, mu_dev, op.c, op.invd, x, o, fb, flags, nullptr);
+        k::cheb_resident(c, a, op.k, mu_dev, op.c, op.invd, x, o, flags, nullptr);
         continue;
       }
       k::ChebArgs a1;
@@ -1264,9 +1264,37 @@ void apply_filter_block(Ctx& c, const DevCsr& a, const StepOp& op, int nvec, con
     apply_filter_dev(c, a, op, nvec, v, out);
     return;
   }
-  // balanced groups of <= 8 columns (9 -> 5 + 4, not 8 + 1: a nearly empty multi-vector launch
-  // costs almost a full one); groups of one or two columns take the single-vector chain
   const int ngroups = (nvec + 7) / 8;
+  if (k::cheb_block_available(a) && nvec > 2) {
+    // padded-row matrices (stencils): groups of <= 8 columns as row-major n x 8 blocks through
+    // the block kernel (one read of a row's entries for the whole group, 64-byte gathers)
+    double* blk = dev_alloc<double>((size_t)n * 8 * 5);
+    double* Xin = blk;
+    double* T[3] = {blk + (size_t)n * 8, blk + (size_t)n * 16, blk + (size_t)n * 24};
+    double* O = blk + (size_t)n * 32;
+    try {
+      for (int g = 0, c0 = 0; g < ngroups; ++g) {
+        const int nv = nvec / ngroups + (g < nvec % ngroups ? 1 : 0);
+        k::cheb_block_pack(c, v + (size_t)c0 * n, Xin, n, nv);
+        k::cheb_block_step(c, a, true, Xin, nullptr, T[0], O, op.c, op.invd, op.mu[0], op.mu[1]);
+        for (int j = 2; j <= op.k; ++j)
+          k::cheb_block_step(c, a, false, T[(j - 2) % 3], j == 2 ? Xin : T[j % 3], T[(j - 1) % 3], O,
+                             op.c, op.invd, 0.0, op.mu[j]);
+        k::cheb_block_unpack(c, O, out + (size_t)c0 * n, n, nv);
+        c0 += nv;
+      }
+      ctx_sync(c);
+    } catch (...) {
+      ctx_sync(c);
+      dev_free(blk);
+      throw;
+    }
+    dev_free(blk);
+    return;
+  }
+  // longer rows: balanced groups of <= 8 columns (9 -> 5 + 4, not 8 + 1: a nearly empty
+  // multi-vector launch costs almost a full one) through the CSR multi-vector kernel; groups of
+  // one or two columns take the single-vector chain
   double* buf = dev_alloc<double>((size_t)n * 24);
   try {
     for (int g = 0, c0 = 0; g < ngroups; ++g) {
@@ -1522,15 +1550,15 @@ void filter_bench(Ctx& c, const DevCsr& a, const StepOp& op, int reps, double& m
     double* mu_dev = dev_alloc<double>(op.k + 1);
     h2d(c, mu_dev, op.mu.data(), sizeof(double) * (op.k + 1));
     const int tiles = k::resident_tiles(a);
-    long long* flags = nullptr;
+    void* flags = nullptr;
     if (tiles > 0) {
-      flags = dev_alloc<long long>(tiles);
-      SE_CUDA(cudaMemsetAsync(flags, 0, sizeof(long long) * tiles, c.stream));
+      flags = dev_alloc<char>(k::resident_state_bytes(a));
+      SE_CUDA(cudaMemsetAsync(flags, 0, k::resident_state_bytes(a), c.stream));
       ctx_sync(c);
     }
     SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     if (tiles > 0) {  // as in production: the whole filter is one resident launch
-      k::cheb_resident(c, a, op.k, mu_dev, op.c, op.invd, v, out, fb, flags, nullptr);
+      k::cheb_resident(c, a, op.k, mu_dev, op.c, op.invd, v, out, flags, nullptr);
     } else {
       k::ChebArgs a1;
       a1.c = op.c;
@@ -1686,6 +1714,45 @@ void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms) {
 
 namespace se {
 // Time k degrees of the multi-vector filter over nv vectors (graph-captured, replayed).
+// Time kdeg degrees of the row-major block filter (8 vectors; graph-captured, replayed).
+void block_filter_bench(Ctx& c, const DevCsr& a, int kdeg, int reps, double& ms) {
+  if (kdeg < 2 || reps < 1) fail(SE_EINVAL, "se_block_filter_bench: bad sizes");
+  if (!k::cheb_block_available(a)) fail(SE_EINVAL, "se_block_filter_bench: rows longer than 8 entries");
+  const int n = a.n;
+  double* blk = dev_alloc<double>((size_t)n * 8 * 5);
+  SE_CUDA(cudaMemsetAsync(blk, 0, sizeof(double) * (size_t)n * 40, c.stream));
+  double* Xin = blk;
+  double* T[3] = {blk + (size_t)n * 8, blk + (size_t)n * 16, blk + (size_t)n * 24};
+  double* O = blk + (size_t)n * 32;
+  cudaGraphExec_t ge = nullptr;
+  try {
+    ctx_sync(c);
+    SE_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    k::cheb_block_step(c, a, true, Xin, nullptr, T[0], O, 6.0, 1.0 / 6.0, 0.5, 0.1);
+    for (int j = 2; j <= kdeg; ++j)
+      k::cheb_block_step(c, a, false, T[(j - 2) % 3], j == 2 ? Xin : T[j % 3], T[(j - 1) % 3], O, 6.0,
+                         1.0 / 6.0, 0.0, 0.1);
+    cudaGraph_t g;
+    SE_CUDA(cudaStreamEndCapture(c.stream, &g));
+    SE_CUDA(cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority));
+    cudaGraphDestroy(g);
+    SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev0, c.stream));
+    for (int r = 0; r < reps; ++r) SE_CUDA(cudaGraphLaunch(ge, c.stream));
+    SE_CUDA(cudaEventRecord(c.ev1, c.stream));
+    SE_CUDA(cudaEventSynchronize(c.ev1));
+    float f = 0.f;
+    SE_CUDA(cudaEventElapsedTime(&f, c.ev0, c.ev1));
+    ms = f;
+  } catch (...) {
+    if (ge) cudaGraphExecDestroy(ge);
+    dev_free(blk);
+    throw;
+  }
+  cudaGraphExecDestroy(ge);
+  dev_free(blk);
+}
+
 void multi_filter_bench(Ctx& c, const DevCsr& a, int nv, int kdeg, int reps, double& ms) {
   if (nv < 1 || nv > 8 || kdeg < 2 || reps < 1) fail(SE_EINVAL, "se_multi_filter_bench: bad sizes");
   const int n = a.n;

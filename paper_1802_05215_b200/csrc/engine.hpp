@@ -101,4 +101,5 @@ void cgs2_bench(Ctx& c, int n, int kcols, int reps, int mode, double& ms);
 }
 namespace se {
 void multi_filter_bench(Ctx& c, const DevCsr& a, int nv, int kdeg, int reps, double& ms);
+void block_filter_bench(Ctx& c, const DevCsr& a, int kdeg, int reps, double& ms);
 }

@@ -67,18 +67,26 @@ void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args);
 
 
 
+// Block filter degree on a row-major n x 8 vector block (padded-row matrices; K2): Y = T_j,
+// O = running sum; first: j = 1 (X = v, P unused), else X = T_{j-1}, P = T_{j-2}.
+bool cheb_block_available(const DevCsr& a);
+void cheb_block_pack(Ctx& c, const double* colmajor, double* rowmajor, int n, int nv);
+void cheb_block_unpack(Ctx& c, const double* rowmajor, double* colmajor, int n, int nv);
+void cheb_block_step(Ctx& c, const DevCsr& a, bool first, const double* X, const double* P,
+                     double* Y, double* O, double cc, double invd, double mu0, double muj);
+
 // Resident filter (resident.cu): out = sum_j mu[j] T_j(Ahat) x, all kdeg degrees in one
-// cooperative launch with the matrix held in shared memory; available when a.resident != null.
-// buf: three n-vectors (tile exchange), flags: resident_tiles(a) zero-initialised counters that
-// belong to one caller (they advance monotonically across launches).
+// cooperative launch with the matrix held in shared memory; available when resident_tiles(a) > 0.
+// state: resident_state_bytes(a) zero-initialised device bytes that belong to one caller (the
+// tile-exchange buffers and the tag epoch, which advances across launches).
 void resident_build(Ctx& c, DevCsr& a);
 void resident_free(DevCsr& a);
 int resident_tiles(const DevCsr& a);
+size_t resident_state_bytes(const DevCsr& a);
 void resident_enable(bool on);  // process-wide switch (A/B measurements); default on
 bool resident_enabled();
 void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, double cc, double invd,
-                   const double* x, double* out, double* const* buf, long long* flags,
-                   const Ctl* halt);
+                   const double* x, double* out, void* state, const Ctl* halt);
 
 // Block KPM step over b <= 16 row-major probe columns (dos.hpp:98-108):
 //   first: w1 = (A w0 - c w0)/d ; zeta[0], zeta[1] partials

@@ -9,15 +9,22 @@
 // with its tile of the current Chebyshev vector (double-buffered), while the previous vector, the
 // current vector and the running sum out = sum_j mu_j T_j v of its own rows live in registers.
 // Per degree a CTA only exchanges vector entries with the tiles its columns reach: it writes its
-// new tile to a global (L2) buffer, publishes its degree counter with a release store, and polls
-// the counters of its neighbour tiles with acquire loads before gathering their entries -- a
-// dataflow hand-off between neighbouring tiles (2 of a 7-point stencil's 7 gathers leave the
-// tile) instead of a grid-wide barrier or a kernel boundary.
+// new tile to a global (L2) exchange buffer as tagged 16-byte entries {lo32, tag, hi32, tag}
+// (NCCL's LL idea: each 8-byte half is atomic and carries the degree that produced it), and a
+// consumer re-reads a remote entry until both tags name the degree it needs.  The data is its
+// own arrival signal: no flag, no fence, no grid barrier, no kernel boundary -- a dataflow
+// hand-off between neighbouring tiles (2 of a 7-point stencil's 7 gathers leave the tile).
 //
-// Safety: the launch is cooperative (all CTAs co-resident by construction), the wait is bounded
-// (a stuck neighbour traps instead of hanging the device), and the write-after-read hazard of
-// the three rotating exchange buffers is covered by the same wait because the neighbour relation
-// is symmetrised when the plan is built.
+// Safety: the launch is cooperative (all CTAs co-resident by construction) and the wait is bounded
+// (an entry that never arrives traps instead of hanging the device).  FOUR exchange buffers
+// rotate (slot = degree mod 4): a tile writes degree j + 3 over degree j - 1 only after it has
+// finished degree j + 2, which needed a degree j + 1 entry from each tile it reads; that tile
+// had then passed its end-of-degree-j barrier, i.e. ALL its threads were done reading degree
+// j - 1 entries.  On a structurally symmetric tile pattern (checked when the plan is built) the
+// tiles a tile reads are the tiles that read it, so no entry is overwritten while a neighbour
+// still needs it -- by construction, not by timing (three buffers would leave a window).  Tags
+// grow monotonically across applications (epoch + degree), so a stale entry never passes for a
+// fresh one.
 //
 // Numerics: per row exactly the arithmetic of k_spmv_cheb (storage-order sums of individually
 // rounded products, the same map and recurrence), so the result is bit-identical to the
@@ -37,13 +44,24 @@ __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, 
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 
-__device__ __forceinline__ long long ld_acquire(const long long* p) {
-  long long v;
-  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
-  return v;
+// Tile exchange in the style of NCCL's LL protocol: a vector entry travels as 16 bytes
+// {lo32, tag, hi32, tag}; each 8-byte half is written and read atomically and carries the tag of
+// the degree that produced it, so a consumer simply re-reads an entry until both tags match --
+// no flag, no fence, no separate poll: the data is its own arrival signal.
+__device__ __forceinline__ void st_ll(uint4* p, double v, unsigned tag) {
+  const unsigned lo = (unsigned)__double2loint(v), hi = (unsigned)__double2hiint(v);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "r"(lo), "r"(tag),
+               "r"(hi), "r"(tag)
+               : "memory");
 }
-__device__ __forceinline__ void st_release(long long* p, long long v) {
-  asm volatile("st.release.gpu.global.s64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ bool ld_ll(const uint4* p, unsigned tag, double& v) {
+  unsigned a, b, c, d;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "l"(p)
+               : "memory");
+  v = __hiloint2double((int)c, (int)a);
+  return b == tag && d == tag;
 }
 
 struct ResArgs {
@@ -51,19 +69,17 @@ struct ResArgs {
   const int* rp;
   const int* ci;
   const double* v;
-  const int* nbr_ptr;
-  const int* nbr;
   const double* x;    // input vector (contiguous)
   double* out;        // sum_j mu_j T_j x
-  double* buf[3];     // exchange buffers (n doubles each)
+  uint4* xch[4];      // exchange buffers (n tagged entries each)
   const double* mu;   // k + 1 coefficients (device)
   double c, invd;
-  long long* flags;   // one degree counter per tile (monotone across launches)
+  unsigned* epoch;    // tag base: advanced by kdeg at the end of every launch
   const Ctl* halt;
   int cap_nnz;        // shared-memory capacity of a tile's entries
 };
 
-constexpr long long kSpinLimit = 1ll << 24;
+constexpr int kSpinLimit = 1 << 22;
 
 // RPT rows per thread; T threads per CTA (blockDim.x).
 template <int RPT>
@@ -88,8 +104,7 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (a.halt && a.halt->halted) return;
-  const long long f0 = ld_acquire(a.flags + b);  // every tile ended the last launch at this value
-  const int nb0 = a.nbr_ptr[b], nb1 = a.nbr_ptr[b + 1];
+  const unsigned tag0 = *a.epoch;  // advanced by k_epoch_advance after every application
 
   double prev[RPT], cur[RPT], acc_out[RPT];
   int ps[RPT], pe[RPT];
@@ -110,20 +125,36 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
     pe[q] = lr < rows ? s_rp[lr + 1] : 0;
   }
 
-  // row sum of A times the vector whose own tile is sx (shared) and whose other entries are in
-  // g (global: the input vector through the read-only path, exchange buffers through L2)
-  auto row_sum = [&](int q, const double* sx, const double* g, bool readonly) {
+  // Row sum of A times the vector whose own tile is sx (shared memory).  Entries outside the
+  // tile come from g (degree 1: the input vector) or from the exchange buffer xc, re-read
+  // until they carry `tag`.  Products are formed as operands arrive; the additions run in
+  // storage order.
+  auto row_sum = [&](int q, const double* sx, const double* g, const uint4* xc, unsigned tag) {
     double acc = 0.0;
     for (int p = ps[q]; p < pe[q]; p += 8) {
       double xv[8];
+      unsigned pending = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         xv[u] = 0.0;
         if (p + u < pe[q]) {
           const int col = s_col[p + u];
           const unsigned off = (unsigned)(col - r0);
-          xv[u] = off < (unsigned)rows ? sx[off] : (readonly ? __ldg(g + col) : __ldcg(g + col));
+          if (off < (unsigned)rows)
+            xv[u] = sx[off];
+          else if (g)
+            xv[u] = __ldg(g + col);
+          else if (!ld_ll(xc + col, tag, xv[u]))
+            pending |= 1u << u;
         }
+      }
+      int spins = 0;
+      while (pending) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if ((pending >> u) & 1u)
+            if (ld_ll(xc + s_col[p + u], tag, xv[u])) pending &= ~(1u << u);
+        if (++spins > kSpinLimit) __trap();  // a neighbour never arrived: fail, do not hang
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -131,67 +162,49 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
     }
     return acc;
   };
-  auto publish = [&](long long value) {
-    __syncthreads();  // every thread's exchange stores are issued; s_x hand-over
-    if (tid == 0) {
-      __threadfence();
-      st_release(a.flags + b, value);
-    }
-  };
-  auto wait_neighbours = [&](long long value) {
-    if (tid < 32) {
-      for (int q = nb0 + tid; q < nb1; q += 32) {
-        const long long* f = a.flags + a.nbr[q];
-        long long spins = 0;
-        while (ld_acquire(f) < value)
-          if (++spins > kSpinLimit) __trap();  // a neighbour never arrived: fail, do not hang
-      }
-    }
-    __syncthreads();
-  };
 
   // degree 1: T_1 = Ahat x; out = mu0 x + mu1 T_1   (filter_poly.hpp:260-269)
   {
     const double mu0 = __ldg(a.mu), mu1 = __ldg(a.mu + 1);
-    double* dst = a.buf[1];
+    uint4* dst = a.xch[1];  // slot = degree & 3
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int lr = tid + q * T;
       if (lr >= rows) continue;
-      const double t = mul(sub(row_sum(q, s_x, a.x, true), mul(a.c, prev[q])), a.invd);
+      const double t = mul(sub(row_sum(q, s_x, a.x, nullptr, 0u), mul(a.c, prev[q])), a.invd);
       cur[q] = t;
       acc_out[q] = add(add(0.0, mul(mu0, prev[q])), mul(mu1, t));
       if (a.kdeg > 1) {
-        __stcg(dst + r0 + lr, t);
+        st_ll(dst + r0 + lr, t, tag0 + 1u);
         s_x[a.tile_rows + lr] = t;
       }
     }
-    publish(f0 + 1);
+    __syncthreads();  // the tile's new vector is in shared memory for everyone
   }
   // degrees 2..k: T_j = 2 Ahat T_{j-1} - T_{j-2}; out += mu_j T_j   (filter_poly.hpp:270-276)
   for (int j = 2; j <= a.kdeg; ++j) {
-    wait_neighbours(f0 + j - 1);
     const double muj = __ldg(a.mu + j);
-    const double* src = a.buf[(j - 1) % 3];
-    double* dst = a.buf[j % 3];
+    const uint4* src = a.xch[(j - 1) & 3];
+    uint4* dst = a.xch[j & 3];
     const double* sx = s_x + ((j - 1) & 1) * a.tile_rows;
     double* sxn = s_x + (j & 1) * a.tile_rows;
     const bool more = j < a.kdeg;
+    const unsigned want = tag0 + (unsigned)(j - 1);
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int lr = tid + q * T;
       if (lr >= rows) continue;
-      const double t = mul(sub(row_sum(q, sx, src, false), mul(a.c, cur[q])), a.invd);
+      const double t = mul(sub(row_sum(q, sx, nullptr, src, want), mul(a.c, cur[q])), a.invd);
       const double tj = sub(mul(2.0, t), prev[q]);
       acc_out[q] = add(acc_out[q], mul(muj, tj));
       prev[q] = cur[q];
       cur[q] = tj;
       if (more) {
-        __stcg(dst + r0 + lr, tj);
+        st_ll(dst + r0 + lr, tj, want + 1u);
         sxn[lr] = tj;
       }
     }
-    publish(f0 + j);
+    __syncthreads();
   }
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
@@ -200,52 +213,43 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
   }
 }
 
-// per tile: smallest and largest column index of its rows
-__global__ void k_tile_col_span(int n, int tile_rows, const int* __restrict__ rp,
-                                const int* __restrict__ ci, int* __restrict__ span) {
+// per tile: bit t of mask[tile] is set when a row of the tile has an entry in tile t's columns
+constexpr int kMaskWords = 8;  // up to 256 tiles
+__global__ void k_tile_adjacency(int n, int tile_rows, const int* __restrict__ rp,
+                                 const int* __restrict__ ci, unsigned* __restrict__ mask) {
+  __shared__ unsigned s_m[kMaskWords];
+  if (threadIdx.x < kMaskWords) s_m[threadIdx.x] = 0u;
+  __syncthreads();
   const int b = blockIdx.x;
   const int r0 = b * tile_rows, r1 = min(n, r0 + tile_rows);
-  int lo = n, hi = -1;
   for (int p = rp[r0] + threadIdx.x; p < rp[r1]; p += blockDim.x) {
-    const int c = ci[p];
-    lo = min(lo, c);
-    hi = max(hi, c);
+    const int t = ci[p] / tile_rows;
+    atomicOr(&s_m[t >> 5], 1u << (t & 31));
   }
-  __shared__ int s_lo[256], s_hi[256];
-  s_lo[threadIdx.x] = lo;
-  s_hi[threadIdx.x] = hi;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      s_lo[threadIdx.x] = min(s_lo[threadIdx.x], s_lo[threadIdx.x + o]);
-      s_hi[threadIdx.x] = max(s_hi[threadIdx.x], s_hi[threadIdx.x + o]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    span[2 * b] = s_lo[0];
-    span[2 * b + 1] = s_hi[0];
-  }
+  if (threadIdx.x < kMaskWords) mask[(size_t)b * kMaskWords + threadIdx.x] = s_m[threadIdx.x];
+}
+
+__global__ void k_epoch_advance(unsigned* epoch, int kdeg, const Ctl* halt) {
+  if (halt && halt->halted) return;
+  *epoch += (unsigned)kdeg;
 }
 
 size_t res_smem_bytes(int tile_rows, int cap_nnz) {
   return (size_t)cap_nnz * 12 + (size_t)tile_rows * 16 + (size_t)(tile_rows + 1) * 4 + 16;
 }
 
+std::atomic<bool> g_resident_on{true};
+
 }  // namespace
 
-// The plan of a matrix: row tiles (one per CTA), per-tile entry capacity, neighbour lists.
+// The plan of a matrix: row tiles (one per CTA) and the per-tile entry capacity.
 struct ResidentPlan {
   int nct = 0, tile_rows = 0, threads = 0, rpt = 0, cap_nnz = 0;
   size_t smem = 0;
-  int* nbr_ptr = nullptr;  // device
-  int* nbr = nullptr;      // device
 };
 
 void resident_free(DevCsr& a) {
-  if (!a.resident) return;
-  dev_free_shared(a.resident->nbr_ptr);
-  dev_free_shared(a.resident->nbr);
   delete a.resident;
   a.resident = nullptr;
 }
@@ -266,55 +270,34 @@ void resident_build(Ctx& c, DevCsr& a) {
   const int nct = (a.n + tile_rows - 1) / tile_rows;
   const int threads = tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256);
   const int rpt = (tile_rows + threads - 1) / threads;
-  // per-tile entry counts and column spans
+  // per-tile entry counts: the largest sizes the shared-memory image
   std::vector<int> rp_tiles(nct + 1);
   for (int b = 0; b <= nct; ++b)
-    SE_CUDA(cudaMemcpyAsync(&rp_tiles[b], a.rp + std::min(a.n, b * tile_rows), sizeof(int),
-                            cudaMemcpyDeviceToHost, c.stream));
-  int* dspan = dev_alloc<int>(2 * (size_t)nct);
-  k_tile_col_span<<<nct, 256, 0, c.stream>>>(a.n, tile_rows, a.rp, a.ci, dspan);
-  SE_CUDA(cudaGetLastError());
-  ++c.launches;
-  std::vector<int> span(2 * (size_t)nct);
-  SE_CUDA(cudaMemcpyAsync(span.data(), dspan, sizeof(int) * span.size(), cudaMemcpyDeviceToHost,
-                          c.stream));
+    SE_CUDA(cudaMemcpyAsync(&rp_tiles[b], a.rp + std::min((long)a.n, (long)b * tile_rows),
+                            sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   ctx_sync(c);
-  dev_free(dspan);
   int cap = 0;
   for (int b = 0; b < nct; ++b) cap = std::max(cap, rp_tiles[b + 1] - rp_tiles[b]);
   cap = (cap + 1) & ~1;
   const size_t smem = res_smem_bytes(tile_rows, cap);
-  if (smem > (size_t)max_optin) return;
-  // neighbour tiles: every tile whose rows my columns reach, symmetrised (the write-after-read
-  // hazard of the exchange buffers is covered by waiting on the tiles that read mine)
-  std::vector<std::vector<char>> adj(nct, std::vector<char>(nct, 0));
-  for (int b = 0; b < nct; ++b) {
-    if (span[2 * b + 1] < 0) continue;
-    const int t0 = span[2 * b] / tile_rows, t1 = span[2 * b + 1] / tile_rows;
-    for (int t = t0; t <= t1; ++t)
-      if (t != b) adj[b][t] = adj[t][b] = 1;
+  if (smem > (size_t)max_optin || nct > 32 * kMaskWords) return;
+  // tile dependence must be symmetric (a tile reads exactly the tiles that read it): that is
+  // what keeps a producer from lapping a consumer on the rotating exchange buffers
+  {
+    unsigned* dmask = dev_alloc<unsigned>((size_t)nct * kMaskWords);
+    k_tile_adjacency<<<nct, 256, 0, c.stream>>>(a.n, tile_rows, a.rp, a.ci, dmask);
+    SE_CUDA(cudaGetLastError());
+    ++c.launches;
+    std::vector<unsigned> m((size_t)nct * kMaskWords);
+    SE_CUDA(cudaMemcpyAsync(m.data(), dmask, sizeof(unsigned) * m.size(), cudaMemcpyDeviceToHost,
+                            c.stream));
+    ctx_sync(c);
+    dev_free(dmask);
+    auto reads = [&](int x, int y) { return (m[(size_t)x * kMaskWords + (y >> 5)] >> (y & 31)) & 1u; };
+    for (int x = 0; x < nct; ++x)
+      for (int y = x + 1; y < nct; ++y)
+        if (reads(x, y) != reads(y, x)) return;
   }
-  std::vector<int> nptr(nct + 1, 0), nlist;
-  for (int b = 0; b < nct; ++b) {
-    for (int t = 0; t < nct; ++t)
-      if (adj[b][t]) nlist.push_back(t);
-    nptr[b + 1] = (int)nlist.size();
-  }
-  auto* p = new ResidentPlan;
-  p->nct = nct;
-  p->tile_rows = tile_rows;
-  p->threads = threads;
-  p->rpt = rpt;
-  p->cap_nnz = cap;
-  p->smem = smem;
-  p->nbr_ptr = dev_alloc_shared<int>(nptr.size());
-  p->nbr = dev_alloc_shared<int>(std::max<size_t>(nlist.size(), 1));
-  SE_CUDA(cudaMemcpyAsync(p->nbr_ptr, nptr.data(), sizeof(int) * nptr.size(), cudaMemcpyHostToDevice,
-                          c.stream));
-  if (!nlist.empty())
-    SE_CUDA(cudaMemcpyAsync(p->nbr, nlist.data(), sizeof(int) * nlist.size(),
-                            cudaMemcpyHostToDevice, c.stream));
-  ctx_sync(c);
   // the launch must be able to hold every CTA at once
   auto fits = [&](auto kern) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin) != cudaSuccess) {
@@ -329,20 +312,24 @@ void resident_build(Ctx& c, DevCsr& a) {
     return (long)per_sm * c.num_sms >= nct;
   };
   const bool ok = rpt == 1 ? fits(k_cheb_resident<1>) : rpt == 2 ? fits(k_cheb_resident<2>) : false;
+  if (!ok) return;
+  auto* p = new ResidentPlan;
+  p->nct = nct;
+  p->tile_rows = tile_rows;
+  p->threads = threads;
+  p->rpt = rpt;
+  p->cap_nnz = cap;
+  p->smem = smem;
   a.resident = p;
-  if (!ok) resident_free(a);
 }
 
-namespace {
-std::atomic<bool> g_resident_on{true};
-}
 void resident_enable(bool on) { g_resident_on.store(on); }
 bool resident_enabled() { return g_resident_on.load(); }
 int resident_tiles(const DevCsr& a) { return a.resident && resident_enabled() ? a.resident->nct : 0; }
+size_t resident_state_bytes(const DevCsr& a) { return 4 * (size_t)a.n * sizeof(uint4) + 16; }
 
 void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, double cc, double invd,
-                   const double* x, double* out, double* const* buf, long long* flags,
-                   const Ctl* halt) {
+                   const double* x, double* out, void* state, const Ctl* halt) {
   const ResidentPlan& p = *a.resident;
   ResArgs g{};
   g.n = a.n;
@@ -351,15 +338,15 @@ void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, doub
   g.rp = a.rp;
   g.ci = a.ci;
   g.v = a.v;
-  g.nbr_ptr = p.nbr_ptr;
-  g.nbr = p.nbr;
   g.x = x;
   g.out = out;
-  for (int q = 0; q < 3; ++q) g.buf[q] = buf[q];
+  // state: [epoch (16 bytes)] [4 exchange buffers of n tagged entries]
+  g.epoch = static_cast<unsigned*>(state);
+  uint4* xch = reinterpret_cast<uint4*>(static_cast<unsigned char*>(state) + 16);
+  for (int q = 0; q < 4; ++q) g.xch[q] = xch + (size_t)q * a.n;
   g.mu = mu_dev;
   g.c = cc;
   g.invd = invd;
-  g.flags = flags;
   g.halt = halt;
   g.cap_nnz = p.cap_nnz;
   cudaLaunchConfig_t cfg{};
@@ -378,7 +365,11 @@ void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, doub
     SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<1>, g));
   else
     SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<2>, g));
-  ++c.launches;
+  // the next application's tags start past this one's (a separate, stream-ordered launch: a
+  // tile far from tile 0 in the matrix graph may start after tile 0 has finished a short filter)
+  k_epoch_advance<<<1, 1, 0, c.stream>>>(g.epoch, kdeg, halt);
+  SE_CUDA(cudaGetLastError());
+  c.launches += 2;
 }
 
 }  // namespace k

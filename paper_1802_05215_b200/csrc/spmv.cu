@@ -591,6 +591,136 @@ __global__ void __launch_bounds__(kKpmThreads, kEllMinB) k_kpm_ell(
   kpm_finish(f0, f1, b, first, dbl, partial, counter, zeta, kmom);
 }
 
+// ---- block filter degree on a row-major vector block (K2, padded-row matrices) ------------------
+// The block filter of cheb_si / the block apply_pol for matrices with <= kEllW entries per row
+// (stencils): kBV = 8 vectors stored row-major (n x 8, one 64-byte line per row), 4 lanes x 2
+// vectors per row, 8 rows per warp and sweep.  A row's entries are read once for all 8 vectors
+// (two 16-byte column loads and four 16-byte value loads shared by the row's 4 lanes), every
+// gather is a 16-byte piece of a 64-byte line, column indices are loaded one sweep ahead and the
+// next sweep's gather rows are prefetched into L2 -- the structure of k_kpm_ell, with the
+// filter's update (filter_poly.hpp:260-276) instead of the moment dots.  Row sums run in storage
+// order with individually rounded products; the pad entries add 0 * x, so each vector's result is
+// the single-vector kernel's (and the reference's) bit for bit.
+constexpr int kBV = 8;
+constexpr int kBlkThreads = 256;
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kBlkThreads, 3) k_cheb_ell_block(
+    int n, const int* __restrict__ ec, const double* __restrict__ ea,
+    const double* __restrict__ X,     // T_{j-1} (FIRST: the input block v)
+    const double* __restrict__ P,     // T_{j-2} (unused when FIRST)
+    double* __restrict__ Y,           // T_j
+    double* __restrict__ O,           // running sum (FIRST: written, else updated)
+    double cc, double invd, double mu0, double muj) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, g = lane >> 2, l4 = lane & 3;
+  const int warps = (int)(gridDim.x * (kBlkThreads / 32));
+  const int nb = (n + 7) / 8;
+  int rb = (int)(blockIdx.x * (kBlkThreads / 32) + (threadIdx.x >> 5));
+  auto load_cols = [&](int rbq, int4& lo, int4& hi) {
+    const int r = 8 * rbq + g;
+    lo = make_int4(0, 0, 0, 0);
+    hi = lo;
+    if (rbq < nb && r < n) {
+      lo = __ldg(reinterpret_cast<const int4*>(ec + (size_t)r * kEllW));
+      hi = __ldg(reinterpret_cast<const int4*>(ec + (size_t)r * kEllW + 4));
+    }
+  };
+  // prefetch: the 8 rows x 8 entries of the sweep one stride ahead are 64 column indices; lane
+  // (g, l4) prefetches the rows named by entries l4 and l4 + 4 of row g
+  int4 cl, ch;
+  load_cols(rb, cl, ch);
+  for (; rb < nb; rb += warps) {
+    int4 nl, nh;
+    load_cols(rb + warps, nl, nh);
+    {
+      const int c0 = l4 == 0 ? nl.x : l4 == 1 ? nl.y : l4 == 2 ? nl.z : nl.w;
+      const int c1 = l4 == 0 ? nh.x : l4 == 1 ? nh.y : l4 == 2 ? nh.z : nh.w;
+      if (rb + warps < nb && 8 * (rb + warps) + g < n) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (size_t)c0 * kBV));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (size_t)c1 * kBV));
+      }
+    }
+    const int r = 8 * rb + g;
+    if (r < n) {
+      const size_t o = (size_t)r * kBV + 2 * l4;
+      const int cs[kEllW] = {cl.x, cl.y, cl.z, cl.w, ch.x, ch.y, ch.z, ch.w};
+      double2 x[kEllW];
+#pragma unroll
+      for (int u = 0; u < kEllW; ++u)
+        x[u] = __ldg(reinterpret_cast<const double2*>(X + (size_t)cs[u] * kBV + 2 * l4));
+      const double2 xr = cs[kEllW - 1] == r ? x[kEllW - 1]
+                                            : __ldg(reinterpret_cast<const double2*>(X + o));
+      double2 pr = make_double2(0.0, 0.0), ov = pr;
+      if (!FIRST) {
+        pr = __ldg(reinterpret_cast<const double2*>(P + o));
+        ov = *reinterpret_cast<const double2*>(O + o);
+      }
+      const double2* ap = reinterpret_cast<const double2*>(ea + (size_t)r * kEllW);
+      double av[kEllW];
+#pragma unroll
+      for (int q = 0; q < kEllW / 2; ++q) {
+        const double2 e = __ldg(ap + q);
+        av[2 * q] = e.x;
+        av[2 * q + 1] = e.y;
+      }
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < kEllW; ++u) {
+        acc.x = add(acc.x, mul(av[u], x[u].x));
+        acc.y = add(acc.y, mul(av[u], x[u].y));
+      }
+      // Ahat x = (A x - c x) * (1/d)   (filter_poly.hpp:265)
+      const double2 t = make_double2(mul(sub(acc.x, mul(cc, xr.x)), invd),
+                                     mul(sub(acc.y, mul(cc, xr.y)), invd));
+      if (FIRST) {
+        *reinterpret_cast<double2*>(Y + o) = t;
+        *reinterpret_cast<double2*>(O + o) =
+            make_double2(add(add(0.0, mul(mu0, xr.x)), mul(muj, t.x)),
+                         add(add(0.0, mul(mu0, xr.y)), mul(muj, t.y)));
+      } else {
+        const double2 tj = make_double2(sub(mul(2.0, t.x), pr.x), sub(mul(2.0, t.y), pr.y));
+        *reinterpret_cast<double2*>(Y + o) = tj;
+        *reinterpret_cast<double2*>(O + o) =
+            make_double2(add(ov.x, mul(muj, tj.x)), add(ov.y, mul(muj, tj.y)));
+      }
+    }
+    cl = nl;
+    ch = nh;
+  }
+}
+
+// column-major (nv columns, ld n) -> row-major n x 8 (columns nv..7 zero), and back
+__global__ void __launch_bounds__(256) k_block_pack(const double* __restrict__ cm, double* __restrict__ rm,
+                                                    int n, int nv) {
+  __shared__ double tile[kBV][33];
+  const int i0 = blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 32 * kBV; e += 256) {
+    const int l = e >> 5, i = e & 31;
+    tile[l][i] = (l < nv && i0 + i < n) ? cm[(size_t)l * n + i0 + i] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * kBV; e += 256) {
+    const int i = e >> 3, l = e & 7;
+    if (i0 + i < n) rm[(size_t)(i0 + i) * kBV + l] = tile[l][i];
+  }
+}
+__global__ void __launch_bounds__(256) k_block_unpack(const double* __restrict__ rm, double* __restrict__ cm,
+                                                      int n, int nv) {
+  __shared__ double tile[kBV][33];
+  const int i0 = blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 32 * kBV; e += 256) {
+    const int i = e >> 3, l = e & 7;
+    if (i0 + i < n) tile[l][i] = rm[(size_t)(i0 + i) * kBV + l];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * kBV; e += 256) {
+    const int l = e >> 5, i = e & 31;
+    if (l < nv && i0 + i < n) cm[(size_t)l * n + i0 + i] = tile[l][i];
+  }
+}
+
 // CSR -> padded rows (kEllW per row; pad col = row, val = 0), one thread per row
 __global__ void k_build_ell(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                             const double* __restrict__ v, int* __restrict__ ec, double* __restrict__ ea) {
@@ -758,6 +888,54 @@ void spmv_cheb_multi(Ctx& c, const DevCsr& a, const MultiArgs& args) {
   cfg.numAttrs = 2;
   SE_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_cheb_multi, a.n, (const int*)a.rp, (const int*)a.ci,
                              (const double*)a.v, args));
+  ++c.launches;
+}
+
+bool cheb_block_available(const DevCsr& a) { return a.ell_c != nullptr && a.n > 0; }
+
+void cheb_block_pack(Ctx& c, const double* cm, double* rm, int n, int nv) {
+  k_block_pack<<<(n + 31) / 32, 256, 0, c.stream>>>(cm, rm, n, nv);
+  SE_CUDA(cudaGetLastError());
+  ++c.launches;
+}
+void cheb_block_unpack(Ctx& c, const double* rm, double* cm, int n, int nv) {
+  k_block_unpack<<<(n + 31) / 32, 256, 0, c.stream>>>(rm, cm, n, nv);
+  SE_CUDA(cudaGetLastError());
+  ++c.launches;
+}
+
+void cheb_block_step(Ctx& c, const DevCsr& a, bool first, const double* X, const double* P,
+                     double* Y, double* O, double cc, double invd, double mu0, double muj) {
+  if (!a.ell_c) fail(SE_EINVAL, "internal: block filter needs the padded-row copy");
+  // one contiguous sweep window: the grid is exactly the resident CTAs
+  static int per_sm[2] = {0, 0};
+  int& occ = per_sm[first ? 1 : 0];
+  if (occ == 0) {
+    if (first)
+      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cheb_ell_block<true>, kBlkThreads, 0));
+    else
+      SE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cheb_ell_block<false>, kBlkThreads, 0));
+    occ = std::max(occ, 1);
+  }
+  const int nb = (a.n + 7) / 8;
+  const int want = (nb + kBlkThreads / 32 - 1) / (kBlkThreads / 32);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)std::max(1, std::min(want, occ * c.num_sms)));
+  cfg.blockDim = dim3(kBlkThreads);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = c.prio_hi;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  if (first)
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_ell_block<true>, a.n, (const int*)a.ell_c,
+                               (const double*)a.ell_a, X, P, Y, O, cc, invd, mu0, muj));
+  else
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_ell_block<false>, a.n, (const int*)a.ell_c,
+                               (const double*)a.ell_a, X, P, Y, O, cc, invd, mu0, muj));
   ++c.launches;
 }
 

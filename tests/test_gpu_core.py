@@ -303,3 +303,25 @@ def test_resident_filter_in_the_slice_solve(gpu_ctx):
         api.set_resident_filter(True)
     assert r1.niter == r0.niter and np.array_equal(r1.eigenvalues, r0.eigenvalues)
     assert np.array_equal(r1.residuals, r0.residuals)
+
+
+@pytest.mark.parametrize("case,ncols", [("irr8", 11), ("lap3d", 8), ("lap2d", 3), ("banded", 5)])
+def test_block_filter_bitwise(gpu_ctx, case, ncols):
+    """Block apply_pol: the row-major 8-vector block kernel on padded-row matrices (stencils, an
+    irregular matrix with 0..8 entries per row and empty rows; full, split and narrow groups) and
+    the CSR multi-vector kernel on longer rows -- every column bitwise the oracle's apply_pol."""
+    api = _api()
+    if case == "lap3d":
+        a, (lo, hi) = api.gen_laplacian([17, 13, 11]), (0.0, 12.0)
+    elif case == "lap2d":
+        a, (lo, hi) = api.gen_laplacian([33, 29]), (0.0, 8.0)
+    elif case == "irr8":
+        a, (lo, hi) = _irregular(3001, 7, 8), (-4.0, 6.0)
+    else:
+        a, (lo, hi) = api.gen_random_sparse(3000, 3), (-12.0, 18.0)
+    f = api.find_pol(lo + 0.31 * (hi - lo), lo + 0.40 * (hi - lo), api.SpectralBounds(lo, hi))
+    X = clib.rng_vectors(9, "normal", a.n, ncols)
+    out = api.apply_pol(f, a, X)
+    for j in range(ncols):
+        ref = clib.apply_pol(a.row_ptr, a.col_idx, a.vals, f.mu, f.c, f.d, X[j])
+        assert np.array_equal(out[j], ref), (j, np.max(np.abs(out[j] - ref)))
