@@ -888,10 +888,11 @@ def _d_matvec(d: "DeviceCsr", x) -> np.ndarray:
 SAMPLE_VECTORS = 0
 
 
-def set_resident_filter(on: bool) -> None:
+def set_resident_filter(on) -> None:
     """Process-wide switch of the resident (one launch for all degrees) filter; results are
-    bit-identical either way.  Default on."""
-    call("se_resident_filter", int(bool(on)))
+    bit-identical either way.  Default on (1); 2 selects 1024-thread tiles for matrices uploaded
+    afterwards (a measurement variant)."""
+    call("se_resident_filter", int(on))
 
 
 def resident_tiles(d) -> int:

@@ -499,7 +499,7 @@ int se_cgs2_bench(se_ctx* ctx, int n, int k, int reps, int mode, double* ms) {
 }
 
 int se_resident_filter(int enable) {
-  return guard([&] { k::resident_enable(enable != 0); });
+  return guard([&] { k::resident_enable(enable); });
 }
 
 int se_csr_resident_tiles(const se_csr* a, int* tiles) {

@@ -82,8 +82,8 @@ struct ResArgs {
 constexpr int kSpinLimit = 1 << 22;
 
 // RPT rows per thread; T threads per CTA (blockDim.x).
-template <int RPT>
-__global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
+template <int RPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_cheb_resident(ResArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = blockDim.x, tid = threadIdx.x;
   const int b = blockIdx.x;
@@ -125,53 +125,91 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
     pe[q] = lr < rows ? s_rp[lr + 1] : 0;
   }
 
-  // Row sum of A times the vector whose own tile is sx (shared memory).  Entries outside the
-  // tile come from g (degree 1: the input vector) or from the exchange buffer xc, re-read
-  // until they carry `tag`.  Products are formed as operands arrive; the additions run in
-  // storage order.
-  auto row_sum = [&](int q, const double* sx, const double* g, const uint4* xc, unsigned tag) {
-    double acc = 0.0;
-    for (int p = ps[q]; p < pe[q]; p += 8) {
-      double xv[8];
-      unsigned pending = 0;
+  // Row sums of A times the vector whose own tile is sx (shared memory), for all of the thread's
+  // rows at once.  Entries outside the tile come from g (degree 1: the input vector) or from the
+  // exchange buffer xc.  The loads of ALL rows are issued first -- remote ones included, whatever
+  // their tags say -- so the L2 round trip of the exchange overlaps the shared-memory work; only
+  // then are the tags checked, entries that had not arrived re-read until they carry `tag`, and
+  // each row summed in storage order.  Rows longer than 8 entries continue 8 at a time.
+  auto row_sums = [&](const double* sx, const double* g, const uint4* xc, unsigned tag,
+                      double (&acc)[RPT]) {
+    double xv[RPT][8];
+    unsigned pending[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      pending[q] = 0;
+      acc[q] = 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        xv[u] = 0.0;
-        if (p + u < pe[q]) {
-          const int col = s_col[p + u];
+        xv[q][u] = 0.0;
+        if (ps[q] + u < pe[q]) {
+          const int col = s_col[ps[q] + u];
           const unsigned off = (unsigned)(col - r0);
           if (off < (unsigned)rows)
-            xv[u] = sx[off];
+            xv[q][u] = sx[off];
           else if (g)
-            xv[u] = __ldg(g + col);
-          else if (!ld_ll(xc + col, tag, xv[u]))
-            pending |= 1u << u;
+            xv[q][u] = __ldg(g + col);
+          else if (!ld_ll(xc + col, tag, xv[q][u]))
+            pending[q] |= 1u << u;
         }
       }
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
       int spins = 0;
-      while (pending) {
+      while (pending[q]) {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if ((pending >> u) & 1u)
-            if (ld_ll(xc + s_col[p + u], tag, xv[u])) pending &= ~(1u << u);
+          if ((pending[q] >> u) & 1u)
+            if (ld_ll(xc + s_col[ps[q] + u], tag, xv[q][u])) pending[q] &= ~(1u << u);
         if (++spins > kSpinLimit) __trap();  // a neighbour never arrived: fail, do not hang
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (p + u < pe[q]) acc = add(acc, mul(s_val[p + u], xv[u]));
+        if (ps[q] + u < pe[q]) acc[q] = add(acc[q], mul(s_val[ps[q] + u], xv[q][u]));
+      for (int p = ps[q] + 8; p < pe[q]; p += 8) {  // long rows: the remaining entries
+        double yv[8];
+        unsigned pend = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          yv[u] = 0.0;
+          if (p + u < pe[q]) {
+            const int col = s_col[p + u];
+            const unsigned off = (unsigned)(col - r0);
+            if (off < (unsigned)rows)
+              yv[u] = sx[off];
+            else if (g)
+              yv[u] = __ldg(g + col);
+            else if (!ld_ll(xc + col, tag, yv[u]))
+              pend |= 1u << u;
+          }
+        }
+        spins = 0;
+        while (pend) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if ((pend >> u) & 1u)
+              if (ld_ll(xc + s_col[p + u], tag, yv[u])) pend &= ~(1u << u);
+          if (++spins > kSpinLimit) __trap();
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (p + u < pe[q]) acc[q] = add(acc[q], mul(s_val[p + u], yv[u]));
+      }
     }
-    return acc;
   };
 
+  double rs[RPT];
   // degree 1: T_1 = Ahat x; out = mu0 x + mu1 T_1   (filter_poly.hpp:260-269)
   {
     const double mu0 = __ldg(a.mu), mu1 = __ldg(a.mu + 1);
     uint4* dst = a.xch[1];  // slot = degree & 3
+    row_sums(s_x, a.x, nullptr, 0u, rs);
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int lr = tid + q * T;
       if (lr >= rows) continue;
-      const double t = mul(sub(row_sum(q, s_x, a.x, nullptr, 0u), mul(a.c, prev[q])), a.invd);
+      const double t = mul(sub(rs[q], mul(a.c, prev[q])), a.invd);
       cur[q] = t;
       acc_out[q] = add(add(0.0, mul(mu0, prev[q])), mul(mu1, t));
       if (a.kdeg > 1) {
@@ -190,11 +228,12 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
     double* sxn = s_x + (j & 1) * a.tile_rows;
     const bool more = j < a.kdeg;
     const unsigned want = tag0 + (unsigned)(j - 1);
+    row_sums(sx, nullptr, src, want, rs);
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int lr = tid + q * T;
       if (lr >= rows) continue;
-      const double t = mul(sub(row_sum(q, sx, nullptr, src, want), mul(a.c, cur[q])), a.invd);
+      const double t = mul(sub(rs[q], mul(a.c, cur[q])), a.invd);
       const double tj = sub(mul(2.0, t), prev[q]);
       acc_out[q] = add(acc_out[q], mul(muj, tj));
       prev[q] = cur[q];
@@ -239,7 +278,7 @@ size_t res_smem_bytes(int tile_rows, int cap_nnz) {
   return (size_t)cap_nnz * 12 + (size_t)tile_rows * 16 + (size_t)(tile_rows + 1) * 4 + 16;
 }
 
-std::atomic<bool> g_resident_on{true};
+std::atomic<int> g_resident_mode{1};  // 0 off; 1: <= 512 threads a tile; 2: <= 1024
 
 }  // namespace
 
@@ -268,8 +307,11 @@ void resident_build(Ctx& c, DevCsr& a) {
   tile_rows = (tile_rows + 31) / 32 * 32;
   if (tile_rows > 2048) return;
   const int nct = (a.n + tile_rows - 1) / tile_rows;
-  const int threads = tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256);
-  const int rpt = (tile_rows + threads - 1) / threads;
+  // at most 512 threads, so a thread may hold the operands of all its rows (up to 4 x 8
+  // entries) in registers while the exchange loads are in flight
+  const int maxt = g_resident_mode.load() == 2 ? 1024 : 512;
+  const int threads = tile_rows > 512 ? maxt : (tile_rows > 256 ? 512 : 256);
+  const int rpt = tile_rows <= threads ? 1 : (tile_rows <= 2 * threads ? 2 : 4);
   // per-tile entry counts: the largest sizes the shared-memory image
   std::vector<int> rp_tiles(nct + 1);
   for (int b = 0; b <= nct; ++b)
@@ -311,7 +353,10 @@ void resident_build(Ctx& c, DevCsr& a) {
     }
     return (long)per_sm * c.num_sms >= nct;
   };
-  const bool ok = rpt == 1 ? fits(k_cheb_resident<1>) : rpt == 2 ? fits(k_cheb_resident<2>) : false;
+  const bool ok = threads == 1024 ? fits(k_cheb_resident<2, 1024>)
+                  : rpt == 1      ? fits(k_cheb_resident<1, 512>)
+                  : rpt == 2      ? fits(k_cheb_resident<2, 512>)
+                                  : fits(k_cheb_resident<4, 512>);
   if (!ok) return;
   auto* p = new ResidentPlan;
   p->nct = nct;
@@ -323,8 +368,8 @@ void resident_build(Ctx& c, DevCsr& a) {
   a.resident = p;
 }
 
-void resident_enable(bool on) { g_resident_on.store(on); }
-bool resident_enabled() { return g_resident_on.load(); }
+void resident_enable(int mode) { g_resident_mode.store(mode); }
+bool resident_enabled() { return g_resident_mode.load() != 0; }
 int resident_tiles(const DevCsr& a) { return a.resident && resident_enabled() ? a.resident->nct : 0; }
 size_t resident_state_bytes(const DevCsr& a) { return 4 * (size_t)a.n * sizeof(uint4) + 16; }
 
@@ -361,10 +406,14 @@ void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, doub
   attr[1].val.priority = c.prio_hi;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  if (p.rpt == 1)
-    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<1>, g));
+  if (p.threads == 1024)
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<2, 1024>, g));
+  else if (p.rpt == 1)
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<1, 512>, g));
+  else if (p.rpt == 2)
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<2, 512>, g));
   else
-    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<2>, g));
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<4, 512>, g));
   // the next application's tags start past this one's (a separate, stream-ordered launch: a
   // tile far from tile 0 in the matrix graph may start after tile 0 has finished a short filter)
   k_epoch_advance<<<1, 1, 0, c.stream>>>(g.epoch, kdeg, halt);
