@@ -191,7 +191,27 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
         _lib.call("se_filter_bench", ctx.handle, A.handle, C.byref(s), 3, C.byref(ms2), C.byref(nl),
                   C.byref(byt))
         out[tag] = (byt.value / (ms2.value * 1e-3) / 1e9, ms2.value * 1e-3 / nl.value, byt.value / nl.value)
+        if tag == "workload":
+            out["workload_resident"] = api.resident_tiles(A) > 0
+            # the same chain as one launch per degree (the resident filter switched off)
+            api.set_resident_filter(0)
+            try:
+                _lib.call("se_filter_bench", ctx.handle, A.handle, C.byref(s), 3, C.byref(ms2),
+                          C.byref(nl), C.byref(byt))
+                out["workload_per_degree_us"] = ms2.value * 1e3 / nl.value
+            finally:
+                api.set_resident_filter(1)
+        else:  # the 8-vector block filter (cheb_si / block apply_pol) on the same matrix
+            msb = C.c_double()
+            _lib.call("se_block_filter_bench", ctx.handle, A.handle, 60, 3, C.byref(msb))
+            per_b = msb.value / (60 * 3) * 1e-3
+            by_b = 12.0 * A.nnz + 4.0 * (A.n + 1) + 40.0 * A.n * 8
+            out["block"] = (by_b / per_b / 1e9, per_b, by_b)
         A.free()
+    # Rayleigh-Ritz contraction U = W Y on the workload's widest slice (fp64 tensor cores)
+    gm, gn, gk = n, 720, 2880
+    g_ms = api.mult_cols_bench(gm, gn, gk, a_rowmajor=True, reps=2, ctx=ctx)
+    out["gemm"] = (2.0 * gm * gn * gk / (g_ms * 1e-3) / 1e12, g_ms, (gm, gn, gk))
     # KPM block-step (K3) on BASELINE cfg3's matrix (160^3, 16 Rademacher probes per block,
     # doubling recurrence: bytes Abytes + 24 n b per step)
     A = api.DeviceCsr.laplacian([160, 160, 160], ctx)
@@ -226,8 +246,24 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
                                           "frac": round(out["hbm"][0] / peak, 4),
                                           "us_per_launch": round(out["hbm"][1] * 1e6, 2),
                                           "traffic": _t("spmv_cheb_160cubed")},
-                            "workload_64^3_L2_resident": {"achieved": round(out["workload"][0], 1),
-                                                          "us_per_launch": round(out["workload"][1] * 1e6, 2)}},
+                            "workload_64^3_L2_resident": {
+                                "kernel": ("k_cheb_resident: all degrees of one filter application "
+                                           "in one cooperative launch, matrix tiles in shared memory"
+                                           if out.get("workload_resident") else "k_spmv_cheb per degree"),
+                                "achieved": round(out["workload"][0], 1),
+                                "us_per_degree": round(out["workload"][1] * 1e6, 2),
+                                "us_per_degree_one_launch_per_degree":
+                                    round(out.get("workload_per_degree_us", 0.0), 2)}},
+            "block_filter": {"kernel": "k_cheb_ell_block (8-vector filter degree, row-major block; "
+                                       "filter_poly.hpp:256-277 per column)",
+                             "shape": "160^3, 8 vectors", "achieved": round(out["block"][0], 1),
+                             "frac": round(out["block"][0] / peak, 4),
+                             "us_per_degree": round(out["block"][1] * 1e6, 2),
+                             "bytes_per_degree": round(out["block"][2])},
+            "ritz_gemm": {"kernel": "k_ritz_gemm (DMMA m8n8k4 f64): U = W Y, eigensolvers.hpp:275-283",
+                          "bound": "tensor (fp64)", "shape": list(out["gemm"][2]),
+                          "achieved_tflops_fp64": round(out["gemm"][0], 1),
+                          "ms": round(out["gemm"][1], 2)},
             "kpm_block_step": {"kernel": "k_kpm_ell (16-probe block, padded rows, doubling; dos.hpp:96-110)",
                                "shape": "160^3 (BASELINE cfg3 matrix), b=16",
                                "achieved": round(out["kpm"][0], 1), "frac": round(out["kpm"][0] / peak, 4),
