@@ -511,7 +511,8 @@ def main():
         roof["in_situ"] = {
             "what": "CGS2 bytes of one timed step (every streamed basis column, 8 n each, + vector "
                     "traffic; device counters of all slices) / that step's wall time: the rate the "
-                    "dominant kernel class sustains inside the concurrent step",
+                    "dominant kernel class sustains inside the whole step (filter and Ritz "
+                    "extraction included in the denominator)",
             "orth_bytes_per_step": obytes, "orth_passes": passes, "mean_cols": mean_cols,
             "step_s": round(step_s, 3), "achieved": round(rate, 1),
             "frac": round(rate / roof["peak"], 4)}

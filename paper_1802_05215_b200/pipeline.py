@@ -449,8 +449,13 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
                 wk = trim_to_slice(r.eigenvalues, r.residuals, w, nw, wlo, whi, delta)
                 vals.append(np.asarray(r.eigenvalues)[wk])
                 ress.append(np.asarray(r.residuals)[wk])
-                wv = (np.asarray(r.vectors)[:, wk]
-                      if plan.want_vectors and r.vectors is not None else None)
+                wv = None
+                if plan.want_vectors and r.vectors is not None:
+                    # seam trimming drops at most a few columns, usually none: no copy then
+                    # (a fancy-indexed copy of a 1 GB block costs more than its D2H)
+                    wv = np.asarray(r.vectors)
+                    if wk.size != wv.shape[1]:
+                        wv = wv[:, wk]
                 if wv is not None and sink is None:
                     vecs.append(wv)
                 out.degree = max(out.degree, k)
@@ -483,7 +488,8 @@ def run(plan: Plan, backend, dist: Optional[Dist] = None, sink=None) -> Pipeline
             out.eigenvalues = allv[keep]
             out.residuals = np.concatenate(ress)[keep] if ress else np.zeros(0)
             if vecs:
-                out.vectors = (vecs[0] if len(vecs) == 1 else np.concatenate(vecs, axis=1))[:, keep]
+                allvec = vecs[0] if len(vecs) == 1 else np.concatenate(vecs, axis=1)
+                out.vectors = allvec if keep.size == allvec.shape[1] else allvec[:, keep]
         except Exception as e:  # per-slice failure is recorded (sliceeig_main.cpp:506-514)
             out.error = f"{type(e).__name__}: {e}"
         out.seconds = time.perf_counter() - ts
