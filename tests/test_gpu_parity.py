@@ -553,3 +553,29 @@ def test_tr_chunked_candidates_and_staged_restart(gpu_ctx):
         assert res.eigenvalues.size == truth.size, (res.eigenvalues.size, truth.size)
         assert np.all(np.abs(res.eigenvalues - truth) <= 1e-10 * np.abs(truth))
         assert np.all(res.residuals <= 1e-8 * np.maximum(1.0, np.abs(res.eigenvalues)))
+
+
+def test_sampled_vectors_of_a_device_resident_result(gpu_ctx):
+    """Results too large to download whole (cfg4/cfg5 at full size) stay on the device; with
+    want_vectors=False and api.SAMPLE_VECTORS a driver still hands back a few eigenvectors
+    (se_results_vector).  They are the same columns as the full download, ascending order
+    included (the result adopts the locked set's buffer after an in-place permutation)."""
+    api = _api()
+    a = api.gen_laplacian([30, 30])
+    f = api.find_pol(0.5, 0.9, api.SpectralBounds(0.0, 8.0))
+    cfg = api.SolverConfig(est_count=40)
+    full = api.cheb_lan_tr(a, None, f, 0.5, 0.9, cfg)
+    assert np.all(np.diff(full.eigenvalues) >= 0)
+    for j in range(full.eigenvalues.size):  # every column pairs with its eigenvalue
+        lam, res = api.rayleigh_and_residual(a, None, np.ascontiguousarray(full.vectors[:, j]))
+        assert abs(lam - full.eigenvalues[j]) <= 1e-10 * abs(lam) and res <= 1e-8
+    api.SAMPLE_VECTORS = 5
+    try:
+        part = api.cheb_lan_tr(a, None, f, 0.5, 0.9, cfg, want_vectors=False)
+    finally:
+        api.SAMPLE_VECTORS = 0
+    assert part.vectors is None and part.sample_index is not None
+    assert np.array_equal(part.eigenvalues, full.eigenvalues)
+    assert 2 <= part.sample_index.size <= 5
+    for q, j in enumerate(part.sample_index):
+        assert np.array_equal(part.sample_vectors[:, q], full.vectors[:, j])
