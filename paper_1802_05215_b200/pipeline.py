@@ -44,6 +44,8 @@ class Plan:
     seed: int = 1234
     bounds: Optional[tuple] = None  # fixed (lmin, lmax) skips the bounds stage
     solver_m: int = 0              # SolverConfig.m override (0: reference default)
+    solver_max_its: int = 0        # SolverConfig.max_its override (0: 40 est + 300); a smaller
+                                   # budget ends a slice early with hit_max_its, as in the reference
     jobs: int = 0                  # concurrent slices per rank (0: all of the rank's slices)
     only: Optional[Sequence[int]] = None  # debug/profiling: solve only these slice indices
     want_vectors: bool = False
@@ -359,7 +361,8 @@ class GpuBackend:
         A = api.DeviceCsr(self.A.handle, ctx)  # se_csr is shareable across contexts on a device
         try:
             f = api.find_pol(lo, hi, api.SpectralBounds(lmin, lmax), api.PolyOpts(damping=plan.damping))
-            cfg = api.SolverConfig(m=m or plan.solver_m, res_tol=plan.tol, seed=plan.seed,
+            cfg = api.SolverConfig(m=m or plan.solver_m, max_its=plan.solver_max_its,
+                                   res_tol=plan.tol, seed=plan.seed,
                                    est_count=max(1, int(math.ceil(est))))
             if plan.solver == "si":  # filtered subspace iteration (eigensolvers.hpp:760-940)
                 r = api.cheb_si(A, None, f, lo, hi, cfg.est_count, cfg, want_vectors=plan.want_vectors)

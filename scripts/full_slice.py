@@ -42,6 +42,9 @@ def main():
     ap.add_argument("--slice", type=int, default=0)
     ap.add_argument("--max-windows", type=int, default=0, help="cfg4: solve only the first W windows")
     ap.add_argument("--sample", type=int, default=16, help="re-checked vectors per window")
+    ap.add_argument("--max-its", type=int, default=0,
+                    help="Lanczos step budget (SolverConfig.max_its): a bounded partial solve that "
+                         "returns the pairs converged so far with hit_max_its, as the reference does")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     out_path = a.out or f"gpurun_out/full_slice_{a.which}.json"
@@ -62,7 +65,7 @@ def main():
         xi, eta = cfg4_window(be0, 1234)
         plan = Plan(xi=xi, eta=eta, ns=8, solver="tr", damping="sigma", dos_m=100, dos_nvec=40,
                     dos_npts=3000, probes="rademacher", tol=1e-9, seed=1234, only=[a.slice],
-                    want_vectors=False)
+                    want_vectors=False, solver_max_its=a.max_its)
         api.SAMPLE_VECTORS = a.sample  # 83 GB of eigenvectors stay on the device; a sample is checked
         desc = ("cfg4: random banded (half-width 3) + 8 extras, n = 2,000,000 (seed 1234), middle 2% "
                 "of the DOS ([t_0.49, t_0.51]) in 8 DOS slices, ChebLanTr tol 1e-9")
@@ -101,7 +104,8 @@ def main():
         "slice": a.slice, "interval": [s.lo, s.hi], "dos_estimate": round(s.est, 1),
         "window_est_cap": round(window_estimate(A.n, be.memory(), 1), 1),
         "windows": [vars(w) for w in s.windows], "error": s.error,
-        "found": int(lam.size), "partial": bool(a.max_windows),
+        "found": int(lam.size), "partial": bool(a.max_windows) or bool(s.hit_max_its),
+        "max_its": a.max_its or None,
         "found_vs_estimate": round(lam.size / s.est, 4) if s.est else None,
         "niter": s.niter, "n_A_matvec": s.n_A_matvec, "hit_max_its": s.hit_max_its,
         "max_residual_rel": float(np.max(rr / np.maximum(1.0, np.abs(lam)))) if lam.size else None,
