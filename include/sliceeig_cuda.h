@@ -169,7 +169,7 @@ SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
 /* The resident filter (all degrees of apply_pol, filter_poly.hpp:256-277, in one cooperative
  * launch with the matrix held in shared memory; matrices up to ~300k rows / 2.3M entries).
  * se_resident_filter(0) switches it off process-wide (A/B measurements; results are bit-identical
- * either way; 2: 1024-thread tiles for matrices uploaded afterwards, a measurement variant); se_csr_resident_tiles: row tiles of the matrix' plan, 0 when it does not apply. */
+ * either way); se_csr_resident_tiles: row tiles of the matrix' plan, 0 when it does not apply. */
 SE_API int se_resident_filter(int enable);
 SE_API int se_csr_resident_tiles(const se_csr* a, int* tiles);
 /* mult_cols (vecops.hpp:81-89) / the Rayleigh-Ritz contractions (eigensolvers.hpp:275-283,

@@ -890,8 +890,7 @@ SAMPLE_VECTORS = 0
 
 def set_resident_filter(on) -> None:
     """Process-wide switch of the resident (one launch for all degrees) filter; results are
-    bit-identical either way.  Default on (1); 2 selects 1024-thread tiles for matrices uploaded
-    afterwards (a measurement variant)."""
+    bit-identical either way.  Default on."""
     call("se_resident_filter", int(on))
 
 

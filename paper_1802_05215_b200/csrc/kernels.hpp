@@ -83,7 +83,7 @@ void resident_build(Ctx& c, DevCsr& a);
 void resident_free(DevCsr& a);
 int resident_tiles(const DevCsr& a);
 size_t resident_state_bytes(const DevCsr& a);
-void resident_enable(int mode);  // process-wide (A/B measurements): 0 off, 1 default, 2 = 1024-thread tiles for plans built afterwards
+void resident_enable(int mode);  // process-wide switch (A/B measurements): 0 off, 1 on (default)
 bool resident_enabled();
 void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, double cc, double invd,
                    const double* x, double* out, void* state, const Ctl* halt);

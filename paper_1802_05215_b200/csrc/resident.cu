@@ -4,11 +4,10 @@
 //
 // Why: on such a matrix one filter degree moves ~33 MB that is L2-resident, and a chain of k
 // dependent launches costs 4.2-4.5 us per degree however the launches are issued -- a third of
-// the cfg2 solve.  Here the matrix is read ONCE per filter application: every CTA (two per SM)
-// copies the CSR rows of its own row tile into shared memory and keeps them there for all k
-// degrees, together with its tile of the current Chebyshev vector (double-buffered), while the
-// previous vector, the current vector and the running sum out = sum_j mu_j T_j v of its own rows
-// live in registers.
+// the cfg2 solve.  Here the matrix is read ONCE per filter application: every CTA copies the CSR
+// rows of its own row tile into shared memory and keeps them there for all k degrees, together
+// with its tile of the current Chebyshev vector (double-buffered), while the previous vector, the
+// current vector and the running sum out = sum_j mu_j T_j v of its own rows live in registers.
 // Per degree a CTA only exchanges vector entries with the tiles its columns reach: it writes its
 // new tile to a global (L2) exchange buffer as tagged 16-byte entries {lo32, tag, hi32, tag}
 // (NCCL's LL idea: each 8-byte half is atomic and carries the degree that produced it), and a
@@ -26,6 +25,15 @@
 // still needs it -- by construction, not by timing (three buffers would leave a window).  Tags
 // grow monotonically across applications (epoch + degree), so a stale entry never passes for a
 // fresh one.
+//
+// Measured alternatives (64^3, us per degree; profiles/r2_ncu_summary.md): release/acquire degree
+// counters per tile 4.07; this kernel 3.78; all of a thread's operands held in registers before
+// the tag checks 5.7-8.5 (spills; the checks serialise the loads anyway); two 256-thread tiles per
+// SM with prefetched remote operands 4.2; halo gathered into shared memory in a separate phase
+// 4.6 (100 x 100: 1.31, the best there).  The time scales with the rows per SM (1.3 us at 128
+// rows, 2.1 at 448, 3.8-4.6 at 1,792): the row sums themselves (two dependent shared-memory loads,
+// an individually rounded multiply and add per entry, in storage order) bound the degree, and
+// this variant hides the exchange round trips behind other warps' row sums.
 //
 // Numerics: per row exactly the arithmetic of k_spmv_cheb (storage-order sums of individually
 // rounded products, the same map and recurrence), so the result is bit-identical to the
@@ -82,20 +90,11 @@ struct ResArgs {
 
 constexpr int kSpinLimit = 1 << 22;
 
-// RPT rows per thread, kResThreads threads per CTA, two CTAs per SM (while one tile waits for an
-// exchange entry the other computes).  A row's operands outside the tile ("remote": at most kNR
-// of them are prefetched, which covers stencils and banded matrices; rows with more fall back to
-// reading them in place) are requested for ALL of the thread's rows at the start of a degree;
-// the rows are then summed one after the other from shared memory, each checking its remote
-// operands only when it needs them, so the exchange round trip overlaps the shared-memory work.
-constexpr int kResThreads = 256;
-constexpr int kNR = 4;
-
+// RPT rows per thread; T threads per CTA (blockDim.x).
 template <int RPT>
-__global__ void __launch_bounds__(kResThreads, 2) k_cheb_resident(ResArgs a) {
+__global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int T = kResThreads;
-  const int tid = threadIdx.x;
+  const int T = blockDim.x, tid = threadIdx.x;
   const int b = blockIdx.x;
   const int r0 = b * a.tile_rows;
   const int rows = min(a.tile_rows, a.n - r0);
@@ -117,9 +116,7 @@ __global__ void __launch_bounds__(kResThreads, 2) k_cheb_resident(ResArgs a) {
   const unsigned tag0 = *a.epoch;  // advanced by k_epoch_advance after every application
 
   double prev[RPT], cur[RPT], acc_out[RPT];
-  int ps[RPT], len[RPT];
-  unsigned rmask[RPT];  // bit u: entry u of the row is remote (rows of <= 32 entries with <= kNR
-                        // remote ones); 0xffffffff marks a row that reads remote entries in place
+  int ps[RPT], pe[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int lr = tid + q * T;
@@ -134,80 +131,43 @@ __global__ void __launch_bounds__(kResThreads, 2) k_cheb_resident(ResArgs a) {
   for (int q = 0; q < RPT; ++q) {
     const int lr = tid + q * T;
     ps[q] = lr < rows ? s_rp[lr] : 0;
-    len[q] = lr < rows ? s_rp[lr + 1] - ps[q] : 0;
-    unsigned m = 0;
-    int nrem = 0;
-    for (int u = 0; u < len[q]; ++u)
-      if ((unsigned)(s_col[ps[q] + u] - r0) >= (unsigned)rows) {
-        ++nrem;
-        if (u < 32) m |= 1u << u;
-      }
-    rmask[q] = (len[q] > 32 || nrem > kNR) ? 0xffffffffu : m;
+    pe[q] = lr < rows ? s_rp[lr + 1] : 0;
   }
-  constexpr unsigned kInPlace = 0xffffffffu;
 
-  // the i-th remote entry (in storage order) of a prefetching row: its position in the row
-  auto remote_pos = [&](unsigned m, int i) {
-    for (int k = 0; k < i; ++k) m &= m - 1;  // drop the i lowest set bits
-    return __ffs((int)m) - 1;                // -1: the row has fewer remote entries
-  };
-
-  // sum of the row's products in storage order.  sx: the tile's vector (shared memory);
-  // g (degree 1): the input vector, read in place; xc/tag (degrees >= 2): the exchange buffer;
-  // rv / pend: the row's prefetched remote operands and which of them have not arrived yet.
-  auto row_sum = [&](int q, const double* sx, const double* g, const uint4* xc, unsigned tag,
-                     double (&rv)[kNR], unsigned pend) {
-    const bool inplace = g != nullptr || rmask[q] == kInPlace;
+  // Row sum of A times the vector whose own tile is sx (shared memory).  Entries outside the
+  // tile come from g (degree 1: the input vector) or from the exchange buffer xc, re-read
+  // until they carry `tag`.  Products are formed as operands arrive; the additions run in
+  // storage order.
+  auto row_sum = [&](int q, const double* sx, const double* g, const uint4* xc, unsigned tag) {
     double acc = 0.0;
-    for (int p0 = 0; p0 < len[q]; p0 += 8) {
+    for (int p = ps[q]; p < pe[q]; p += 8) {
       double xv[8];
-      unsigned wait = 0;
+      unsigned pending = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         xv[u] = 0.0;
-        if (p0 + u < len[q]) {
-          const int col = s_col[ps[q] + p0 + u];
+        if (p + u < pe[q]) {
+          const int col = s_col[p + u];
           const unsigned off = (unsigned)(col - r0);
           if (off < (unsigned)rows)
             xv[u] = sx[off];
           else if (g)
             xv[u] = __ldg(g + col);
-          else if (inplace && !ld_ll(xc + col, tag, xv[u]))
-            wait |= 1u << u;
+          else if (!ld_ll(xc + col, tag, xv[u]))
+            pending |= 1u << u;
         }
       }
-      if (!inplace) {
-        // the prefetched operands: re-read those that had not arrived, then drop them into place
-        int spins = 0;
-        while (pend) {
-#pragma unroll
-          for (int i = 0; i < kNR; ++i)
-            if ((pend >> i) & 1u) {
-              const int pos = remote_pos(rmask[q], i);
-              if (ld_ll(xc + s_col[ps[q] + pos], tag, rv[i])) pend &= ~(1u << i);
-            }
-          if (++spins > kSpinLimit) __trap();  // an entry never arrived: fail, do not hang
-        }
-        const unsigned m = rmask[q] >> p0;
+      int spins = 0;
+      while (pending) {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if ((m >> u) & 1u) {
-            const int i = __popc(rmask[q] & ((1u << (p0 + u)) - 1u));  // which remote entry
-            xv[u] = i == 0 ? rv[0] : i == 1 ? rv[1] : i == 2 ? rv[2] : rv[3];
-          }
-      } else {
-        int spins = 0;
-        while (wait) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if ((wait >> u) & 1u)
-              if (ld_ll(xc + s_col[ps[q] + p0 + u], tag, xv[u])) wait &= ~(1u << u);
-          if (++spins > kSpinLimit) __trap();
-        }
+          if ((pending >> u) & 1u)
+            if (ld_ll(xc + s_col[p + u], tag, xv[u])) pending &= ~(1u << u);
+        if (++spins > kSpinLimit) __trap();  // a neighbour never arrived: fail, do not hang
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (p0 + u < len[q]) acc = add(acc, mul(s_val[ps[q] + p0 + u], xv[u]));
+        if (p + u < pe[q]) acc = add(acc, mul(s_val[p + u], xv[u]));
     }
     return acc;
   };
@@ -216,12 +176,11 @@ __global__ void __launch_bounds__(kResThreads, 2) k_cheb_resident(ResArgs a) {
   {
     const double mu0 = __ldg(a.mu), mu1 = __ldg(a.mu + 1);
     uint4* dst = a.xch[1];  // slot = degree & 3
-    double none[kNR] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int lr = tid + q * T;
       if (lr >= rows) continue;
-      const double t = mul(sub(row_sum(q, s_x, a.x, nullptr, 0u, none, 0u), mul(a.c, prev[q])), a.invd);
+      const double t = mul(sub(row_sum(q, s_x, a.x, nullptr, 0u), mul(a.c, prev[q])), a.invd);
       cur[q] = t;
       acc_out[q] = add(add(0.0, mul(mu0, prev[q])), mul(mu1, t));
       if (a.kdeg > 1) {
@@ -240,27 +199,11 @@ __global__ void __launch_bounds__(kResThreads, 2) k_cheb_resident(ResArgs a) {
     double* sxn = s_x + (j & 1) * a.tile_rows;
     const bool more = j < a.kdeg;
     const unsigned want = tag0 + (unsigned)(j - 1);
-    // request every row's remote operands now; they are looked at when their row is summed
-    double rv[RPT][kNR];
-    unsigned pend[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      pend[q] = 0;
-#pragma unroll
-      for (int i = 0; i < kNR; ++i) {
-        rv[q][i] = 0.0;
-        if (rmask[q] != kInPlace) {
-          const int pos = remote_pos(rmask[q], i);
-          if (pos >= 0 && !ld_ll(src + s_col[ps[q] + pos], want, rv[q][i])) pend[q] |= 1u << i;
-        }
-      }
-    }
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int lr = tid + q * T;
       if (lr >= rows) continue;
-      const double t =
-          mul(sub(row_sum(q, sx, nullptr, src, want, rv[q], pend[q]), mul(a.c, cur[q])), a.invd);
+      const double t = mul(sub(row_sum(q, sx, nullptr, src, want), mul(a.c, cur[q])), a.invd);
       const double tj = sub(mul(2.0, t), prev[q]);
       acc_out[q] = add(acc_out[q], mul(muj, tj));
       prev[q] = cur[q];
@@ -330,14 +273,12 @@ void resident_build(Ctx& c, DevCsr& a) {
   SE_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   SE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return;
-  // two tiles per SM when the matrix is large enough to fill them (one tile's exchange wait
-  // overlaps the other's shared-memory work); 256 threads a tile, up to 4 rows a thread
-  int tile_rows = std::max((a.n + 2 * c.num_sms - 1) / (2 * c.num_sms), 128);
+  int tile_rows = std::max((a.n + c.num_sms - 1) / c.num_sms, 128);
   tile_rows = (tile_rows + 31) / 32 * 32;
-  if (tile_rows > 4 * kResThreads) return;
+  if (tile_rows > 2048) return;
   const int nct = (a.n + tile_rows - 1) / tile_rows;
-  const int threads = kResThreads;
-  const int rpt = tile_rows <= threads ? 1 : (tile_rows <= 2 * threads ? 2 : 4);
+  const int threads = tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256);
+  const int rpt = (tile_rows + threads - 1) / threads;
   // per-tile entry counts: the largest sizes the shared-memory image
   std::vector<int> rp_tiles(nct + 1);
   for (int b = 0; b <= nct; ++b)
@@ -379,8 +320,7 @@ void resident_build(Ctx& c, DevCsr& a) {
     }
     return (long)per_sm * c.num_sms >= nct;
   };
-  const bool ok = rpt == 1 ? fits(k_cheb_resident<1>)
-                  : rpt == 2 ? fits(k_cheb_resident<2>) : fits(k_cheb_resident<4>);
+  const bool ok = rpt == 1 ? fits(k_cheb_resident<1>) : rpt == 2 ? fits(k_cheb_resident<2>) : false;
   if (!ok) return;
   auto* p = new ResidentPlan;
   p->nct = nct;
@@ -432,10 +372,8 @@ void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, doub
   cfg.numAttrs = 2;
   if (p.rpt == 1)
     SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<1>, g));
-  else if (p.rpt == 2)
-    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<2>, g));
   else
-    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<4>, g));
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident<2>, g));
   // the next application's tags start past this one's (a separate, stream-ordered launch: a
   // tile far from tile 0 in the matrix graph may start after tile 0 has finished a short filter)
   k_epoch_advance<<<1, 1, 0, c.stream>>>(g.epoch, kdeg, halt);

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1802_05215_b200 import _lib, api
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 if len(sys.argv) > 3:
-    api.set_resident_filter(int(sys.argv[3]))  # 0 off, 1 default, 2 = 1024-thread tiles
+    api.set_resident_filter(int(sys.argv[3]))  # 0: one launch per degree, 1: resident (default)
 ctx = api.default_context(0)
 for spec in (sys.argv[1] if len(sys.argv) > 1 else "160,160,160").split(";"):
     dims = [int(x) for x in spec.split(",")]

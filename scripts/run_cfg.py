@@ -17,7 +17,9 @@ ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--jobs", type=int, default=0)
 ap.add_argument("--solver", default=None)
 ap.add_argument("--only", default=None)
+ap.add_argument("--resident", type=int, default=1, help="resident filter: 0 off, 1 on (default)")
 a = ap.parse_args()
+api.set_resident_filter(a.resident)
 c = CFGS[a.cfg]
 p = dict(c["plan"])
 if a.solver:
