@@ -236,7 +236,12 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
             "kernel": "CGS2 step on the row-major Krylov basis: k_rw_stream T1 + fused MID (N1, "
                       "||t1||, T2) + N2 with their finishing reductions (orth.hpp:63-80, rowgs.cu)",
             "achieved": round(g, 1), "peak": peak, "unit": "GB/s", "frac": round(g / peak, 4),
-            "peak_kind": peak_kind, "traffic": _t("rw_cgs2_step_n262144"),
+            "peak_kind": peak_kind,
+            # ncu capture at k = 1,440 columns (traffic 1.001 x algorithmic), scaled to this shape
+            "traffic": (round(_t("rw_cgs2_step_n262144") * by /
+                              traffic["rw_cgs2_step_n262144"]["algorithmic_bytes"])
+                        if _t("rw_cgs2_step_n262144") else None),
+            "traffic_capture": traffic.get("rw_cgs2_step_n262144"),
             "shape": f"n={n}, k={cfg2_mean_cols} basis columns (mean over the cfg2 run), re-pass forced",
             "us_per_step": round(per * 1e6, 2), "bytes_per_step": by,
             "algorithmic_bytes": "24 n k + 40 n (three reads of W; t read by T1, read+written by MID and N2)",
@@ -259,11 +264,13 @@ def kernel_rooflines(local_gpu: int, dims, cfg2_mean_cols: int):
                              "shape": "160^3, 8 vectors", "achieved": round(out["block"][0], 1),
                              "frac": round(out["block"][0] / peak, 4),
                              "us_per_degree": round(out["block"][1] * 1e6, 2),
-                             "bytes_per_degree": round(out["block"][2])},
+                             "bytes_per_degree": round(out["block"][2]),
+                             "traffic": _t("cheb_ell_block_160cubed_v8")},
             "ritz_gemm": {"kernel": "k_ritz_gemm (DMMA m8n8k4 f64): U = W Y, eigensolvers.hpp:275-283",
                           "bound": "tensor (fp64)", "shape": list(out["gemm"][2]),
                           "achieved_tflops_fp64": round(out["gemm"][0], 1),
-                          "ms": round(out["gemm"][1], 2)},
+                          "ms": round(out["gemm"][1], 2),
+                          "traffic": _t("ritz_gemm_262144x720x2880")},
             "kpm_block_step": {"kernel": "k_kpm_ell (16-probe block, padded rows, doubling; dos.hpp:96-110)",
                                "shape": "160^3 (BASELINE cfg3 matrix), b=16",
                                "achieved": round(out["kpm"][0], 1), "frac": round(out["kpm"][0] / peak, 4),

@@ -172,6 +172,9 @@ SE_API int se_cgs_bench(se_ctx* ctx, int n, int k, int reps, double* ms);
  * either way); se_csr_resident_tiles: row tiles of the matrix' plan, 0 when it does not apply. */
 SE_API int se_resident_filter(int enable);
 SE_API int se_csr_resident_tiles(const se_csr* a, int* tiles);
+/* Shared-memory bytes one tile of the plan holds (0: no plan).  Above half an SM's shared memory a
+ * filter launch owns the GPU while it runs, and a caller solves its slices one at a time. */
+SE_API int se_csr_resident_smem(const se_csr* a, size_t* bytes);
 /* mult_cols (vecops.hpp:81-89) / the Rayleigh-Ritz contractions (eigensolvers.hpp:275-283,
  * 838-871) on the fp64 tensor cores: out (m x n, column-major, ldc) = A B, B[k + col ldb],
  * A[row lda + k] (a_kcontig) or A[row + k lda]; host buffers.  With a or b NULL the operands are

@@ -77,6 +77,7 @@ SIGNATURES = {
     "se_block_filter_bench": [_VP, _VP, C.c_int, C.c_int, _PD],
     "se_resident_filter": [C.c_int],
     "se_csr_resident_tiles": [_VP, _PI],
+    "se_csr_resident_smem": [_VP, C.POINTER(C.c_size_t)],
     "se_mult_cols": [_VP, C.c_int, C.c_int, C.c_int, _PD, C.c_long, C.c_int, _PD, C.c_long, _PD,
                      C.c_long, C.c_int, _PD],
     "se_cgs2_bench": [_VP, C.c_int, C.c_int, C.c_int, C.c_int, _PD],

@@ -901,6 +901,13 @@ def resident_tiles(d) -> int:
     return t.value
 
 
+def resident_tile_smem(d) -> int:
+    """Shared-memory bytes one tile of the resident filter holds (0: no plan)."""
+    b = C.c_size_t()
+    call("se_csr_resident_smem", _dev(d).handle, C.byref(b))
+    return int(b.value)
+
+
 def mult_cols(a: np.ndarray, b: np.ndarray, a_rowmajor: bool = True, ctx=None) -> np.ndarray:
     """out = A @ B on the GPU's fp64 tensor cores (mult_cols vecops.hpp:81-89; the Ritz
     combination U = W Y of eigensolvers.hpp:275-283).  a: (m, k) C-contiguous (the row-major

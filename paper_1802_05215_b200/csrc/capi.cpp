@@ -509,6 +509,13 @@ int se_csr_resident_tiles(const se_csr* a, int* tiles) {
   });
 }
 
+int se_csr_resident_smem(const se_csr* a, size_t* bytes) {
+  return guard([&] {
+    if (!a || !bytes) fail(SE_EINVAL, "se_csr_resident_smem: null argument");
+    *bytes = k::resident_tile_smem(M(a));
+  });
+}
+
 int se_mult_cols(se_ctx* ctx, int m, int n, int k, const double* a, long lda, int a_kcontig,
                  const double* b, long ldb, double* out, long ldc, int reps, double* ms) {
   return guard([&] {

@@ -83,6 +83,7 @@ void resident_build(Ctx& c, DevCsr& a);
 void resident_free(DevCsr& a);
 int resident_tiles(const DevCsr& a);
 size_t resident_state_bytes(const DevCsr& a);
+size_t resident_tile_smem(const DevCsr& a);
 void resident_enable(int mode);  // process-wide switch (A/B measurements): 0 off, 1 on (default)
 bool resident_enabled();
 void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, double cc, double invd,

@@ -222,8 +222,225 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
   }
 }
 
+// ---- padded-row fast path (rows of at most 8 entries: stencils) ----------------------------------
+// ncu on the kernel above (profiles/r2_resident_64.ncu-rep): 253 warp instructions per row, issue
+// slots 48% busy with half the warp slots filled -- it is bound by INSTRUCTIONS (per-entry
+// predicates, the local / input / exchange three-way branch, the retry bookkeeping), not by the
+// exchange.  For matrices whose rows hold at most 8 entries the tile is kept in padded-row form
+// instead (entry-major, s_val[u][row] / s_opi[u][row], so a warp's accesses are consecutive;
+// pad entries have value 0 and the row itself as operand: acc + 0 * x leaves the storage-order
+// sum unchanged), each entry carries the shared-memory index of its operand (>= 0: a row of the
+// tile; < 0: ~halo slot), and the halo -- the previous vector's entries the tile references
+// outside itself, a list fixed by the pattern and built once per matrix -- is gathered into
+// shared memory at the start of a degree: every thread issues its few halo loads back to back
+// (one L2 round trip, not one per entry) and re-reads an entry until it carries the degree's tag.
+// The row sums are then 8 unrolled, unpredicated shared-memory multiply-adds.  Two 512-thread
+// tiles share an SM, so one tile's exchange wait overlaps the other's row sums.
+__device__ __forceinline__ uint4 ld_raw(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ bool ll_ok(const uint4& r, unsigned tag) { return r.y == tag && r.w == tag; }
+__device__ __forceinline__ double ll_value(const uint4& r) { return __hiloint2double((int)r.z, (int)r.x); }
+
+struct EllArgs {
+  int n, tile_rows, kdeg;
+  const int* rp;
+  const int* opi;     // per matrix entry: operand index (>= 0: row of the tile; < 0: ~halo slot)
+  const double* v;
+  const int* hcol;    // per tile: the columns of its halo slots (cap_halo each)
+  const int* hcnt;    // per tile: halo slots in use
+  const double* x;
+  double* out;
+  uint4* xch[4];
+  const double* mu;
+  double c, invd;
+  unsigned* epoch;
+  const Ctl* halt;
+  int cap_halo;
+};
+
+constexpr int kEllR = 8;        // padded row width
+constexpr int kHaloBatch = 4;   // halo loads a thread keeps in flight
+
+template <int RPT>
+__global__ void __launch_bounds__(512, 2) k_cheb_resident_ell(EllArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int b = blockIdx.x;
+  const int TR = a.tile_rows;
+  const int r0 = b * TR;
+  const int rows = min(TR, a.n - r0);
+  double* s_val = reinterpret_cast<double*>(smem_raw);      // [8][TR]
+  double* s_x = s_val + kEllR * TR;                          // [2][TR]
+  double* s_halo = s_x + 2 * TR;                             // [cap_halo]
+  unsigned short* s_opi = reinterpret_cast<unsigned short*>(s_halo + a.cap_halo);  // [8][TR]:
+  // operand index of an entry: < TR a row of the tile, else TR + halo slot
+  // the tile's matrix rows in padded form: independent of the previous kernel
+  for (int lr = tid; lr < rows; lr += T) {
+    const int p0 = __ldg(a.rp + r0 + lr), p1 = __ldg(a.rp + r0 + lr + 1);
+#pragma unroll
+    for (int u = 0; u < kEllR; ++u) {
+      const bool in = p0 + u < p1;
+      s_val[u * TR + lr] = in ? __ldg(a.v + p0 + u) : 0.0;
+      const int oi = in ? __ldg(a.opi + p0 + u) : lr;
+      s_opi[u * TR + lr] = (unsigned short)(oi >= 0 ? oi : TR + ~oi);
+    }
+  }
+  const int hcnt = __ldg(a.hcnt + b);
+  const int* __restrict__ hcol = a.hcol + (size_t)b * a.cap_halo;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (a.halt && a.halt->halted) return;
+  const unsigned tag0 = *a.epoch;
+
+  double prev[RPT], cur[RPT], acc_out[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int lr = tid + q * T;
+    const bool live = lr < rows;
+    prev[q] = live ? __ldg(a.x + r0 + lr) : 0.0;
+    cur[q] = 0.0;
+    acc_out[q] = 0.0;
+    if (live) s_x[lr] = prev[q];
+  }
+  for (int h = tid; h < hcnt; h += T) s_halo[h] = __ldg(a.x + __ldg(hcol + h));  // degree 1's halo
+  __syncthreads();
+
+  auto row_sum = [&](int lr, const double* sx) {
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < kEllR; ++u) {
+      const int oi = s_opi[u * TR + lr];
+      const double* base = oi < TR ? sx : s_halo - TR;
+      acc = add(acc, mul(s_val[u * TR + lr], base[oi]));
+    }
+    return acc;
+  };
+
+  // degree 1   (filter_poly.hpp:260-269)
+  {
+    const double mu0 = __ldg(a.mu), mu1 = __ldg(a.mu + 1);
+    uint4* dst = a.xch[1];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int lr = tid + q * T;
+      if (lr >= rows) continue;
+      const double t = mul(sub(row_sum(lr, s_x), mul(a.c, prev[q])), a.invd);
+      cur[q] = t;
+      acc_out[q] = add(add(0.0, mul(mu0, prev[q])), mul(mu1, t));
+      if (a.kdeg > 1) {
+        st_ll(dst + r0 + lr, t, tag0 + 1u);
+        s_x[TR + lr] = t;
+      }
+    }
+    __syncthreads();
+  }
+  // degrees 2..k   (filter_poly.hpp:270-276)
+  for (int j = 2; j <= a.kdeg; ++j) {
+    const double muj = __ldg(a.mu + j);
+    const uint4* src = a.xch[(j - 1) & 3];
+    uint4* dst = a.xch[j & 3];
+    const double* sx = s_x + ((j - 1) & 1) * TR;
+    double* sxn = s_x + (j & 1) * TR;
+    const bool more = j < a.kdeg;
+    const unsigned want = tag0 + (unsigned)(j - 1);
+    for (int h0 = tid; h0 < hcnt; h0 += kHaloBatch * T) {
+      uint4 raw[kHaloBatch];
+      int col[kHaloBatch];
+#pragma unroll
+      for (int k = 0; k < kHaloBatch; ++k) {
+        const int h = h0 + k * T;
+        col[k] = h < hcnt ? __ldg(hcol + h) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < kHaloBatch; ++k)
+        if (col[k] >= 0) raw[k] = ld_raw(src + col[k]);
+#pragma unroll
+      for (int k = 0; k < kHaloBatch; ++k) {
+        if (col[k] < 0) continue;
+        int spins = 0;
+        while (!ll_ok(raw[k], want)) {
+          raw[k] = ld_raw(src + col[k]);
+          if (++spins > kSpinLimit) __trap();  // an entry never arrived: fail, do not hang
+        }
+        s_halo[h0 + k * T] = ll_value(raw[k]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int lr = tid + q * T;
+      if (lr >= rows) continue;
+      const double t = mul(sub(row_sum(lr, sx), mul(a.c, cur[q])), a.invd);
+      const double tj = sub(mul(2.0, t), prev[q]);
+      acc_out[q] = add(acc_out[q], mul(muj, tj));
+      prev[q] = cur[q];
+      cur[q] = tj;
+      if (more) {
+        st_ll(dst + r0 + lr, tj, want + 1u);
+        sxn[lr] = tj;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int lr = tid + q * T;
+    if (lr < rows) a.out[r0 + lr] = acc_out[q];
+  }
+}
+
+// per matrix entry its operand index; per tile its halo column list (one slot per remote entry)
+__global__ void k_tile_operands(int n, int tile_rows, int cap_halo, const int* __restrict__ rp,
+                                const int* __restrict__ ci, int* __restrict__ opi,
+                                int* __restrict__ hcol, int* __restrict__ hcnt) {
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int r0 = b * tile_rows, r1 = min(n, r0 + tile_rows);
+  for (int p = rp[r0] + threadIdx.x; p < rp[r1]; p += blockDim.x) {
+    const int c = ci[p];
+    if (c >= r0 && c < r1) {
+      opi[p] = c - r0;
+    } else {
+      const int slot = atomicAdd(&s_cnt, 1);
+      if (slot < cap_halo) hcol[(size_t)b * cap_halo + slot] = c;
+      opi[p] = ~slot;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) hcnt[b] = s_cnt;
+}
+
+__global__ void k_tile_remote_count(int n, int tile_rows, const int* __restrict__ rp,
+                                    const int* __restrict__ ci, int* __restrict__ nrem) {
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int r0 = b * tile_rows, r1 = min(n, r0 + tile_rows);
+  int mine = 0;
+  for (int p = rp[r0] + threadIdx.x; p < rp[r1]; p += blockDim.x) {
+    const int c = ci[p];
+    mine += (c < r0 || c >= r1);
+  }
+  atomicAdd(&s_cnt, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) nrem[b] = s_cnt;
+}
+
+size_t ell_smem_bytes(int tile_rows, int cap_halo) {
+  return (size_t)tile_rows * kEllR * 10 + (size_t)tile_rows * 16 + (size_t)cap_halo * 8 + 16;
+}
+
 // per tile: bit t of mask[tile] is set when a row of the tile has an entry in tile t's columns
-constexpr int kMaskWords = 8;  // up to 256 tiles
+constexpr int kMaskWords = 10;  // up to 320 tiles (two per SM)
 __global__ void k_tile_adjacency(int n, int tile_rows, const int* __restrict__ rp,
                                  const int* __restrict__ ci, unsigned* __restrict__ mask) {
   __shared__ unsigned s_m[kMaskWords];
@@ -256,9 +473,20 @@ std::atomic<int> g_resident_mode{1};  // 0 off
 struct ResidentPlan {
   int nct = 0, tile_rows = 0, threads = 0, rpt = 0, cap_nnz = 0;
   size_t smem = 0;
+  // padded-row fast path (rows of <= 8 entries): operand indices and per-tile halo lists
+  bool ell = false;
+  int cap_halo = 0;
+  size_t ell_smem = 0;
+  int* opi = nullptr;   // device, nnz
+  int* hcol = nullptr;  // device, nct x cap_halo
+  int* hcnt = nullptr;  // device, nct
 };
 
 void resident_free(DevCsr& a) {
+  if (!a.resident) return;
+  dev_free_shared(a.resident->opi);
+  dev_free_shared(a.resident->hcol);
+  dev_free_shared(a.resident->hcnt);
   delete a.resident;
   a.resident = nullptr;
 }
@@ -273,11 +501,16 @@ void resident_build(Ctx& c, DevCsr& a) {
   SE_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   SE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return;
-  int tile_rows = std::max((a.n + c.num_sms - 1) / c.num_sms, 128);
+  // padded-row matrices (rows of <= 8 entries) take two 512-thread tiles per SM, others one
+  // tile of up to 1,024 threads
+  const bool want_ell = a.max_row_nnz > 0 && a.max_row_nnz <= kEllR;
+  const int per_sm_tiles = want_ell ? 2 : 1;
+  int tile_rows = std::max((a.n + per_sm_tiles * c.num_sms - 1) / (per_sm_tiles * c.num_sms), 128);
   tile_rows = (tile_rows + 31) / 32 * 32;
-  if (tile_rows > 2048) return;
+  if (tile_rows > (want_ell ? 1024 : 2048)) return;
   const int nct = (a.n + tile_rows - 1) / tile_rows;
-  const int threads = tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256);
+  const int threads = want_ell ? (tile_rows > 256 ? 512 : 256)
+                               : (tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256));
   const int rpt = (tile_rows + threads - 1) / threads;
   // per-tile entry counts: the largest sizes the shared-memory image
   std::vector<int> rp_tiles(nct + 1);
@@ -330,16 +563,104 @@ void resident_build(Ctx& c, DevCsr& a) {
   p->cap_nnz = cap;
   p->smem = smem;
   a.resident = p;
+  // the padded-row fast path, when every row holds at most 8 entries and the image fits
+  if (want_ell) {
+    int* dnrem = dev_alloc<int>(nct);
+    k_tile_remote_count<<<nct, 256, 0, c.stream>>>(a.n, tile_rows, a.rp, a.ci, dnrem);
+    SE_CUDA(cudaGetLastError());
+    ++c.launches;
+    std::vector<int> nrem(nct);
+    SE_CUDA(cudaMemcpyAsync(nrem.data(), dnrem, sizeof(int) * nct, cudaMemcpyDeviceToHost, c.stream));
+    ctx_sync(c);
+    dev_free(dnrem);
+    int cap_halo = 2;
+    for (int v : nrem) cap_halo = std::max(cap_halo, v);
+    cap_halo = (cap_halo + 1) & ~1;
+    const size_t esm = ell_smem_bytes(tile_rows, cap_halo);
+    auto efits = [&](auto kern) {
+      if (esm > (size_t)max_optin || tile_rows + cap_halo > 65535) return false;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, esm) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return (long)per_sm * c.num_sms >= nct;
+    };
+    if (rpt == 1 ? efits(k_cheb_resident_ell<1>) : efits(k_cheb_resident_ell<2>)) {
+      p->opi = dev_alloc_shared<int>((size_t)a.nnz);
+      p->hcol = dev_alloc_shared<int>((size_t)nct * cap_halo);
+      p->hcnt = dev_alloc_shared<int>(nct);
+      k_tile_operands<<<nct, 256, 0, c.stream>>>(a.n, tile_rows, cap_halo, a.rp, a.ci, p->opi, p->hcol,
+                                                 p->hcnt);
+      SE_CUDA(cudaGetLastError());
+      ++c.launches;
+      ctx_sync(c);
+      p->cap_halo = cap_halo;
+      p->ell_smem = esm;
+      p->ell = true;
+    }
+  }
 }
 
 void resident_enable(int mode) { g_resident_mode.store(mode); }
 bool resident_enabled() { return g_resident_mode.load() != 0; }
 int resident_tiles(const DevCsr& a) { return a.resident && resident_enabled() ? a.resident->nct : 0; }
+// Shared memory one tile of the resident filter holds (0: no plan): above half an SM's shared
+// memory two filter launches cannot share the GPU, and slices are then best solved one at a time.
+size_t resident_tile_smem(const DevCsr& a) {
+  if (!a.resident || !resident_enabled()) return 0;
+  return a.resident->ell && g_resident_mode.load() != 2 ? a.resident->ell_smem : a.resident->smem;
+}
 size_t resident_state_bytes(const DevCsr& a) { return 4 * (size_t)a.n * sizeof(uint4) + 16; }
 
 void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, double cc, double invd,
                    const double* x, double* out, void* state, const Ctl* halt) {
   const ResidentPlan& p = *a.resident;
+  if (p.ell && g_resident_mode.load() != 2) {  // mode 2: force the general kernel (A/B timing)
+    EllArgs e{};
+    e.n = a.n;
+    e.tile_rows = p.tile_rows;
+    e.kdeg = kdeg;
+    e.rp = a.rp;
+    e.opi = p.opi;
+    e.v = a.v;
+    e.hcol = p.hcol;
+    e.hcnt = p.hcnt;
+    e.x = x;
+    e.out = out;
+    e.epoch = static_cast<unsigned*>(state);
+    uint4* ex = reinterpret_cast<uint4*>(static_cast<unsigned char*>(state) + 16);
+    for (int q = 0; q < 4; ++q) e.xch[q] = ex + (size_t)q * a.n;
+    e.mu = mu_dev;
+    e.c = cc;
+    e.invd = invd;
+    e.halt = halt;
+    e.cap_halo = p.cap_halo;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.nct);
+    cfg.blockDim = dim3(p.threads);
+    cfg.dynamicSmemBytes = p.ell_smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = c.prio_hi;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (p.rpt == 1)
+      SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident_ell<1>, e));
+    else
+      SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident_ell<2>, e));
+    k_epoch_advance<<<1, 1, 0, c.stream>>>(e.epoch, kdeg, halt);
+    SE_CUDA(cudaGetLastError());
+    c.launches += 2;
+    return;
+  }
   ResArgs g{};
   g.n = a.n;
   g.tile_rows = p.tile_rows;

@@ -335,9 +335,11 @@ class GpuBackend:
         return self.ctx.kernel_launches() + sum(c.kernel_launches() for c in self._thread_ctx.values())
 
     def resident(self) -> bool:
-        """True when the filter runs as one resident cooperative launch per application
-        (resident.cu): such a launch holds every SM, so slices on this GPU run one at a time."""
-        return api.resident_tiles(self.A) > 0
+        """True when a filter application is one resident cooperative launch (resident.cu) whose
+        tiles fill more than half of every SM's shared memory: such a launch owns the GPU while
+        it runs, so this GPU's slices are solved one at a time.  Small matrices (cfg1, the 32^3
+        proxy) leave room for several launches and keep their slices concurrent."""
+        return api.resident_tile_smem(self.A) > 110 * 1024
 
     def memory(self) -> float:
         """Total device memory in bytes (sizes the memory plan's windows)."""
