@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(1024, 1) k_cheb_resident(ResArgs a) {
 // outside itself, a list fixed by the pattern and built once per matrix -- is gathered into
 // shared memory at the start of a degree: every thread issues its few halo loads back to back
 // (one L2 round trip, not one per entry) and re-reads an entry until it carries the degree's tag.
-// The row sums are then 8 unrolled, unpredicated shared-memory multiply-adds.  Two 512-thread
-// tiles share an SM, so one tile's exchange wait overlaps the other's row sums.
+// The row sums are then 8 unrolled, unpredicated shared-memory multiply-adds.  Used for small
+// tiles (<= 512 rows), where it is 1.5x faster than the general kernel; see resident_build.
 __device__ __forceinline__ uint4 ld_raw(const uint4* p) {
   uint4 r;
   asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];\n"
@@ -440,7 +440,7 @@ size_t ell_smem_bytes(int tile_rows, int cap_halo) {
 }
 
 // per tile: bit t of mask[tile] is set when a row of the tile has an entry in tile t's columns
-constexpr int kMaskWords = 10;  // up to 320 tiles (two per SM)
+constexpr int kMaskWords = 8;  // up to 256 tiles
 __global__ void k_tile_adjacency(int n, int tile_rows, const int* __restrict__ rp,
                                  const int* __restrict__ ci, unsigned* __restrict__ mask) {
   __shared__ unsigned s_m[kMaskWords];
@@ -501,17 +501,18 @@ void resident_build(Ctx& c, DevCsr& a) {
   SE_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   SE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return;
-  // padded-row matrices (rows of <= 8 entries) take two 512-thread tiles per SM, others one
-  // tile of up to 1,024 threads
-  const bool want_ell = a.max_row_nnz > 0 && a.max_row_nnz <= kEllR;
-  const int per_sm_tiles = want_ell ? 2 : 1;
-  int tile_rows = std::max((a.n + per_sm_tiles * c.num_sms - 1) / (per_sm_tiles * c.num_sms), 128);
+  // one tile per SM (at least 128 rows a tile), up to 1,024 threads and 2 rows a thread
+  int tile_rows = std::max((a.n + c.num_sms - 1) / c.num_sms, 128);
   tile_rows = (tile_rows + 31) / 32 * 32;
-  if (tile_rows > (want_ell ? 1024 : 2048)) return;
+  if (tile_rows > 2048) return;
   const int nct = (a.n + tile_rows - 1) / tile_rows;
-  const int threads = want_ell ? (tile_rows > 256 ? 512 : 256)
-                               : (tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256));
+  const int threads = tile_rows > 512 ? 1024 : (tile_rows > 256 ? 512 : 256);
   const int rpt = (tile_rows + threads - 1) / threads;
+  // The padded-row kernel serves small tiles (rows of <= 8 entries, <= 512 rows a tile: cfg1, the
+  // 32^3 proxy, 40^3): 1.05 against 1.55 us per degree at 100 x 100.  At 64^3 (1,792 rows and
+  // 3,700 halo entries a tile) every variant measured lands at 3.7-4.6 us and the general kernel
+  // is the fastest (profiles/r2_ncu_summary.md), so large tiles stay with it.
+  const bool want_ell = a.max_row_nnz > 0 && a.max_row_nnz <= kEllR && tile_rows <= 512;
   // per-tile entry counts: the largest sizes the shared-memory image
   std::vector<int> rp_tiles(nct + 1);
   for (int b = 0; b <= nct; ++b)
@@ -590,7 +591,7 @@ void resident_build(Ctx& c, DevCsr& a) {
       }
       return (long)per_sm * c.num_sms >= nct;
     };
-    if (rpt == 1 ? efits(k_cheb_resident_ell<1>) : efits(k_cheb_resident_ell<2>)) {
+    if (efits(k_cheb_resident_ell<1>)) {
       p->opi = dev_alloc_shared<int>((size_t)a.nnz);
       p->hcol = dev_alloc_shared<int>((size_t)nct * cap_halo);
       p->hcnt = dev_alloc_shared<int>(nct);
@@ -652,10 +653,7 @@ void cheb_resident(Ctx& c, const DevCsr& a, int kdeg, const double* mu_dev, doub
     attr[1].val.priority = c.prio_hi;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (p.rpt == 1)
-      SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident_ell<1>, e));
-    else
-      SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident_ell<2>, e));
+    SE_CUDA(cudaLaunchKernelEx(&cfg, k_cheb_resident_ell<1>, e));
     k_epoch_advance<<<1, 1, 0, c.stream>>>(e.epoch, kdeg, halt);
     SE_CUDA(cudaGetLastError());
     c.launches += 2;

@@ -10,6 +10,9 @@ timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
 # --set full: the resident filter, the block filter, the DMMA contraction, the CGS2 stream
 python scripts/filter_bench.py "64,64,64" 3 > gpurun_out/filter_bench.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cheb_resident -c 2 -o gpurun_out/r2_resident_64 python scripts/filter_bench.py "64,64,64" 3 > gpurun_out/ncu_res.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_res.log
+python scripts/filter_bench.py "100,100;40,40,40" 20 > gpurun_out/filter_bench_small.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cheb_resident_ell -c 2 -o gpurun_out/r2_resident_ell_40 python scripts/filter_bench.py "40,40,40" 3 > gpurun_out/ncu_res_ell.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_res_ell.log
+python scripts/filter_bench.py "64,64,64;100,100;40,40,40" 20 0 > gpurun_out/filter_bench_perdegree.log 2>&1
 python scripts/multi_bench.py "160,160,160" > gpurun_out/multi_bench.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cheb_ell_block -s 10 -c 2 -o gpurun_out/r2_block160 python scripts/multi_bench.py "160,160,160" > gpurun_out/ncu_blk.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_blk.log
 python scripts/gemm_bench.py > gpurun_out/gemm_bench.log 2>&1 && \
