@@ -986,9 +986,15 @@ std::unique_ptr<SliceResult> run_tr(Slice& s) {
         else
           trset.push_back({vals[j0 + q], ylast[q], q});
       }
+      // the locking copies read U on the Lanczos stream; the next chunk's evaluation rewrites U
+      // on the high-priority stream, so they must have finished first
+      if (lo > 0) ctx_sync(s.c);
     }
     s.prof[2] += now_s() - tq;
     s.cnt.n_A_matvec += ncand;
+    if (std::getenv("SE_PROFILE"))
+      std::fprintf(stderr, "[se] tr cycle: its %ld steps %d candidates %d in-slice %d locked %d kept %zu (%.1f s)\n",
+                   its, steps, ncand, found, kr.nlock, trset.size(), now_s() - t0);
     if (found == 0) {
       if (++empty_cycles >= 2) break;
     } else {
