@@ -54,7 +54,8 @@ def main():
         _, d = api.mass_scaling(A.n, 1234)
         A.scale_sym(d)
         plan = Plan(xi=1.0, eta=2.0, ns=8, solver="tr", damping="sigma", dos_m=100, dos_nvec=40,
-                    probes="rademacher", tol=1e-8, seed=1234, only=[a.slice], want_vectors=True)
+                    probes="rademacher", tol=1e-8, seed=1234, only=[a.slice], want_vectors=True,
+                    solver_max_its=a.max_its)
         desc = ("cfg5: D A D, A = 128^3 Laplacian, lumped mass uniform [0.5, 1.5] (seed 1234), "
                 "[1, 2] in 8 DOS slices, ChebLanTr tol 1e-8")
     else:
